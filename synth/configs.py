@@ -1,0 +1,249 @@
+"""The five BASELINE.json workloads as seeded synthetic problems.
+
+Seed = 2310_00889 + config index (PCG64 via numpy.random.default_rng).  Every array
+is what the operator takes as input; nothing here evaluates the operator.
+
+  c1  Laplace DL, torus R=1 rho=0.1, 8 x 10 x 12 -> 2x upsampled, T = 960 nodes + 200 points
+  c2  Stokes eta S + D, trefoil (R17) rho(s)=0.05(1+0.3cos 6 pi s), 32 x 10 x 16
+  c3  Stokes, two tori R=1 rho=0.05 at gap 0.0025 (R19), 64 x 12 x 20 each
+  c4  Stokes mobility (K(I-L)+L), 64 random loops in [0,8]^3, 32 x 10 x 12 each
+  c5  Stokes, 512 loops R=1 rho=0.05 in [0,16]^3, 9 x 10 x 12 each (R16); c5alt: 36 panels
+"""
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from .geometry import (Body, torus_body, trefoil_body, discretize, random_rotation,
+                       panel_arclength, centerline_min_distance)
+from .nearlist import build_near_csr
+
+BASE_SEED = 2310_00889
+LAPLACE_DL = 1
+STOKES_SLDL = 2
+
+
+def eta_cfie_input(rho: float) -> float:
+    """CFIE single-layer scaling 1/(2 rho ln(1/rho)) (Eqs. e:laplace-bie-new P:L1750,
+    e:stokes-bie-new P:L1868).  Supplied to BOTH sides as part of the operator's
+    definition (the C library exports its own slb_eta_cfie, tested against this)."""
+    return 1.0 / (2.0 * rho * np.log(1.0 / rho))
+
+
+@dataclass
+class Problem:
+    name: str
+    kernel: int                 # LAPLACE_DL or STOKES_SLDL
+    seed: int
+    Ns: int
+    Nt: int
+    Ms: int
+    Mt: int
+    n_bodies: int
+    panels_per_body: List[int]
+    body_of_panel: np.ndarray   # [P] int32
+    # coarse (Nystrom) grid, layout [panel][i][j]
+    y_c: np.ndarray
+    n_c: np.ndarray
+    w_c: np.ndarray
+    # fine (smooth-quadrature) grid, same panels, layout [panel][m_s][m_t]
+    y_f: np.ndarray
+    n_f: np.ndarray
+    w_f: np.ndarray
+    eta_f: np.ndarray           # [M] CFIE eta of the source's body (0 for Laplace DL)
+    eta_body: np.ndarray        # [n_bodies]
+    x_trg: np.ndarray           # [T,3]; first n_on are the coarse nodes in node order
+    n_on: int
+    c_identity: float
+    sigma: np.ndarray           # [N, sdim] coarse density
+    row_ptr: np.ndarray         # [T+1] int64
+    panel_idx: np.ndarray       # [nnz] int32, ascending per row
+    blk_seed: int
+    s_blk: float
+    projector: bool = False
+    panel_len: Optional[np.ndarray] = None
+    body_center: Optional[np.ndarray] = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def P(self):
+        return int(self.body_of_panel.shape[0])
+
+    @property
+    def sdim(self):
+        return 1 if self.kernel == LAPLACE_DL else 3
+
+    @property
+    def tdim(self):
+        return self.sdim
+
+    @property
+    def Nn(self):
+        return self.Ns * self.Nt
+
+    @property
+    def Mn(self):
+        return self.Ms * self.Mt
+
+    @property
+    def N(self):
+        return self.P * self.Nn
+
+    @property
+    def M(self):
+        return self.P * self.Mn
+
+    @property
+    def T(self):
+        return int(self.x_trg.shape[0])
+
+    @property
+    def nnz(self):
+        return int(self.panel_idx.shape[0])
+
+    @property
+    def block_len(self):
+        return self.tdim * self.Nn * self.sdim
+
+    def pairs(self):
+        return self.T * self.M
+
+
+def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 2),
+              extra_targets=None, c1_rule=False, projector=False, rng=None):
+    Ms, Mt = q[0] * Ns, q[1] * Nt
+    coarse = [discretize(b, P, Ns, Nt) for b, P in zip(bodies, P_per_body)]
+    fine = [discretize(b, P, Ms, Mt) for b, P in zip(bodies, P_per_body)]
+    cat = lambda L, a: np.ascontiguousarray(np.concatenate([getattr(g, a) for g in L], axis=0))
+    y_c, n_c, w_c = cat(coarse, "y"), cat(coarse, "n"), cat(coarse, "w")
+    y_f, n_f, w_f = cat(fine, "y"), cat(fine, "n"), cat(fine, "w")
+    body_of_panel = np.concatenate([np.full(P, b, np.int32) for b, P in enumerate(P_per_body)])
+    Ptot = int(body_of_panel.shape[0])
+    Nn, Mn = Ns * Nt, Ms * Mt
+    if kernel == STOKES_SLDL:
+        eta_body = np.array([eta_cfie_input(b.rho_min) for b in bodies])
+    else:
+        eta_body = np.zeros(len(bodies))
+    eta_f = np.repeat(eta_body[body_of_panel], Mn).astype(np.float64)
+    n_on = y_c.shape[0]
+    x_trg = y_c.copy()
+    if extra_targets is not None:
+        x_trg = np.ascontiguousarray(np.concatenate([x_trg, extra_targets], axis=0))
+    sdim = 1 if kernel == LAPLACE_DL else 3
+    sigma = rng.standard_normal((y_c.shape[0], sdim))
+    L = np.concatenate([panel_arclength(b, P) for b, P in zip(bodies, P_per_body)])
+    ring_xc = cat(coarse, "xc").reshape(Ptot, Ns, Nt, 3)[:, :, 0, :]
+    rho_ring = np.concatenate([np.broadcast_to(b.rho(g.s.reshape(P, Ns, Nt)[:, :, 0]), (P, Ns))
+                               for b, g, P in zip(bodies, coarse, P_per_body)]).reshape(Ptot, Ns)
+    own = np.full(x_trg.shape[0], -1, np.int64)
+    own[:n_on] = np.repeat(np.arange(Ptot), Nn)
+    forced = None
+    if c1_rule:
+        # config 1 node targets: panels {k-1, k, k+1} mod P of their own body (R15)
+        P0 = P_per_body[0]
+        k = np.repeat(np.arange(P0), Nn)
+        forced = np.stack([(k - 1) % P0, k, (k + 1) % P0], axis=1)
+    row_ptr, panel_idx = build_near_csr(x_trg, y_c.reshape(Ptot, Nn, 3), ring_xc, rho_ring, L,
+                                        own, forced_rows=forced)
+    # coincident-pair guard (R14): no target may sit on a fine source
+    _assert_separated(x_trg, y_f)
+    blk_seed = (seed * 0x9E3779B1 + 0xB10C) & ((1 << 64) - 1)
+    s_blk = 1.0 / (Ns * Nt)
+    centers = np.array([b.center for b in bodies])
+    return Problem(name=name, kernel=kernel, seed=seed, Ns=Ns, Nt=Nt, Ms=Ms, Mt=Mt,
+                   n_bodies=len(bodies), panels_per_body=list(P_per_body),
+                   body_of_panel=body_of_panel, y_c=y_c, n_c=n_c, w_c=w_c, y_f=y_f, n_f=n_f,
+                   w_f=w_f, eta_f=eta_f, eta_body=eta_body, x_trg=x_trg, n_on=n_on,
+                   c_identity=0.5, sigma=sigma, row_ptr=row_ptr, panel_idx=panel_idx,
+                   blk_seed=blk_seed, s_blk=s_blk, projector=projector, panel_len=L,
+                   body_center=centers)
+
+
+def _assert_separated(x, y, tol=1e-9):
+    from scipy.spatial import cKDTree
+    d, _ = cKDTree(y).query(x, k=1)
+    assert d.min() > tol, f"target coincides with a fine source (min dist {d.min():.3e})"
+
+
+def _place_loops(rng, n, R_of, rho_of, lo_hi_of, gap_of, max_tries=200000):
+    bodies = []
+    tries = 0
+    while len(bodies) < n:
+        tries += 1
+        if tries > max_tries:
+            raise RuntimeError("loop placement failed")
+        R, rho = R_of(), rho_of()
+        Q = random_rotation(rng)
+        ax = Q[:, 2]
+        half = R * np.sqrt(np.clip(1 - ax ** 2, 0, 1)) + rho
+        lo, hi = lo_hi_of(half)
+        if np.any(hi <= lo):
+            continue
+        c = lo + (hi - lo) * rng.random(3)
+        cand = torus_body(R, rho, c, Q)
+        cand.extra_R = R
+        ok = True
+        for b in bodies:
+            if np.linalg.norm(b.center - c) > R + b.extra_R + rho + b.rho_min + gap_of(rho, b.rho_min):
+                continue
+            d = centerline_min_distance(cand, b)
+            if d - rho - b.rho_min < gap_of(rho, b.rho_min) + 1e-3:
+                ok = False
+                break
+        if ok:
+            bodies.append(cand)
+    return bodies, tries
+
+
+CONFIGS = ("c1", "c2", "c3", "c4", "c5", "c5alt")
+
+
+def make_config(name: str, **kw) -> Problem:
+    """Build one of the BASELINE configs.  Keyword overrides shrink a config for tests
+    (n_loops, panels) while keeping its shape and recipe."""
+    idx = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4, "c5alt": 4}[name]
+    seed = BASE_SEED + idx + kw.pop("seed_offset", 0)
+    rng = np.random.default_rng(seed)
+    if name == "c1":
+        P = kw.get("panels", 8)
+        b = torus_body(1.0, 0.1)
+        nextra = kw.get("n_extra", 200)
+        extra = rng.uniform(-1.5, 1.5, size=(nextra, 3))
+        return _assemble(name, LAPLACE_DL, seed, [b], [P], 10, 12, extra_targets=extra,
+                         c1_rule=True, rng=rng)
+    if name == "c2":
+        P = kw.get("panels", 32)
+        return _assemble(name, STOKES_SLDL, seed, [trefoil_body()], [P], 10, 16, rng=rng)
+    if name == "c3":
+        P = kw.get("panels", 64)
+        rho, gap = 0.05, 0.0025
+        b0 = torus_body(1.0, rho, (0.0, 0.0, 0.0))
+        b1 = torus_body(1.0, rho, (2.0 + 2 * rho + gap, 0.0, 0.0))
+        return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 20, rng=rng)
+    if name == "c4":
+        n = kw.get("n_loops", 64)
+        P = kw.get("panels", 32)
+        box = kw.get("box", 8.0)
+        bodies, tries = _place_loops(
+            rng, n, lambda: rng.uniform(0.8, 1.2), lambda: rng.uniform(0.02, 0.05),
+            lambda half: (half, box - half), lambda ra, rb: 0.5 * min(ra, rb))
+        pr = _assemble(name, STOKES_SLDL, seed, bodies, [P] * n, 10, 12, projector=True, rng=rng)
+        pr.extra["placement_tries"] = tries
+        return pr
+    if name in ("c5", "c5alt"):
+        n = kw.get("n_loops", 512)
+        P = kw.get("panels", 9 if name == "c5" else 36)
+        box = kw.get("box", 16.0)
+        bodies, tries = _place_loops(
+            rng, n, lambda: 1.0, lambda: 0.05,
+            lambda half: (np.full(3, 1.05), np.full(3, box - 1.05)), lambda ra, rb: 0.025)
+        pr = _assemble(name, STOKES_SLDL, seed, bodies, [P] * n, 10, 12, rng=rng)
+        pr.extra["placement_tries"] = tries
+        return pr
+    raise ValueError(name)
+
+
+def pin_torus(R=1.0, rho=0.1, P=256, Ns=10, Nt=48, center=(0.0, 0.0, 0.0), Q=None):
+    """Refined 'pin geometry' (SURVEY §0.6, §8c 'REF'): coarse = fine (q = 1)."""
+    b = torus_body(R, rho, center, Q)
+    return b, discretize(b, P, Ns, Nt)
