@@ -1,0 +1,80 @@
+"""Glue shared by tests and bench.py: turns a seeded synth.Problem into the device inputs
+of one rank's slb_operator (no method arithmetic here: slicing, copying, seeded fill)."""
+import numpy as np
+import torch
+
+from paper_2310_00889_b200 import Operator, partition_panels, slb_fill_blocks
+
+
+def local_rows(pr, rank, nranks):
+    """Global target ids owned by `rank`, the panel range, and n_on_local."""
+    ranges = partition_panels(pr.P, nranks, pr.body_of_panel, whole_bodies=pr.projector)
+    pb, pe = ranges[rank]
+    rows = np.arange(pb * pr.Nn, pe * pr.Nn, dtype=np.int64)
+    if rank == 0 and pr.T > pr.n_on:
+        rows = np.concatenate([rows, np.arange(pr.n_on, pr.T, dtype=np.int64)])
+    return rows, pb, pe, (pe - pb) * pr.Nn, ranges
+
+
+def _segments(rows):
+    """Contiguous runs [a, b) of a sorted-by-construction row list."""
+    if rows.size == 0:
+        return []
+    br = np.nonzero(np.diff(rows) != 1)[0] + 1
+    starts = np.concatenate([[0], br])
+    ends = np.concatenate([br, [rows.size]])
+    return [(int(rows[s]), int(rows[e - 1]) + 1) for s, e in zip(starts, ends)]
+
+
+class DeviceProblem:
+    def __init__(self, pr, rank=0, nranks=1, device="cuda", fold=True, comm=None, blocks=None):
+        self.pr = pr
+        rows, pb, pe, n_on, ranges = local_rows(pr, rank, nranks)
+        self.rows, self.pb, self.pe, self.n_on, self.ranges = rows, pb, pe, n_on, ranges
+        dev = torch.device(device)
+        f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+        rp = pr.row_ptr
+        cnt = rp[rows + 1] - rp[rows]
+        row_ptr = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(cnt, out=row_ptr[1:])
+        segs = _segments(rows)
+        pidx = np.concatenate([pr.panel_idx[rp[a]:rp[b]] for a, b in segs]) if segs else np.zeros(0, np.int32)
+        self.nnz = int(row_ptr[-1])
+        blen = pr.block_len
+        if blocks is None:
+            self.blocks = torch.empty(max(self.nnz * blen, 2), dtype=torch.float64, device=dev)
+            off = 0
+            for a, b in segs:
+                n = int(rp[b] - rp[a]) * blen
+                if n:
+                    slb_fill_blocks(pr.blk_seed, int(rp[a]) * blen, n, pr.s_blk, self.blocks[off:off + n])
+                off += n
+        else:
+            self.blocks = blocks
+        self.x_trg = f64(pr.x_trg[rows])
+        self.y_f, self.n_f, self.w_f = f64(pr.y_f), f64(pr.n_f), f64(pr.w_f)
+        self.eta_f = f64(pr.eta_f) if pr.kernel == 2 else None
+        self.row_ptr = torch.from_numpy(row_ptr).to(dev)
+        self.panel_idx = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
+        sig = pr.sigma.reshape(pr.N, pr.sdim)[pb * pr.Nn:pe * pr.Nn]
+        self.sigma = f64(sig)
+        nb = 0
+        bop = y_c = w_c = None
+        if pr.projector:
+            b_loc = pr.body_of_panel[pb:pe]
+            nb = int(b_loc.max() - b_loc.min() + 1) if b_loc.size else 0
+            bop = torch.from_numpy((b_loc - (b_loc.min() if b_loc.size else 0)).astype(np.int32)).to(dev)
+            y_c = f64(pr.y_c[pb * pr.Nn:pe * pr.Nn])
+            w_c = f64(pr.w_c[pb * pr.Nn:pe * pr.Nn])
+        self.op = Operator(kernel=pr.kernel, ns=pr.Ns, nt=pr.Nt, ms=pr.Ms, mt=pr.Mt, n_panels_global=pr.P,
+                           panel_begin=pb, panel_end=pe, x_trg=self.x_trg, n_on=n_on, y_fine=self.y_f,
+                           n_fine=self.n_f, w_fine=self.w_f, row_ptr=self.row_ptr, panel_idx=self.panel_idx,
+                           blocks=self.blocks, c_identity=pr.c_identity, eta_fine=self.eta_f, eta=0.0,
+                           folded=not fold, n_bodies=nb, body_of_panel=bop, y_coarse=y_c, w_coarse=w_c,
+                           comm=comm)
+
+    def matvec(self, sigma=None, out=None):
+        return self.op.matvec(self.sigma if sigma is None else sigma, out)
+
+    def close(self):
+        self.op.close()

@@ -1,0 +1,201 @@
+/*
+ * slb.h -- C-ABI of the B200-native slender-body Nystrom layer-potential operator apply
+ * (Malhotra & Barnett, arXiv 2310.00889, "Efficient convergent boundary integral methods
+ * for slender bodies").  Implemented by libslb.so (hand-written CUDA for sm_100a + NCCL).
+ *
+ * The operator (PAPER.md line numbers "P:L"):
+ *
+ *   u_t = c_I [t < n_on] sigma'_t                                    identity term
+ *       + sum_m K(x_t - y_m; n_m) w_m (U sigma')_m                    far field, Eq. e:nystrom-no-correction P:L862-872
+ *       + sum_{k in near(t)} E_{t,k} sigma'_k                         local corrections, Eq. e:nystrom-correction P:L935-961
+ *     E_{t,k} = B_{t,k} - sum_{m in fine(k)} K(x_t - y_m; n_m) w_m U_{m,:}
+ *   with sigma' = sigma, or sigma' = (I - L) sigma and + L sigma for the mobility operator
+ *   (K(I-L) + L) (Eq. e:new-mobility-bie P:L2009, projector Eq. L).
+ *
+ *   Kernels (r = x - y, n the outward unit normal at the source):
+ *     Laplace DL   K = (r.n) / (4 pi |r|^3)
+ *     Stokes       K = eta S(r) + D(r; n),
+ *                  S = (1/8pi)(I/|r| + r r^T/|r|^3)                      (Eq. e:stokes-sl P:L538)
+ *                  D = +(3/4pi)(r.n) r r^T/|r|^5                         (Eq. e:stokes-dl P:L551; sign: DESIGN.md R1)
+ *   U = upsampling: P_s (Lagrange, N_s GL -> M_s GL per panel) x F_th (trigonometric,
+ *       N_th -> M_th uniform).  Pairs with r = 0 contribute 0 (R14).
+ *
+ * Conventions for every function:
+ *   - all floating point is fp64; integer index arrays are int64 (row_ptr) / int32 (panel ids);
+ *   - array pointers are DEVICE pointers (except *_host variants and slb_comm ids), row-major,
+ *     contiguous, 16-byte aligned (cudaMalloc / torch allocations satisfy this);
+ *   - the caller owns every array argument; the library never frees caller memory;
+ *   - every call is asynchronous on the given stream and returns after launch; nothing
+ *     throws across the boundary; argument errors return SLB_ERR_INVALID_ARG or
+ *     SLB_ERR_UNSUPPORTED before anything is launched; launch/CUDA errors return
+ *     SLB_ERR_CUDA; asynchronous device faults surface as SLB_ERR_CUDA on a later call;
+ *   - slb_last_error() gives a human-readable message for the last failing call on this thread;
+ *   - node layout: [panel][i (s, GL ascending)][j (theta_j = 2 pi j / N)][component].
+ * Determinism: for fixed inputs every function is bitwise reproducible, and slb_matvec gives
+ * bitwise-identical u for any number of ranks (the per-target summation order depends only
+ * on the global source count M).
+ */
+#ifndef SLB_H
+#define SLB_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLB_ABI_VERSION 1
+
+typedef enum {
+    SLB_OK = 0,
+    SLB_ERR_INVALID_ARG = 1,
+    SLB_ERR_CUDA = 2,
+    SLB_ERR_NCCL = 3,
+    SLB_ERR_OOM = 4,
+    SLB_ERR_UNSUPPORTED = 5
+} slb_status;
+
+typedef enum { SLB_LAPLACE_DL = 1, SLB_STOKES_SLDL = 2 } slb_kernel;
+
+/* Compiled limits (SLB_ERR_UNSUPPORTED beyond them). */
+#define SLB_MAX_NS 32
+#define SLB_MAX_NT 64
+#define SLB_MAX_MS 64
+#define SLB_MAX_MT 128
+
+int slb_abi_version(void);
+const char* slb_last_error(void);
+
+/* CFIE single-layer mixing parameter eta = 1 / (2 rho ln(1/rho)), 0 < rho < 1
+ * (R11).  Returns NaN outside (0,1). Host function. */
+double slb_eta_cfie(double rho);
+
+/* Number of coincident (r == 0) target/source pairs skipped by far-field launches since
+ * the last reset (device counter; synchronises the device).  R14. */
+long long slb_coincident_count(void);
+void slb_coincident_reset(void);
+
+/* Number of kernels this library has launched since it was loaded (launch accounting). */
+unsigned long long slb_launch_count(void);
+
+/* (a) Upsample a density from the coarse Nystrom grid to the fine smooth-quadrature grid,
+ *   sigma_fine[p][a][b][c] = sum_i sum_j P_s[a][i] F_th[b][j] sigma_coarse[p][i][j][c],
+ *   P_s = barycentric Lagrange from the ns GL nodes to the ms GL nodes of [-1,1],
+ *   F_th[b][j] = C_nt(2 pi b / mt - 2 pi j / nt), C_N the real trigonometric cardinal
+ *   function with the Nyquist cosine (R3).  Requires nt, mt even, ms >= 1.
+ *   sigma_coarse: [n_panels][ns][nt][ncomp]; sigma_fine: [n_panels][ms][mt][ncomp] (written). */
+slb_status slb_upsample(int64_t n_panels, int ns, int nt, int ms, int mt, int ncomp,
+                        const double* sigma_coarse, double* sigma_fine, cudaStream_t s);
+
+/* (b) Far field, Laplace double layer, exact all-pairs sum:
+ *   u[t] = sum_m (x_t - y_m).n_m / (4 pi |x_t - y_m|^3) w_m sigma[m].
+ *   x_trg: [n_trg][3]; y, n: [n_src][3]; w, sigma: [n_src]; u: [n_trg] (written). */
+slb_status slb_farfield_laplace_dl(int64_t n_trg, const double* x_trg, int64_t n_src,
+                                   const double* y, const double* n, const double* w,
+                                   const double* sigma, double* u, cudaStream_t s);
+
+/* (b) Far field, Stokes single + double layer, exact all-pairs sum:
+ *   u[t] = sum_m (eta_m S(x_t - y_m) + D(x_t - y_m; n_m)) w_m sigma[m]   (3-vectors).
+ *   eta_src: [n_src] per-source eta (every entry must be > 0; an entry <= 0 poisons the result
+ *   with NaN) or NULL, in which case the scalar eta (>= 0) is used for all sources; eta == 0
+ *   with eta_src == NULL evaluates the pure double layer.  Pure single layer: pass n = zeros.
+ *   sigma: [n_src][3]; u: [n_trg][3] (written). */
+slb_status slb_farfield_stokes_sldl(int64_t n_trg, const double* x_trg, int64_t n_src,
+                                    const double* y, const double* n, const double* w,
+                                    const double* eta_src, double eta, const double* sigma,
+                                    double* u, cudaStream_t s);
+
+/* (c) Near-field correction apply, u[t] += sum_{p in [row_ptr[t], row_ptr[t+1])}
+ *   blocks[p] (tdim x nodes_per_panel*sdim) . sigma_coarse[panel_idx[p]] (nodes_per_panel*sdim).
+ *   row_ptr: [n_trg+1] int64 (monotone, row_ptr[0] = 0); panel_idx: [nnz] int32;
+ *   blocks: [nnz][tdim][nodes_per_panel*sdim]; sigma_coarse: [n_panels][nodes_per_panel][sdim];
+ *   u: [n_trg][tdim] ACCUMULATED.  tdim, sdim in {1,3}; nodes_per_panel*sdim even. */
+slb_status slb_nearcorr_apply(int64_t n_trg, int tdim, int sdim, int nodes_per_panel,
+                              const int64_t* row_ptr, const int32_t* panel_idx,
+                              const double* blocks, const double* sigma_coarse, double* u,
+                              cudaStream_t s);
+
+/* (c, setup) Fold the smooth-rule subtraction into the blocks in place:
+ *   blocks[p] <- blocks[p] - G_{t,k} U_k, G_{t,k}[i][(m,j)] = K_ij(x_t - y_m; n_m) w_m over the
+ *   ms*mt fine nodes m of panel k = panel_idx[p], U_k the per-panel upsampling (as slb_upsample).
+ *   After folding, slb_nearcorr_apply applies E = B - G U (the paper's E).
+ *   kernel: SLB_LAPLACE_DL (tdim = sdim = 1) or SLB_STOKES_SLDL (3); y_fine, n_fine: [M][3],
+ *   w_fine: [M], eta_fine: [M] (Stokes; may be NULL -> eta). */
+slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_trg,
+                             const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
+                             int ms, int mt, const double* y_fine, const double* n_fine,
+                             const double* w_fine, const double* eta_fine, double eta,
+                             double* blocks, cudaStream_t s);
+
+/* Synthetic special-quadrature blocks (input generation, R10):
+ *   blocks[q] = ((2 u_q - 1) sqrt(3)) s_blk,  u_q = (splitmix64(seed, first + q) >> 11) 2^-53,
+ *   q in [0, count).  Bit-identical to the oracle's definition. */
+slb_status slb_fill_blocks(uint64_t seed, uint64_t first, int64_t count, double s_blk,
+                           double* blocks, cudaStream_t s);
+
+/* ---------------- full operator (single- or multi-GPU) ---------------- */
+typedef struct slb_comm slb_comm;
+typedef struct slb_operator slb_operator;
+
+/* NCCL communicator over one process per GPU.  The 128-byte id is created on one rank with
+ * slb_comm_unique_id and broadcast by the caller (e.g. through torch.distributed). */
+slb_status slb_comm_unique_id(unsigned char id[128]);
+slb_status slb_comm_create(const unsigned char id[128], int nranks, int rank, slb_comm** out);
+slb_status slb_comm_destroy(slb_comm* c);
+
+typedef struct {
+    slb_kernel kernel;
+    int ns, nt, ms, mt;
+    int64_t n_panels_global;
+    int64_t panel_begin, panel_end;     /* this rank's source panels [begin, end) */
+    int64_t n_trg_local;                /* local targets */
+    int64_t n_on_local;                 /* first n_on_local local targets = local panels' coarse nodes */
+    double c_identity;                  /* 0.5 for the BIE operator (exterior limit), 0 for potential evaluation */
+    const double* x_trg;                /* [n_trg_local][3] */
+    const double* y_fine;               /* [M][3] global fine nodes, M = n_panels_global*ms*mt */
+    const double* n_fine;               /* [M][3] */
+    const double* w_fine;               /* [M] */
+    const double* eta_fine;             /* [M] (Stokes, entries > 0) or NULL -> eta */
+    double eta;                         /* scalar eta when eta_fine == NULL (0 -> pure DL) */
+    const int64_t* row_ptr;             /* [n_trg_local+1] local CSR */
+    const int32_t* panel_idx;           /* [nnz] GLOBAL panel ids */
+    double* blocks;                     /* [nnz][tdim][ns*nt*sdim]; folded in place at create unless blocks_folded */
+    int blocks_folded;                  /* 1: blocks already hold E = B - G U */
+    /* mobility projector (Eq. L): n_bodies_local = 0 disables.  Bodies must be whole on a rank. */
+    int64_t n_bodies_local;
+    const int32_t* body_of_panel_local; /* [panel_end-panel_begin] local body id, nondecreasing */
+    const double* y_coarse;             /* [local nodes][3] */
+    const double* w_coarse;             /* [local nodes] */
+} slb_operator_desc;
+
+/* Borrows every descriptor pointer (they must outlive the operator); owns only its scratch
+ * and packed source records.  Synchronises the device once (setup). comm NULL -> 1 GPU. */
+slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_operator** out);
+
+/* One operator apply on this rank: sigma_local [local panels][ns][nt][sdim] ->
+ * u_local [n_trg_local][tdim] (written).  Collective across the communicator's ranks. */
+slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s);
+
+/* Same, with HOST buffers: copies sigma in and u out on stream s (pinned memory gives
+ * asynchronous copies), then synchronises s before returning. */
+slb_status slb_matvec_host(slb_operator* op, const double* sigma_local_host, double* u_local_host,
+                           cudaStream_t s);
+
+/* Stage timing of the last slb_matvec (ms, CUDA events on s; -1 if unavailable):
+ * [0] projector+upsample, [1] all-gather, [2] far field, [3] finalize (reduce+near+identity). */
+slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]);
+
+/* Number of kernel launches slb_matvec issues on this rank (for launch accounting). */
+int slb_operator_launches_per_matvec(const slb_operator* op);
+
+slb_status slb_operator_destroy(slb_operator* op);
+
+/* Microbenchmark: sustained FP64 FMA throughput (GFLOP/s, FMA = 2 flops) of this device,
+ * measured with dependent-chain-free DFMA streams over all SMs for ~iters iterations. */
+slb_status slb_bench_dfma(int64_t iters, double* gflops, cudaStream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLB_H */

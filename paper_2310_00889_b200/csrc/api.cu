@@ -1,0 +1,181 @@
+// api.cu -- C-ABI entry points for the stand-alone steps of the operator apply, plus the
+// error/status plumbing shared by the library.  See include/slb.h for the contract.
+#include <cmath>
+#include <string>
+#include "common.cuh"
+
+namespace slb {
+
+static thread_local std::string g_err;
+unsigned long long g_launch_count = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+slb_status check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": " + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SLB_ERR_OOM : SLB_ERR_CUDA;
+    }
+    return SLB_OK;
+}
+
+slb_status check_sticky(const char* what) {
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string(what) + ": pending CUDA error: " + cudaGetErrorString(e));
+        return SLB_ERR_CUDA;
+    }
+    return SLB_OK;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+unsigned long long* coincident_counter() {
+    static unsigned long long* p = nullptr;
+    if (!p) {
+        if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, sizeof(unsigned long long));
+    }
+    return p;
+}
+
+}  // namespace slb
+
+using namespace slb;
+
+extern "C" {
+
+int slb_abi_version(void) { return SLB_ABI_VERSION; }
+
+const char* slb_last_error(void) { return g_err.c_str(); }
+
+double slb_eta_cfie(double rho) {
+    if (!(rho > 0.0 && rho < 1.0)) return NAN;
+    return 1.0 / (2.0 * rho * std::log(1.0 / rho));
+}
+
+long long slb_coincident_count(void) {
+    unsigned long long* p = coincident_counter();
+    if (!p) return -1;
+    unsigned long long v = 0;
+    if (cudaMemcpy(&v, p, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return (long long)v;
+}
+
+void slb_coincident_reset(void) {
+    unsigned long long* p = coincident_counter();
+    if (p) cudaMemset(p, 0, sizeof(unsigned long long));
+}
+
+unsigned long long slb_launch_count(void) { return g_launch_count; }
+
+slb_status slb_upsample(int64_t n_panels, int ns, int nt, int ms, int mt, int ncomp,
+                        const double* sigma_coarse, double* sigma_fine, cudaStream_t s) {
+    SLB_REQUIRE(n_panels >= 0, SLB_ERR_INVALID_ARG, "n_panels < 0");
+    SLB_REQUIRE(ncomp == 1 || ncomp == 3, SLB_ERR_INVALID_ARG, "ncomp must be 1 or 3");
+    SLB_REQUIRE(ns >= 1 && nt >= 2 && ms >= 1 && mt >= 2 && nt % 2 == 0, SLB_ERR_INVALID_ARG,
+                "need ns, ms >= 1 and even nt >= 2");
+    SLB_REQUIRE(ns <= SLB_MAX_NS && nt <= SLB_MAX_NT && ms <= SLB_MAX_MS && mt <= SLB_MAX_MT,
+                SLB_ERR_UNSUPPORTED, "grid beyond compiled limits");
+    if (n_panels == 0) return SLB_OK;
+    SLB_REQUIRE(sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(check_sticky("slb_upsample") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    static InterpParams ip;   // 29 KB: not on the stack
+    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip), SLB_ERR_UNSUPPORTED,
+                "interpolation matrices exceed the kernel-parameter budget (ms*ns + mt*nt <= 3600)");
+    return upsample_launch(FAR_STOKES_SLDL, n_panels, ip, ncomp, sigma_coarse, sigma_fine, nullptr, nullptr, s);
+}
+
+static slb_status farfield_common(FarKind kind, int64_t n_trg, const double* x, int64_t n_src,
+                                  const double* y, const double* n, const double* w,
+                                  const double* eta_src, double eta, const double* sigma, double* u,
+                                  cudaStream_t s) {
+    SLB_REQUIRE(n_trg >= 0 && n_src >= 0, SLB_ERR_INVALID_ARG, "negative size");
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(x && u, SLB_ERR_INVALID_ARG, "null target/output pointer");
+    SLB_REQUIRE(n_src == 0 || (y && n && w && sigma), SLB_ERR_INVALID_ARG, "null source pointer");
+    SLB_REQUIRE(check_sticky("farfield") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    unsigned long long* zc = coincident_counter();
+    SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
+    const int tdim = (kind == FAR_LAPLACE) ? 1 : 3;
+    FarPlan plan = far_plan(n_src);
+    double *geo = nullptr, *sc = nullptr, *dyn = nullptr, *part = nullptr;
+    const int64_t M = n_src > 0 ? n_src : 1;
+    SLB_CUDA(cudaMallocAsync(&geo, sizeof(double) * M * 6, s));
+    SLB_CUDA(cudaMallocAsync(&sc, sizeof(double) * M * 3, s));
+    SLB_CUDA(cudaMallocAsync(&dyn, sizeof(double) * M * 4, s));
+    SLB_CUDA(cudaMallocAsync(&part, sizeof(double) * plan.n_chunks * n_trg * tdim, s));
+    slb_status st = SLB_OK;
+    if (n_src > 0) {
+        if (st == SLB_OK) st = pack_geo(kind, n_src, y, n, eta_src, eta, geo, s);
+        if (st == SLB_OK) st = pack_scale(kind, n_src, n, w, eta_src, eta, sc, s);
+        if (st == SLB_OK) st = pack_dyn(kind, n_src, sc, sigma, dyn, s);
+    }
+    if (st == SLB_OK) st = far_partials(kind, plan, n_trg, x, geo, dyn, part, zc, s);
+    if (st == SLB_OK) st = far_reduce(plan, n_trg, tdim, part, u, s);
+    cudaFreeAsync(geo, s);
+    cudaFreeAsync(sc, s);
+    cudaFreeAsync(dyn, s);
+    cudaFreeAsync(part, s);
+    return st;
+}
+
+slb_status slb_farfield_laplace_dl(int64_t n_trg, const double* x_trg, int64_t n_src, const double* y,
+                                   const double* n, const double* w, const double* sigma, double* u,
+                                   cudaStream_t s) {
+    return farfield_common(FAR_LAPLACE, n_trg, x_trg, n_src, y, n, w, nullptr, 0.0, sigma, u, s);
+}
+
+slb_status slb_farfield_stokes_sldl(int64_t n_trg, const double* x_trg, int64_t n_src, const double* y,
+                                    const double* n, const double* w, const double* eta_src, double eta,
+                                    const double* sigma, double* u, cudaStream_t s) {
+    SLB_REQUIRE(eta_src || eta >= 0.0, SLB_ERR_INVALID_ARG, "scalar eta must be >= 0");
+    FarKind kind = (eta_src || eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL;
+    return farfield_common(kind, n_trg, x_trg, n_src, y, n, w, eta_src, eta, sigma, u, s);
+}
+
+slb_status slb_nearcorr_apply(int64_t n_trg, int tdim, int sdim, int nodes_per_panel,
+                              const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
+                              const double* sigma_coarse, double* u, cudaStream_t s) {
+    SLB_REQUIRE(n_trg >= 0, SLB_ERR_INVALID_ARG, "n_trg < 0");
+    SLB_REQUIRE((tdim == 1 || tdim == 3) && (sdim == 1 || sdim == 3), SLB_ERR_INVALID_ARG,
+                "tdim and sdim must be 1 or 3");
+    SLB_REQUIRE(nodes_per_panel > 0 && (nodes_per_panel * sdim) % 2 == 0, SLB_ERR_INVALID_ARG,
+                "nodes_per_panel*sdim must be positive and even");
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(row_ptr && u, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(check_sticky("slb_nearcorr_apply") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    return near_apply_launch(n_trg, tdim, nodes_per_panel * sdim, row_ptr, panel_idx, blocks,
+                             sigma_coarse, u, s);
+}
+
+slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* row_ptr,
+                             const int32_t* panel_idx, int ns, int nt, int ms, int mt,
+                             const double* y_fine, const double* n_fine, const double* w_fine,
+                             const double* eta_fine, double eta, double* blocks, cudaStream_t s) {
+    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL, SLB_ERR_INVALID_ARG, "bad kernel");
+    SLB_REQUIRE(n_trg >= 0, SLB_ERR_INVALID_ARG, "n_trg < 0");
+    SLB_REQUIRE(ns >= 1 && nt >= 2 && ms >= 1 && mt >= 2 && nt % 2 == 0, SLB_ERR_INVALID_ARG, "bad grid");
+    SLB_REQUIRE(ns <= SLB_MAX_NS && nt <= SLB_MAX_NT && ms <= SLB_MAX_MS && mt <= SLB_MAX_MT,
+                SLB_ERR_UNSUPPORTED, "grid beyond compiled limits");
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(x_trg && row_ptr && y_fine && n_fine && w_fine, SLB_ERR_INVALID_ARG, "null pointer");
+    static InterpParams ip;
+    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip), SLB_ERR_UNSUPPORTED, "interpolation matrices too large");
+    FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE
+                                            : ((eta_fine || eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL);
+    return fold_launch(kind, n_trg, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine, w_fine, eta_fine, eta,
+                       blocks, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// common.cuh -- internal helpers of libslb (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include "../../include/slb.h"
+
+namespace slb {
+
+void set_error(const std::string& msg);
+
+#define SLB_REQUIRE(cond, code, msg)                                   \
+    do {                                                               \
+        if (!(cond)) {                                                 \
+            ::slb::set_error(std::string(__func__) + ": " + (msg));    \
+            return (code);                                             \
+        }                                                              \
+    } while (0)
+
+#define SLB_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            ::slb::set_error(std::string(__func__) + ": " #call ": " +              \
+                             cudaGetErrorString(e_));                               \
+            return e_ == cudaErrorMemoryAllocation ? SLB_ERR_OOM : SLB_ERR_CUDA;    \
+        }                                                                           \
+    } while (0)
+
+// check for launch errors (and sticky asynchronous faults) after a launch
+slb_status check_launch(const char* what);
+slb_status check_sticky(const char* what);
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// ---- host-side interpolation operators (own implementation; shares nothing with oracle/) ----
+// Gauss-Legendre nodes (ascending) and weights on [-1,1].
+void gl_nodes(int n, double* x, double* w);
+// Barycentric Lagrange interpolation matrix from nodes xs[0..nf) to points xt[0..nt): P[m][i].
+void bary_matrix(int nf, const double* xs, int nt, const double* xt, double* P);
+// Trigonometric interpolation matrix F[b][j] = (1/N)[1 + 2 sum_{l=1}^{N/2-1} cos(l d) + cos(N d / 2)],
+// d = 2 pi b / M - 2 pi j / N  (the real interpolant with the Nyquist cosine; N even).
+void trig_matrix(int N, int M, double* F);
+
+// Interpolation matrices passed BY VALUE as a kernel parameter (<= 32 KB param space).
+constexpr int kMaxInterp = 3600;   // doubles: ms*ns + mt*nt
+struct InterpParams {
+    int ns, nt, ms, mt;
+    double v[kMaxInterp];          // P_s [ms][ns] followed by F [mt][nt]
+};
+bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip);
+
+// ---- device helpers ----
+#ifdef __CUDACC__
+__device__ __forceinline__ double rsqrt_mufu(double x) {
+    // raw MUFU.RSQ64H approximation (ftz); refined by the caller
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+
+// 1/sqrt(r2) to ~1 ulp: MUFU seed + one cubic (3rd-order) correction
+//   y = y0 (1 + e/2 + 3 e^2/8),  e = 1 - r2 y0^2.   5 FP64-pipe instructions.
+__device__ __forceinline__ double rsqrt_refined(double r2) {
+    double y0 = rsqrt_mufu(r2);
+    double e = fma(-r2, y0 * y0, 1.0);
+    double p = fma(e, 0.375, 0.5);
+    double ye = y0 * e;
+    return fma(ye, p, y0);
+}
+
+__device__ __forceinline__ bool is_zero_r2(double r2) {
+    // r2 >= 0 always; hi word == 0  <=>  r2 < 2^-1022 (0 or subnormal): coincident pair (R14)
+    return __double2hiint(r2) == 0;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+#endif  // __CUDACC__
+
+// Kernel launch bookkeeping for launch accounting.
+extern unsigned long long g_launch_count;
+
+int num_sms();
+
+// ---- far-field engine (farfield.cu) ----
+enum FarKind { FAR_LAPLACE = 0, FAR_STOKES_SLDL = 1, FAR_STOKES_DL = 2 };
+
+// Summation plan; depends ONLY on the source count M (bitwise determinism across ranks).
+struct FarPlan {
+    int64_t M;
+    int64_t chunk;     // sources per chunk (multiple of 256)
+    int64_t n_chunks;
+    int split;         // warps sharing one target group inside a CTA (1 or 4)
+};
+FarPlan far_plan(int64_t M);
+
+// Packed source records: geo[m] = {y(3), a(3)}, dyn[m] = {d(3), 0}
+//   Laplace:     a unused,              d = w sigma n / (4 pi)
+//   Stokes SLDL: a = (3/(4 pi e)) n,     d = e w sigma,   e = eta/(8 pi)
+//   Stokes DL:   a = (3/(4 pi)) n,       d = w sigma
+slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t n_trg, const double* x_trg,
+                        const double* geo, const double* dyn, double* partials,
+                        unsigned long long* coincident, cudaStream_t s);
+slb_status far_reduce(const FarPlan& plan, int64_t n_trg, int tdim, const double* partials,
+                      double* u, cudaStream_t s);
+unsigned long long* coincident_counter();
+
+// ---- packing kernels (farfield.cu) ----
+slb_status pack_geo(FarKind kind, int64_t M, const double* y, const double* n, const double* eta_src,
+                    double eta, double* geo, cudaStream_t s);
+// per-source scale used by the dyn packing: Stokes -> sc[m] = e_m w_m (SLDL) or w_m (DL), 1 double;
+// Laplace -> sc[m] = w_m n_m / (4 pi), 3 doubles
+slb_status pack_scale(FarKind kind, int64_t M, const double* n, const double* w, const double* eta_src,
+                      double eta, double* sc, cudaStream_t s);
+slb_status pack_dyn(FarKind kind, int64_t M, const double* sc, const double* sigma, double* dyn,
+                    cudaStream_t s);
+
+// ---- upsample (upsample.cu) ----
+// sigma_fine: written as plain values (dyn == nullptr) or packed into dyn records with sc.
+slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int ncomp,
+                           const double* sigma_coarse, double* sigma_fine, const double* sc,
+                           double* dyn, cudaStream_t s);
+
+// ---- near (nearcorr.cu) ----
+slb_status near_apply_launch(int64_t n_trg, int tdim, int cols, const int64_t* row_ptr,
+                             const int32_t* panel_idx, const double* blocks, const double* sigma_c,
+                             double* u, cudaStream_t s);
+// fused finalize: u[t] = sum_c partials[c][t] + near(t) + c_id * sig_loc[t] (t < n_on) + Lsig[t]
+slb_status finalize_launch(const FarPlan& plan, int64_t n_trg, int tdim, int cols,
+                           const double* partials, const int64_t* row_ptr, const int32_t* panel_idx,
+                           const double* blocks, const double* sigma_c_global, int64_t n_on,
+                           double c_id, const double* sig_local, const double* Lsig, double* u,
+                           cudaStream_t s);
+slb_status fold_launch(FarKind kind, int64_t n_trg, const double* x_trg, const int64_t* row_ptr,
+                       const int32_t* panel_idx, const InterpParams& ip, const double* y_fine,
+                       const double* n_fine, const double* w_fine, const double* eta_fine,
+                       double eta, double* blocks, cudaStream_t s);
+
+// ---- projector (projector.cu) ----
+slb_status body_moments_launch(int64_t n_bodies, const int64_t* node_begin, const double* y,
+                               const double* w, double* mom /*[nb][16]*/, cudaStream_t s);
+slb_status proj_launch(int64_t n_bodies, const int64_t* node_begin, const double* y,
+                       const double* w, const double* bodyc /*[nb][16]*/, const double* sigma,
+                       double* coef /*[nb][6]*/, double* sigma_p, double* Lsig,
+                       int64_t max_nodes_per_body, cudaStream_t s);
+
+}  // namespace slb

@@ -1,0 +1,246 @@
+// nearcorr.cu -- (c) block-sparse near-field correction, its setup fold, and the fused
+// finalize of the operator apply.
+//
+// PAPER.md Eq. e:nystrom-correction: u(x) += sum_{k: x in N_k} sum_ij E_ij^(k)(x) sigma_ij,
+// E = (special quadrature) - G w, stored as a sparse matrix
+// "whose product with the current density vector is added to the result of the FMM".
+//
+// Apply: one warp per target row; each lane streams 16-byte slices of the row's blocks
+// (ld.global.cs: evict-first, the blocks are touched once per apply) and reads the matching
+// slices of the coarse density (L2-resident, ld.global.nc); lane partial sums are combined
+// with a fixed xor-butterfly, so the result is deterministic.  HBM-bound: bytes per (t,k) =
+// 8 tdim sdim N_n (+4 index).
+#include <algorithm>
+#include "common.cuh"
+
+namespace slb {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+template <int TD>
+__device__ __forceinline__ void near_row(int64_t t, int cols2, int lane, const int64_t* __restrict__ row_ptr,
+                                         const int32_t* __restrict__ panel_idx,
+                                         const double* __restrict__ blocks,
+                                         const double* __restrict__ sigma_c, double acc[TD]) {
+    const int64_t p0 = row_ptr[t], p1 = row_ptr[t + 1];
+    for (int64_t p = p0; p < p1; ++p) {
+        const int64_t k = panel_idx[p];
+        const double2* B = reinterpret_cast<const double2*>(blocks) + p * TD * cols2;
+        const double2* S = reinterpret_cast<const double2*>(sigma_c) + k * cols2;
+#pragma unroll 3
+        for (int q = lane; q < cols2; q += 32) {
+            double2 s2 = __ldg(S + q);
+#pragma unroll
+            for (int r = 0; r < TD; ++r) {
+                double2 b2 = __ldcs(B + r * cols2 + q);
+                acc[r] = fma(b2.x, s2.x, fma(b2.y, s2.y, acc[r]));
+            }
+        }
+    }
+}
+
+template <int TD>
+__global__ void __launch_bounds__(256)
+near_apply_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
+                  const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
+                  const double* __restrict__ sigma_c, double* __restrict__ u) {
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    double acc[TD];
+#pragma unroll
+    for (int r = 0; r < TD; ++r) acc[r] = 0.0;
+    near_row<TD>(t, cols2, lane, row_ptr, panel_idx, blocks, sigma_c, acc);
+#pragma unroll
+    for (int r = 0; r < TD; ++r) {
+        double v = warp_sum(acc[r]);
+        if (lane == r) u[t * TD + r] += v;
+    }
+}
+
+slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr,
+                             const int32_t* panel_idx, const double* blocks, const double* sigma_c,
+                             double* u, cudaStream_t s) {
+    if (T <= 0) return SLB_OK;
+    const int cols2 = cols / 2;
+    unsigned grid = (unsigned)((T + 7) / 8);
+    if (tdim == 1) near_apply_kernel<1><<<grid, 256, 0, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, u);
+    else near_apply_kernel<3><<<grid, 256, 0, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, u);
+    ++g_launch_count;
+    return check_launch("near_apply_kernel");
+}
+
+// Fused finalize of slb_matvec (one warp per local target):
+//   u[t] = ((sum_c partials[c][t]) + near(t)) + c_id sigma'_t [t < n_on] + (L sigma)_t
+template <int TD>
+__global__ void __launch_bounds__(256)
+finalize_kernel(int64_t T, int64_t n_chunks, int cols2, const double* __restrict__ partials,
+                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
+                const double* __restrict__ blocks, const double* __restrict__ sigma_c,
+                int64_t n_on, double c_id, const double* __restrict__ sig_local,
+                const double* __restrict__ Lsig, double* __restrict__ u) {
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    double far[TD], nr[TD];
+#pragma unroll
+    for (int r = 0; r < TD; ++r) { far[r] = 0.0; nr[r] = 0.0; }
+    for (int64_t c = lane; c < n_chunks; c += 32)
+#pragma unroll
+        for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
+    near_row<TD>(t, cols2, lane, row_ptr, panel_idx, blocks, sigma_c, nr);
+#pragma unroll
+    for (int r = 0; r < TD; ++r) {
+        double f = warp_sum(far[r]);
+        double n = warp_sum(nr[r]);
+        if (lane == r) {
+            double v = f + n;
+            if (t < n_on) {
+                v += c_id * sig_local[t * TD + r];
+                if (Lsig) v += Lsig[t * TD + r];
+            }
+            u[t * TD + r] = v;
+        }
+    }
+}
+
+slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, const double* partials,
+                           const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
+                           const double* sigma_c_global, int64_t n_on, double c_id,
+                           const double* sig_local, const double* Lsig, double* u, cudaStream_t s) {
+    if (T <= 0) return SLB_OK;
+    const int cols2 = cols / 2;
+    unsigned grid = (unsigned)((T + 7) / 8);
+    if (tdim == 1)
+        finalize_kernel<1><<<grid, 256, 0, s>>>(T, plan.n_chunks, cols2, partials, row_ptr, panel_idx, blocks,
+                                                sigma_c_global, n_on, c_id, sig_local, Lsig, u);
+    else
+        finalize_kernel<3><<<grid, 256, 0, s>>>(T, plan.n_chunks, cols2, partials, row_ptr, panel_idx, blocks,
+                                                sigma_c_global, n_on, c_id, sig_local, Lsig, u);
+    ++g_launch_count;
+    return check_launch("finalize_kernel");
+}
+
+// ------------------------------------------------------------------ fold (setup)
+// For each target t (one CTA) and each near panel k = panel_idx[p]:
+//   G[ij][m] = K_ij(x_t - y_m; n_m) w_m over panel k's fine nodes m (K symmetric: 6 entries),
+//   H[ij][a][b] = sum_{mt} G[ij][a][mt] F[mt][b]        (theta adjoint, ms x nt)
+//   blocks[p][i][(a' b) j] -= sum_{a} Ps[a][a'] H[ij][a][b]
+__global__ void __launch_bounds__(128)
+fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ row_ptr,
+            const int32_t* __restrict__ panel_idx, const __grid_constant__ InterpParams ip,
+            const double* __restrict__ y_f, const double* __restrict__ n_f, const double* __restrict__ w_f,
+            const double* __restrict__ eta_f, double eta, double* __restrict__ blocks) {
+    extern __shared__ double sm[];
+    const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
+    const double* Ps = ip.v;
+    const double* F = ip.v + ms * ns;
+    const int Mn = ms * mt, Nn = ns * nt;
+    const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
+    const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
+    double* G = sm;                 // [NG][Mn]
+    double* H = sm + NG * Mn;       // [NG][ms][nt]
+    const int64_t t = blockIdx.x;
+    if (t >= T) return;
+    const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
+    for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
+        const int64_t k = panel_idx[p];
+        for (int q = threadIdx.x; q < Mn; q += blockDim.x) {
+            const int64_t m = k * Mn + q;
+            double r[3] = {x0 - y_f[3 * m], x1 - y_f[3 * m + 1], x2 - y_f[3 * m + 2]};
+            double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+            double nn[3] = {n_f[3 * m], n_f[3 * m + 1], n_f[3 * m + 2]};
+            double w = w_f[m];
+            if (r2 == 0.0) {
+                for (int g = 0; g < NG; ++g) G[g * Mn + q] = 0.0;
+                continue;
+            }
+            double ir = 1.0 / sqrt(r2);
+            double rn = r[0] * nn[0] + r[1] * nn[1] + r[2] * nn[2];
+            if (kind == FAR_LAPLACE) {
+                G[q] = rn * ir * ir * ir / (4.0 * kPi) * w;
+            } else {
+                double e = (kind == FAR_STOKES_SLDL) ? (eta_f ? eta_f[m] : eta) : 0.0;
+                double ir3 = ir * ir * ir;
+                double sl = e / (8.0 * kPi);
+                double dl = 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
+                int g = 0;
+                for (int i = 0; i < 3; ++i)
+                    for (int j = i; j < 3; ++j, ++g) {
+                        double v = sl * ((i == j ? ir : 0.0) + r[i] * r[j] * ir3) + dl * r[i] * r[j];
+                        G[g * Mn + q] = v * w;
+                    }
+            }
+        }
+        __syncthreads();
+        const int nH = NG * ms * nt;
+        for (int q = threadIdx.x; q < nH; q += blockDim.x) {
+            int b = q % nt, a = (q / nt) % ms, g = q / (nt * ms);
+            const double* Gr = G + g * Mn + a * mt;
+            double acc = 0.0;
+            for (int c = 0; c < mt; ++c) acc = fma(Gr[c], F[c * nt + b], acc);
+            H[q] = acc;
+        }
+        __syncthreads();
+        double* Bp = blocks + p * (int64_t)TD * Nn * TD;
+        const int nE = TD * Nn * TD;
+        for (int q = threadIdx.x; q < nE; q += blockDim.x) {
+            int j = q % TD, node = (q / TD) % Nn, i = q / (TD * Nn);
+            int a2 = node / nt, b = node % nt;
+            int lo = i < j ? i : j, hi = i < j ? j : i;
+            int g = (TD == 1) ? 0 : (lo == 0 ? hi : (lo == 1 ? 2 + hi : 5));
+            const double* Hg = H + g * ms * nt;
+            double acc = 0.0;
+            for (int a = 0; a < ms; ++a) acc = fma(Ps[a * ns + a2], Hg[a * nt + b], acc);
+            Bp[q] -= acc;
+        }
+        __syncthreads();
+    }
+}
+
+slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64_t* row_ptr,
+                       const int32_t* panel_idx, const InterpParams& ip, const double* y_fine,
+                       const double* n_fine, const double* w_fine, const double* eta_fine, double eta,
+                       double* blocks, cudaStream_t s) {
+    if (T <= 0) return SLB_OK;
+    SLB_REQUIRE(T <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets for fold");
+    const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
+    size_t smem = sizeof(double) * (size_t)(NG * ip.ms * ip.mt + NG * ip.ms * ip.nt);
+    SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "fold: grid too large for shared memory");
+    SLB_CUDA(cudaFuncSetAttribute(fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fold_kernel<<<(unsigned)T, 128, smem, s>>>((int)kind, T, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine,
+                                              w_fine, eta_fine, eta, blocks);
+    ++g_launch_count;
+    return check_launch("fold_kernel");
+}
+
+// ------------------------------------------------------------------ synthetic blocks
+__global__ void fill_blocks_kernel(uint64_t seed, uint64_t first, int64_t count, double s_blk,
+                                   double* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += stride) {
+        double u01 = (double)(splitmix64(seed, first + (uint64_t)q) >> 11) * (1.0 / 9007199254740992.0);
+        double v = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u01), 1.0), 1.7320508075688772);
+        out[q] = __dmul_rn(v, s_blk);
+    }
+}
+
+}  // namespace slb
+
+using namespace slb;
+
+extern "C" slb_status slb_fill_blocks(uint64_t seed, uint64_t first, int64_t count, double s_blk,
+                                      double* blocks, cudaStream_t s) {
+    SLB_REQUIRE(count >= 0, SLB_ERR_INVALID_ARG, "count < 0");
+    if (count == 0) return SLB_OK;
+    SLB_REQUIRE(blocks, SLB_ERR_INVALID_ARG, "null blocks");
+    int64_t want = (count + 255) / 256;
+    unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)num_sms() * 16);
+    fill_blocks_kernel<<<grid, 256, 0, s>>>(seed, first, count, s_blk, blocks);
+    ++g_launch_count;
+    return check_launch("fill_blocks_kernel");
+}

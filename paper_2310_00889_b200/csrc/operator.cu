@@ -1,0 +1,415 @@
+// operator.cu -- the full operator apply slb_matvec (single GPU or one rank of many) and the
+// NCCL communicator.
+//
+// Per apply on rank r:
+//   [mobility] per-body projector reductions -> sigma' = sigma - L sigma, L sigma   (Eq. L)
+//   upsample local panels, epilogue packs far-field source records into the GLOBAL dyn array
+//   NCCL all-gather (in place) of the fine records + the coarse sigma'          (only exchange step)
+//   far field: local targets x all M fine sources -> per-chunk partials        (Eq. e:nystrom-no-correction)
+//   finalize: partials + folded near blocks E sigma' + c_I sigma' [+ L sigma]  (Eq. e:nystrom-correction,
+//                                                                              P:L1750/1868/2009)
+// NCCL is loaded at run time (dlopen "libnccl.so.2": the copy torch already loaded is reused).
+#include <dlfcn.h>
+#include <nccl.h>
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include "common.cuh"
+
+namespace slb {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char* (*GetErrorString)(ncclResult_t);
+};
+
+static NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+#define LOADSYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    LOADSYM(GetUniqueId, "ncclGetUniqueId");
+    LOADSYM(CommInitRank, "ncclCommInitRank");
+    LOADSYM(CommDestroy, "ncclCommDestroy");
+    LOADSYM(AllGather, "ncclAllGather");
+    LOADSYM(Broadcast, "ncclBroadcast");
+    LOADSYM(GroupStart, "ncclGroupStart");
+    LOADSYM(GroupEnd, "ncclGroupEnd");
+    LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.Broadcast &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString;
+    return api;
+}
+
+#define SLB_NCCL(call)                                                                        \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) {                                                              \
+            ::slb::set_error(std::string(__func__) + ": " #call ": " + nccl().GetErrorString(r_)); \
+            return SLB_ERR_NCCL;                                                              \
+        }                                                                                     \
+    } while (0)
+
+}  // namespace slb
+
+struct slb_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+struct slb_operator {
+    slb_operator_desc d;
+    slb_comm* comm = nullptr;
+    slb::FarKind kind;
+    int tdim = 1, sdim = 1;
+    slb::FarPlan plan;
+    slb::InterpParams ip;
+    int64_t P_loc = 0, N_loc = 0, Nn = 0, Mn = 0, M = 0, cols = 0;
+    std::vector<int64_t> ranges;        // panel offsets of all ranks [R+1]
+    bool equal_shards = true;
+    // device buffers owned by the operator
+    double* geo = nullptr;              // [M][6]
+    double* sc = nullptr;               // local fine scales [M_loc] or [M_loc][3]
+    double* dyn = nullptr;              // [M][4] global fine records
+    double* coarse = nullptr;           // [P_global][Nn][sdim] global sigma'
+    double* partials = nullptr;         // [n_chunks][T_loc][tdim]
+    double* Lsig = nullptr;             // [N_loc][3]
+    int64_t* nb0 = nullptr;             // [nb+1] local node offsets of bodies
+    double* bodyc = nullptr;            // [nb][16]
+    double* coef = nullptr;             // [nb][6]
+    int64_t max_nodes_body = 0;
+    double* sig_dev = nullptr;          // host-variant staging
+    double* u_dev = nullptr;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool timed = false;
+};
+
+using namespace slb;
+
+static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cudaStream_t s) {
+    slb_comm* c = op->comm;
+    if (!c || c->nranks == 1) return SLB_OK;
+    NcclApi& A = nccl();
+    if (op->equal_shards) {
+        size_t cnt = (size_t)((op->ranges[1] - op->ranges[0]) * per_panel);
+        SLB_NCCL(A.AllGather(buf + op->ranges[c->rank] * per_panel, buf, cnt, ncclDouble, c->comm, s));
+    } else {
+        SLB_NCCL(A.GroupStart());
+        for (int r = 0; r < c->nranks; ++r) {
+            size_t cnt = (size_t)((op->ranges[r + 1] - op->ranges[r]) * per_panel);
+            if (cnt == 0) continue;
+            double* p = buf + op->ranges[r] * per_panel;
+            SLB_NCCL(A.Broadcast(p, p, cnt, ncclDouble, r, c->comm, s));
+        }
+        SLB_NCCL(A.GroupEnd());
+    }
+    return SLB_OK;
+}
+
+static void free_op(slb_operator* op) {
+    if (!op) return;
+    cudaFree(op->geo); cudaFree(op->sc); cudaFree(op->dyn); cudaFree(op->coarse);
+    cudaFree(op->partials); cudaFree(op->Lsig); cudaFree(op->nb0); cudaFree(op->bodyc);
+    cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev);
+    for (auto& e : op->ev) if (e) cudaEventDestroy(e);
+    delete op;
+}
+
+extern "C" {
+
+slb_status slb_comm_unique_id(unsigned char id[128]) {
+    SLB_REQUIRE(id, SLB_ERR_INVALID_ARG, "null id");
+    NcclApi& A = nccl();
+    SLB_REQUIRE(A.ok, SLB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    SLB_NCCL(A.GetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+    return SLB_OK;
+}
+
+slb_status slb_comm_create(const unsigned char id[128], int nranks, int rank, slb_comm** out) {
+    SLB_REQUIRE(id && out && nranks >= 1 && rank >= 0 && rank < nranks, SLB_ERR_INVALID_ARG, "bad args");
+    NcclApi& A = nccl();
+    SLB_REQUIRE(A.ok, SLB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    slb_comm* c = new slb_comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclResult_t r = A.CommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+        set_error(std::string("ncclCommInitRank: ") + A.GetErrorString(r));
+        delete c;
+        return SLB_ERR_NCCL;
+    }
+    *out = c;
+    return SLB_OK;
+}
+
+slb_status slb_comm_destroy(slb_comm* c) {
+    if (!c) return SLB_OK;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    delete c;
+    return SLB_OK;
+}
+
+slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_operator** out) {
+    SLB_REQUIRE(d && out, SLB_ERR_INVALID_ARG, "null descriptor/out");
+    *out = nullptr;
+    SLB_REQUIRE(d->kernel == SLB_LAPLACE_DL || d->kernel == SLB_STOKES_SLDL, SLB_ERR_INVALID_ARG, "bad kernel");
+    SLB_REQUIRE(d->ns >= 1 && d->nt >= 2 && d->ms >= 1 && d->mt >= 2 && d->nt % 2 == 0, SLB_ERR_INVALID_ARG,
+                "bad grid");
+    SLB_REQUIRE(d->ns <= SLB_MAX_NS && d->nt <= SLB_MAX_NT && d->ms <= SLB_MAX_MS && d->mt <= SLB_MAX_MT,
+                SLB_ERR_UNSUPPORTED, "grid beyond compiled limits");
+    SLB_REQUIRE(d->n_panels_global >= 1 && d->panel_begin >= 0 && d->panel_end >= d->panel_begin &&
+                    d->panel_end <= d->n_panels_global,
+                SLB_ERR_INVALID_ARG, "bad panel range");
+    const int R = comm ? comm->nranks : 1;
+    SLB_REQUIRE(R > 1 || (d->panel_begin == 0 && d->panel_end == d->n_panels_global), SLB_ERR_INVALID_ARG,
+                "single-GPU operator must own all panels");
+    SLB_REQUIRE(d->n_trg_local >= 0 && d->n_on_local >= 0 && d->n_on_local <= d->n_trg_local,
+                SLB_ERR_INVALID_ARG, "bad target counts");
+    SLB_REQUIRE(d->y_fine && d->n_fine && d->w_fine, SLB_ERR_INVALID_ARG, "null fine geometry");
+    SLB_REQUIRE(d->n_trg_local == 0 || (d->x_trg && d->row_ptr), SLB_ERR_INVALID_ARG, "null targets/CSR");
+    SLB_REQUIRE(check_sticky("slb_operator_create") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+
+    slb_operator* op = new slb_operator;
+    op->d = *d;
+    op->comm = comm;
+    op->sdim = op->tdim = (d->kernel == SLB_LAPLACE_DL) ? 1 : 3;
+    if (d->kernel == SLB_LAPLACE_DL) op->kind = FAR_LAPLACE;
+    else op->kind = (d->eta_fine || d->eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL;
+    if (!make_interp(d->ns, d->nt, d->ms, d->mt, &op->ip)) {
+        delete op;
+        set_error("slb_operator_create: interpolation matrices too large");
+        return SLB_ERR_UNSUPPORTED;
+    }
+    op->Nn = (int64_t)d->ns * d->nt;
+    op->Mn = (int64_t)d->ms * d->mt;
+    op->M = d->n_panels_global * op->Mn;
+    op->P_loc = d->panel_end - d->panel_begin;
+    op->N_loc = op->P_loc * op->Nn;
+    op->cols = op->Nn * op->sdim;
+    op->plan = far_plan(op->M);
+    if (d->n_on_local > op->N_loc) {
+        free_op(op);
+        set_error("slb_operator_create: n_on_local exceeds the local node count");
+        return SLB_ERR_INVALID_ARG;
+    }
+    if (d->n_bodies_local > 0 && op->kind == FAR_LAPLACE) {
+        free_op(op);
+        set_error("slb_operator_create: the projector needs the Stokes kernel");
+        return SLB_ERR_INVALID_ARG;
+    }
+    cudaStream_t s = 0;
+    auto fail = [&](slb_status st) { free_op(op); return st; };
+#define OPCUDA(call)                                                                             \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess) {                                                                 \
+            set_error(std::string("slb_operator_create: " #call ": ") + cudaGetErrorString(e_)); \
+            return fail(e_ == cudaErrorMemoryAllocation ? SLB_ERR_OOM : SLB_ERR_CUDA);           \
+        }                                                                                        \
+    } while (0)
+#define OPST(expr)                          \
+    do {                                    \
+        slb_status st_ = (expr);            \
+        if (st_ != SLB_OK) return fail(st_); \
+    } while (0)
+    // rank panel ranges
+    op->ranges.assign(R + 1, 0);
+    if (R == 1) {
+        op->ranges[1] = d->n_panels_global;
+    } else {
+        int64_t* dr = nullptr;
+        OPCUDA(cudaMalloc(&dr, sizeof(int64_t) * 2 * R));
+        int64_t mine[2] = {d->panel_begin, d->panel_end};
+        OPCUDA(cudaMemcpy(dr + 2 * comm->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
+        ncclResult_t r = nccl().AllGather(dr + 2 * comm->rank, dr, 2, ncclInt64, comm->comm, s);
+        std::vector<int64_t> all(2 * R);
+        cudaError_t e = cudaMemcpy(all.data(), dr, sizeof(int64_t) * 2 * R, cudaMemcpyDeviceToHost);
+        cudaFree(dr);
+        if (r != ncclSuccess || e != cudaSuccess) {
+            set_error("slb_operator_create: gathering panel ranges failed");
+            return fail(r != ncclSuccess ? SLB_ERR_NCCL : SLB_ERR_CUDA);
+        }
+        for (int q = 0; q < R; ++q) {
+            if (all[2 * q] != op->ranges[q]) {
+                set_error("slb_operator_create: rank panel ranges must be contiguous and ordered by rank");
+                return fail(SLB_ERR_INVALID_ARG);
+            }
+            op->ranges[q + 1] = all[2 * q + 1];
+        }
+        if (op->ranges[R] != d->n_panels_global) {
+            set_error("slb_operator_create: rank panel ranges do not cover all panels");
+            return fail(SLB_ERR_INVALID_ARG);
+        }
+        for (int q = 1; q < R; ++q)
+            if (op->ranges[q + 1] - op->ranges[q] != op->ranges[1] - op->ranges[0]) op->equal_shards = false;
+    }
+    const int64_t T = d->n_trg_local;
+    const int64_t Mloc = op->P_loc * op->Mn;
+    OPCUDA(cudaMalloc(&op->geo, sizeof(double) * op->M * 6));
+    OPCUDA(cudaMalloc(&op->sc, sizeof(double) * std::max<int64_t>(Mloc, 1) * 3));
+    OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
+    OPCUDA(cudaMalloc(&op->coarse, sizeof(double) * d->n_panels_global * op->cols));
+    OPCUDA(cudaMalloc(&op->partials, sizeof(double) * std::max<int64_t>(op->plan.n_chunks * T * op->tdim, 1)));
+    OPCUDA(cudaMalloc(&op->sig_dev, sizeof(double) * std::max<int64_t>(op->N_loc * op->sdim, 1)));
+    OPCUDA(cudaMalloc(&op->u_dev, sizeof(double) * std::max<int64_t>(T * op->tdim, 1)));
+    OPCUDA(cudaMemset(op->dyn, 0, sizeof(double) * op->M * 4));
+    OPCUDA(cudaMemset(op->coarse, 0, sizeof(double) * d->n_panels_global * op->cols));
+    const int64_t f0 = d->panel_begin * op->Mn;
+    OPST(pack_geo(op->kind, op->M, d->y_fine, d->n_fine, d->eta_fine, d->eta, op->geo, s));
+    OPST(pack_scale(op->kind, Mloc, d->n_fine + 3 * f0, d->w_fine + f0, d->eta_fine ? d->eta_fine + f0 : nullptr,
+                    d->eta, op->sc, s));
+    if (!d->blocks_folded && T > 0 && d->blocks)
+        OPST(fold_launch(op->kind, T, d->x_trg, d->row_ptr, d->panel_idx, op->ip, d->y_fine, d->n_fine,
+                         d->w_fine, d->eta_fine, d->eta, d->blocks, s));
+    // projector: body node offsets (local), moments, inverse inertia
+    if (d->n_bodies_local > 0) {
+        if (!(d->body_of_panel_local && d->y_coarse && d->w_coarse)) {
+            set_error("slb_operator_create: projector needs body_of_panel_local, y_coarse, w_coarse");
+            return fail(SLB_ERR_INVALID_ARG);
+        }
+        const int64_t nb = d->n_bodies_local;
+        std::vector<int32_t> bop(op->P_loc);
+        OPCUDA(cudaMemcpy(bop.data(), d->body_of_panel_local, sizeof(int32_t) * op->P_loc, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> nb0(nb + 1, 0);
+        for (int64_t p = 0; p < op->P_loc; ++p) {
+            int32_t b = bop[p];
+            if (b < 0 || b >= nb || (p > 0 && b < bop[p - 1])) {
+                set_error("slb_operator_create: body_of_panel_local must be nondecreasing in [0, n_bodies_local)");
+                return fail(SLB_ERR_INVALID_ARG);
+            }
+            nb0[b + 1] += op->Nn;
+        }
+        for (int64_t b = 0; b < nb; ++b) nb0[b + 1] += nb0[b];
+        for (int64_t b = 0; b < nb; ++b) op->max_nodes_body = std::max(op->max_nodes_body, nb0[b + 1] - nb0[b]);
+        OPCUDA(cudaMalloc(&op->nb0, sizeof(int64_t) * (nb + 1)));
+        OPCUDA(cudaMemcpy(op->nb0, nb0.data(), sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice));
+        OPCUDA(cudaMalloc(&op->bodyc, sizeof(double) * nb * 16));
+        OPCUDA(cudaMalloc(&op->coef, sizeof(double) * nb * 6));
+        OPCUDA(cudaMalloc(&op->Lsig, sizeof(double) * std::max<int64_t>(op->N_loc, 1) * 3));
+        OPST(body_moments_launch(nb, op->nb0, d->y_coarse, d->w_coarse, op->bodyc, s));
+        std::vector<double> mom(nb * 16);
+        OPCUDA(cudaMemcpy(mom.data(), op->bodyc, sizeof(double) * nb * 16, cudaMemcpyDeviceToHost));
+        std::vector<double> bc(nb * 16, 0.0);
+        for (int64_t b = 0; b < nb; ++b) {
+            const double* m = &mom[b * 16];
+            double I[3][3] = {{m[4], m[5], m[6]}, {m[5], m[7], m[8]}, {m[6], m[8], m[9]}};
+            double det = I[0][0] * (I[1][1] * I[2][2] - I[1][2] * I[2][1]) -
+                         I[0][1] * (I[1][0] * I[2][2] - I[1][2] * I[2][0]) +
+                         I[0][2] * (I[1][0] * I[2][1] - I[1][1] * I[2][0]);
+            if (!(std::fabs(det) > 0.0) || !(m[0] > 0.0)) {
+                set_error("slb_operator_create: singular body inertia");
+                return fail(SLB_ERR_INVALID_ARG);
+            }
+            double* o = &bc[b * 16];
+            o[0] = m[0]; o[1] = m[1]; o[2] = m[2]; o[3] = m[3];
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+                    // inverse = adj^T / det  (symmetric matrix)
+                    o[4 + 3 * j + i] = (I[i1][j1] * I[i2][j2] - I[i1][j2] * I[i2][j1]) / det;
+                }
+        }
+        OPCUDA(cudaMemcpy(op->bodyc, bc.data(), sizeof(double) * nb * 16, cudaMemcpyHostToDevice));
+    }
+    for (auto& e : op->ev) OPCUDA(cudaEventCreate(&e));
+    OPCUDA(cudaDeviceSynchronize());
+    OPST(check_launch("slb_operator_create"));
+#undef OPCUDA
+#undef OPST
+    *out = op;
+    return SLB_OK;
+}
+
+slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s) {
+    SLB_REQUIRE(op, SLB_ERR_INVALID_ARG, "null operator");
+    SLB_REQUIRE((op->N_loc == 0 || sigma_local) && (op->d.n_trg_local == 0 || u_local), SLB_ERR_INVALID_ARG,
+                "null density/output");
+    SLB_REQUIRE(check_sticky("slb_matvec") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    const slb_operator_desc& d = op->d;
+    unsigned long long* zc = coincident_counter();
+    SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
+    slb_status st;
+    SLB_CUDA(cudaEventRecord(op->ev[0], s));
+    double* sig_p = op->coarse + d.panel_begin * op->cols;   // local sigma' inside the global coarse buffer
+    const double* Lsig = nullptr;
+    if (d.n_bodies_local > 0) {
+        st = proj_launch(d.n_bodies_local, op->nb0, d.y_coarse, d.w_coarse, op->bodyc, sigma_local, op->coef, sig_p,
+                         op->Lsig, op->max_nodes_body, s);
+        if (st != SLB_OK) return st;
+        Lsig = op->Lsig;
+    } else if (op->N_loc > 0) {
+        SLB_CUDA(cudaMemcpyAsync(sig_p, sigma_local, sizeof(double) * op->N_loc * op->sdim, cudaMemcpyDeviceToDevice, s));
+    }
+    st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, sig_p, nullptr, op->sc,
+                         op->dyn + d.panel_begin * op->Mn * 4, s);
+    if (st != SLB_OK) return st;
+    SLB_CUDA(cudaEventRecord(op->ev[1], s));
+    st = allgather(op, op->dyn, op->Mn * 4, s);
+    if (st != SLB_OK) return st;
+    st = allgather(op, op->coarse, op->cols, s);
+    if (st != SLB_OK) return st;
+    SLB_CUDA(cudaEventRecord(op->ev[2], s));
+    st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
+    if (st != SLB_OK) return st;
+    SLB_CUDA(cudaEventRecord(op->ev[3], s));
+    st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
+                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, s);
+    if (st != SLB_OK) return st;
+    SLB_CUDA(cudaEventRecord(op->ev[4], s));
+    op->timed = true;
+    return SLB_OK;
+}
+
+slb_status slb_matvec_host(slb_operator* op, const double* sigma_host, double* u_host, cudaStream_t s) {
+    SLB_REQUIRE(op && sigma_host && u_host, SLB_ERR_INVALID_ARG, "null argument");
+    SLB_CUDA(cudaMemcpyAsync(op->sig_dev, sigma_host, sizeof(double) * op->N_loc * op->sdim, cudaMemcpyHostToDevice, s));
+    slb_status st = slb_matvec(op, op->sig_dev, op->u_dev, s);
+    if (st != SLB_OK) return st;
+    SLB_CUDA(cudaMemcpyAsync(u_host, op->u_dev, sizeof(double) * op->d.n_trg_local * op->tdim,
+                             cudaMemcpyDeviceToHost, s));
+    SLB_CUDA(cudaStreamSynchronize(s));
+    return SLB_OK;
+}
+
+slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]) {
+    SLB_REQUIRE(op && out_ms, SLB_ERR_INVALID_ARG, "null argument");
+    for (int q = 0; q < 4; ++q) out_ms[q] = -1.0f;
+    if (!op->timed) return SLB_OK;
+    SLB_CUDA(cudaEventSynchronize(op->ev[4]));
+    for (int q = 0; q < 4; ++q) SLB_CUDA(cudaEventElapsedTime(&out_ms[q], op->ev[q], op->ev[q + 1]));
+    return SLB_OK;
+}
+
+int slb_operator_launches_per_matvec(const slb_operator* op) {
+    if (!op) return -1;
+    int n = 3;                                   // upsample, far, finalize
+    if (op->d.n_bodies_local > 0) n += 2;        // projector coef + apply
+    return n;
+}
+
+slb_status slb_operator_destroy(slb_operator* op) {
+    free_op(op);
+    return SLB_OK;
+}
+
+}  // extern "C"
