@@ -16,6 +16,7 @@
 // Summation order per target is fixed by (chunk, split), which depend only on M, so results
 // are bitwise identical for any target partition (multi-GPU determinism).
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace slb {
@@ -75,6 +76,7 @@ struct Pair;
 template <>
 struct Pair<FAR_STOKES_SLDL> {
     static constexpr int D = 3;
+    // u += rinv (g + c r),  c = (r.g) rinv^2 (1 + (r.a) rinv^2):  27 FP64-pipe instructions
     __device__ __forceinline__ static void run(const double x[3], const double* g, const double* d,
                                                double acc[3], unsigned& zc) {
         double rx = x[0] - g[0], ry = x[1] - g[1], rz = x[2] - g[2];
@@ -83,15 +85,14 @@ struct Pair<FAR_STOKES_SLDL> {
         bool z = is_zero_r2(r2);
         rinv = z ? 0.0 : rinv;
         zc += z;
-        double rinv2 = rinv * rinv;
+        double s2 = rinv * rinv;
         double rg = fma(rx, d[0], fma(ry, d[1], rz * d[2]));
         double ra = fma(rx, g[3], fma(ry, g[4], rz * g[5]));
-        double rinv3 = rinv * rinv2;
-        double t2 = fma(ra, rinv2, 1.0);
-        double b = (rg * rinv3) * t2;
-        acc[0] = fma(b, rx, fma(rinv, d[0], acc[0]));
-        acc[1] = fma(b, ry, fma(rinv, d[1], acc[1]));
-        acc[2] = fma(b, rz, fma(rinv, d[2], acc[2]));
+        double q = fma(ra, s2, 1.0);
+        double c = (rg * s2) * q;
+        acc[0] = fma(rinv, fma(c, rx, d[0]), acc[0]);
+        acc[1] = fma(rinv, fma(c, ry, d[1]), acc[1]);
+        acc[2] = fma(rinv, fma(c, rz, d[2]), acc[2]);
     }
 };
 
@@ -135,8 +136,8 @@ struct Pair<FAR_LAPLACE> {
 };
 
 // ------------------------------------------------------------------ main kernel
-template <int KIND, int J, int SPLIT>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int KIND, int J, int SPLIT, int MINB, int UNR>
+__global__ void __launch_bounds__(kThreads, MINB)
 far_kernel(int64_t T, const double* __restrict__ x_trg, const double* __restrict__ geo,
            const double* __restrict__ dyn, int64_t M, int64_t chunk, double* __restrict__ partials,
            unsigned long long* __restrict__ coincident) {
@@ -200,7 +201,7 @@ far_kernel(int64_t T, const double* __restrict__ x_trg, const double* __restrict
         const int n = (int)min((int64_t)kTile, m1 - (m0 + (int64_t)i * kTile));
         const double* G = SGEO(st);
         const double* Dy = SDYN(st);
-#pragma unroll 2
+#pragma unroll UNR
         for (int m = sl; m < n; m += SPLIT) {
             double g[6], d[3];
             const double2* g2 = reinterpret_cast<const double2*>(G + m * kGeo);
@@ -251,7 +252,7 @@ far_kernel(int64_t T, const double* __restrict__ x_trg, const double* __restrict
     }
 }
 
-template <int KIND, int J, int SPLIT>
+template <int KIND, int J, int SPLIT, int MINB, int UNR>
 static slb_status launch_far(const FarPlan& plan, int64_t T, const double* x, const double* geo,
                              const double* dyn, double* partials, unsigned long long* zc,
                              cudaStream_t s) {
@@ -259,14 +260,25 @@ static slb_status launch_far(const FarPlan& plan, int64_t T, const double* x, co
     const size_t smem = (size_t)2 * kTile * (kGeo + kDyn) * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        SLB_CUDA(cudaFuncSetAttribute(far_kernel<KIND, J, SPLIT>,
+        SLB_CUDA(cudaFuncSetAttribute(far_kernel<KIND, J, SPLIT, MINB, UNR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     dim3 grid((unsigned)((T + TPC - 1) / TPC), (unsigned)plan.n_chunks);
-    far_kernel<KIND, J, SPLIT><<<grid, kThreads, smem, s>>>(T, x, geo, dyn, plan.M, plan.chunk, partials, zc);
+    far_kernel<KIND, J, SPLIT, MINB, UNR><<<grid, kThreads, smem, s>>>(T, x, geo, dyn, plan.M, plan.chunk,
+                                                                       partials, zc);
     ++g_launch_count;
     return check_launch("far_kernel");
+}
+
+// Tuning variants of the large-M Stokes kernel (selected by SLB_FAR_VARIANT; 0 = default).
+static int far_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("SLB_FAR_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
 }
 
 slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t T, const double* x,
@@ -274,18 +286,27 @@ slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t T, const doub
                         unsigned long long* zc, cudaStream_t s) {
     if (T <= 0) return SLB_OK;
     SLB_REQUIRE(plan.n_chunks <= 65535, SLB_ERR_UNSUPPORTED, "too many source chunks");
-    constexpr int J = 2;
     if (plan.split == 1) {
         switch (kind) {
-            case FAR_LAPLACE: return launch_far<FAR_LAPLACE, J, 1>(plan, T, x, geo, dyn, partials, zc, s);
-            case FAR_STOKES_SLDL: return launch_far<FAR_STOKES_SLDL, J, 1>(plan, T, x, geo, dyn, partials, zc, s);
-            case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, J, 1>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_LAPLACE: return launch_far<FAR_LAPLACE, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_STOKES_SLDL:
+                switch (far_variant()) {
+                    case 1: return launch_far<FAR_STOKES_SLDL, 2, 1, 3, 2>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 2: return launch_far<FAR_STOKES_SLDL, 4, 1, 1, 1>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 3: return launch_far<FAR_STOKES_SLDL, 4, 1, 2, 1>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 4: return launch_far<FAR_STOKES_SLDL, 1, 1, 4, 4>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 5: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 4>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 6: return launch_far<FAR_STOKES_SLDL, 1, 1, 3, 4>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 7: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 1>(plan, T, x, geo, dyn, partials, zc, s);
+                    default: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+                }
         }
     } else {
         switch (kind) {
-            case FAR_LAPLACE: return launch_far<FAR_LAPLACE, J, 4>(plan, T, x, geo, dyn, partials, zc, s);
-            case FAR_STOKES_SLDL: return launch_far<FAR_STOKES_SLDL, J, 4>(plan, T, x, geo, dyn, partials, zc, s);
-            case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, J, 4>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_LAPLACE: return launch_far<FAR_LAPLACE, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_STOKES_SLDL: return launch_far<FAR_STOKES_SLDL, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
         }
     }
     set_error("far_partials: bad kind");
