@@ -21,108 +21,139 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int TD>
-__device__ __forceinline__ void near_row(int64_t t, int cols2, int lane, const int64_t* __restrict__ row_ptr,
-                                         const int32_t* __restrict__ panel_idx,
-                                         const double* __restrict__ blocks,
-                                         const double* __restrict__ sigma_c, double acc[TD]) {
-    const int64_t p0 = row_ptr[t], p1 = row_ptr[t + 1];
-    for (int64_t p = p0; p < p1; ++p) {
-        const int64_t k = panel_idx[p];
-        const double2* B = reinterpret_cast<const double2*>(blocks) + p * TD * cols2;
-        const double2* S = reinterpret_cast<const double2*>(sigma_c) + k * cols2;
-#pragma unroll 3
-        for (int q = lane; q < cols2; q += 32) {
-            double2 s2 = __ldg(S + q);
-#pragma unroll
-            for (int r = 0; r < TD; ++r) {
-                double2 b2 = __ldcs(B + r * cols2 + q);
-                acc[r] = fma(b2.x, s2.x, fma(b2.y, s2.y, acc[r]));
-            }
+// Streaming near apply (B200): one warp per target row; the row's blocks (t_dim x cols doubles,
+// contiguous) are pulled into a per-warp STG-deep shared-memory ring by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) issued by lane 0, so several KB per warp are in flight
+// with no per-thread address arithmetic; lanes then read the slot (LDS.128) against sigma'_k
+// (L2-resident, ld.global.nc).  Lane partials are combined with a fixed xor butterfly.
+//   MODE 0 (slb_nearcorr_apply):  u[t] += near(t)
+//   MODE 1 (slb_matvec finalize): u[t]  = (sum_c partials[c][t] + near(t)) + c_id sigma'_t [t < n_on] + (L sigma)_t
+constexpr int kNearStages = 3;
+
+template <int TD, int MODE>
+__global__ void __launch_bounds__(128)
+near_stream_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
+                   const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
+                   const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
+                   int64_t n_on, double c_id, const double* __restrict__ sig_local,
+                   const double* __restrict__ Lsig, double* __restrict__ u) {
+    extern __shared__ __align__(128) double2 ring[];      // [warps][STG][TD*cols2]
+    __shared__ __align__(8) uint64_t bars[4 * kNearStages];
+    const int nw = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int slot = TD * cols2;                          // double2 per block
+    const uint32_t bytes = (uint32_t)slot * 16u;
+    double2* myring = ring + (size_t)w * kNearStages * slot;
+    uint64_t* mybar = bars + w * kNearStages;
+    const int64_t t = (int64_t)blockIdx.x * nw + w;
+    const bool active = t < T;
+    if (lane == 0) {
+        for (int q = 0; q < kNearStages; ++q) mbar_init(&mybar[q], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (!active) return;
+    const int64_t p0 = row_ptr[t], nb = row_ptr[t + 1] - p0;
+    const double2* B = reinterpret_cast<const double2*>(blocks);
+    if (lane == 0) {
+        for (int q = 0; q < kNearStages && q < nb; ++q) {
+            mbar_expect_tx(&mybar[q], bytes);
+            bulk_g2s(myring + (size_t)q * slot, B + (p0 + q) * slot, bytes, &mybar[q]);
         }
     }
-}
-
-template <int TD>
-__global__ void __launch_bounds__(256)
-near_apply_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
-                  const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
-                  const double* __restrict__ sigma_c, double* __restrict__ u) {
-    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (t >= T) return;
     double acc[TD];
 #pragma unroll
     for (int r = 0; r < TD; ++r) acc[r] = 0.0;
-    near_row<TD>(t, cols2, lane, row_ptr, panel_idx, blocks, sigma_c, acc);
+    const double2* S2 = reinterpret_cast<const double2*>(sigma_c);
+    for (int64_t i = 0; i < nb; ++i) {
+        const int st = (int)(i % kNearStages);
+        const int64_t k = panel_idx[p0 + i];
+        const double2* Sk = S2 + k * cols2;
+        mbar_wait(&mybar[st], (uint32_t)((i / kNearStages) & 1));
+        const double2* R = myring + (size_t)st * slot;
+#pragma unroll 2
+        for (int c = lane; c < cols2; c += 32) {
+            const double2 sv = __ldg(Sk + c);
 #pragma unroll
-    for (int r = 0; r < TD; ++r) {
-        double v = warp_sum(acc[r]);
-        if (lane == r) u[t * TD + r] += v;
-    }
-}
-
-slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr,
-                             const int32_t* panel_idx, const double* blocks, const double* sigma_c,
-                             double* u, cudaStream_t s) {
-    if (T <= 0) return SLB_OK;
-    const int cols2 = cols / 2;
-    unsigned grid = (unsigned)((T + 7) / 8);
-    if (tdim == 1) near_apply_kernel<1><<<grid, 256, 0, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, u);
-    else near_apply_kernel<3><<<grid, 256, 0, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, u);
-    ++g_launch_count;
-    return check_launch("near_apply_kernel");
-}
-
-// Fused finalize of slb_matvec (one warp per local target):
-//   u[t] = ((sum_c partials[c][t]) + near(t)) + c_id sigma'_t [t < n_on] + (L sigma)_t
-template <int TD>
-__global__ void __launch_bounds__(256)
-finalize_kernel(int64_t T, int64_t n_chunks, int cols2, const double* __restrict__ partials,
-                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
-                const double* __restrict__ blocks, const double* __restrict__ sigma_c,
-                int64_t n_on, double c_id, const double* __restrict__ sig_local,
-                const double* __restrict__ Lsig, double* __restrict__ u) {
-    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (t >= T) return;
-    double far[TD], nr[TD];
-#pragma unroll
-    for (int r = 0; r < TD; ++r) { far[r] = 0.0; nr[r] = 0.0; }
-    for (int64_t c = lane; c < n_chunks; c += 32)
-#pragma unroll
-        for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
-    near_row<TD>(t, cols2, lane, row_ptr, panel_idx, blocks, sigma_c, nr);
-#pragma unroll
-    for (int r = 0; r < TD; ++r) {
-        double f = warp_sum(far[r]);
-        double n = warp_sum(nr[r]);
-        if (lane == r) {
-            double v = f + n;
-            if (t < n_on) {
-                v += c_id * sig_local[t * TD + r];
-                if (Lsig) v += Lsig[t * TD + r];
+            for (int r = 0; r < TD; ++r) {
+                const double2 bv = R[r * cols2 + c];
+                acc[r] = fma(bv.x, sv.x, fma(bv.y, sv.y, acc[r]));
             }
-            u[t * TD + r] = v;
+        }
+        __syncwarp();
+        if (lane == 0 && i + kNearStages < nb) {
+            fence_proxy_async_smem();
+            mbar_expect_tx(&mybar[st], bytes);
+            bulk_g2s(myring + (size_t)st * slot, B + (p0 + i + kNearStages) * slot, bytes, &mybar[st]);
         }
     }
+    double far[TD];
+#pragma unroll
+    for (int r = 0; r < TD; ++r) far[r] = 0.0;
+    if (MODE == 1)
+        for (int64_t c = lane; c < n_chunks; c += 32)
+#pragma unroll
+            for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
+#pragma unroll
+    for (int r = 0; r < TD; ++r) {
+        const double nv = warp_sum(acc[r]);
+        const double fv = MODE == 1 ? warp_sum(far[r]) : 0.0;
+        if (lane == r) {
+            if (MODE == 0) {
+                u[t * TD + r] += nv;
+            } else {
+                double v = fv + nv;
+                if (t < n_on) {
+                    v += c_id * sig_local[t * TD + r];
+                    if (Lsig) v += Lsig[t * TD + r];
+                }
+                u[t * TD + r] = v;
+            }
+        }
+    }
+}
+
+static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, const int64_t* row_ptr,
+                                     const int32_t* panel_idx, const double* blocks, const double* sigma_c,
+                                     const double* partials, int64_t n_chunks, int64_t n_on, double c_id,
+                                     const double* sig_local, const double* Lsig, double* u, cudaStream_t s) {
+    if (T <= 0) return SLB_OK;
+    const int cols2 = cols / 2;
+    const size_t per_warp = (size_t)kNearStages * tdim * cols2 * 16;
+    int nw = 4;
+    while (nw > 1 && per_warp * nw > 200 * 1024) nw >>= 1;
+    SLB_REQUIRE(per_warp * nw <= 227 * 1024, SLB_ERR_UNSUPPORTED, "near blocks too large for the smem ring");
+    const size_t smem = per_warp * nw;
+    const unsigned grid = (unsigned)((T + nw - 1) / nw);
+#define NEAR_LAUNCH(TD, MODE)                                                                               \
+    do {                                                                                                    \
+        SLB_CUDA(cudaFuncSetAttribute(near_stream_kernel<TD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                      (int)smem));                                                          \
+        near_stream_kernel<TD, MODE><<<grid, nw * 32, smem, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, \
+                                                                 partials, n_chunks, n_on, c_id, sig_local, Lsig, u); \
+    } while (0)
+    if (tdim == 1) {
+        if (mode == 0) NEAR_LAUNCH(1, 0); else NEAR_LAUNCH(1, 1);
+    } else {
+        if (mode == 0) NEAR_LAUNCH(3, 0); else NEAR_LAUNCH(3, 1);
+    }
+#undef NEAR_LAUNCH
+    ++g_launch_count;
+    return check_launch("near_stream_kernel");
+}
+
+slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr, const int32_t* panel_idx,
+                             const double* blocks, const double* sigma_c, double* u, cudaStream_t s) {
+    return near_stream_launch(0, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c, nullptr, 0, 0, 0.0, nullptr,
+                              nullptr, u, s);
 }
 
 slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, const double* partials,
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
-                           const double* sigma_c_global, int64_t n_on, double c_id,
-                           const double* sig_local, const double* Lsig, double* u, cudaStream_t s) {
-    if (T <= 0) return SLB_OK;
-    const int cols2 = cols / 2;
-    unsigned grid = (unsigned)((T + 7) / 8);
-    if (tdim == 1)
-        finalize_kernel<1><<<grid, 256, 0, s>>>(T, plan.n_chunks, cols2, partials, row_ptr, panel_idx, blocks,
-                                                sigma_c_global, n_on, c_id, sig_local, Lsig, u);
-    else
-        finalize_kernel<3><<<grid, 256, 0, s>>>(T, plan.n_chunks, cols2, partials, row_ptr, panel_idx, blocks,
-                                                sigma_c_global, n_on, c_id, sig_local, Lsig, u);
-    ++g_launch_count;
-    return check_launch("finalize_kernel");
+                           const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
+                           const double* Lsig, double* u, cudaStream_t s) {
+    return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
+                              n_on, c_id, sig_local, Lsig, u, s);
 }
 
 // ------------------------------------------------------------------ fold (setup)
