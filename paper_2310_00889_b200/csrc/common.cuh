@@ -148,6 +148,13 @@ slb_status far_reduce(const FarPlan& plan, int64_t n_trg, int tdim, const double
                       double* u, cudaStream_t s);
 unsigned long long* coincident_counter();
 
+// ---- constant-bank far field (farconst.cu) ----
+slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
+                           double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
+                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches);
+slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s);
+int far_const_bufs();
+
 // ---- packing kernels (farfield.cu) ----
 slb_status pack_geo(FarKind kind, int64_t M, const double* y, const double* n, const double* eta_src,
                     double eta, double* geo, cudaStream_t s);

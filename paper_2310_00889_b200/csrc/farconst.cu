@@ -1,0 +1,192 @@
+// farconst.cu -- far field for the operator apply with source tiles in the CONSTANT bank.
+//
+// Why (measured): on sm_100a an FP64 instruction whose three source
+// operands are distinct vector registers occupies the FP64 pipe for 3 cycles instead of 2
+// (tools/rf_probe.cu).  In the N-body pair every source value (y, a, g) is warp-uniform; read
+// from shared memory it lands in vector registers and ~8 of the 27 FP64 instructions per pair
+// pay the third cycle (tools/sass_cost.py).  Read from the constant bank with a uniform index it
+// is loaded by LDCU into UNIFORM registers, which are free operands: the modelled pair cost drops
+// from 61 to 55 cycles per warp and the measured pair rate rises ~8% (tools/const_probe.cu).
+//
+// Structure: the packed source records rec[m] = {y(3), a(3), g(3), 0} (80 B) are split into
+// tiles of kConstTile = 200 sources.  Tile i is copied (D2D, stream-ordered) into constant buffer
+// i % 4 and processed by a launch on internal stream i % 4 over ALL local targets; stream s
+// accumulates its tiles s, s+4, s+8, ... into its own partial array, so the summation order per
+// target depends only on M and the four kernels in flight hide each other's tails.  The whole
+// sequence is captured once into a CUDA graph per operator and replayed per apply.
+#include <cuda_runtime.h>
+#include <cstdlib>
+#include <vector>
+#include "common.cuh"
+
+namespace slb {
+
+constexpr int kConstTile = 200;          // sources per constant buffer (200 x 80 B = 16 KB)
+constexpr int kConstBufs = 4;            // buffers = streams = partial arrays
+constexpr int kRec = 10;                 // doubles per packed record
+constexpr int kConstThreads = 128;
+
+__constant__ double c_rec[kConstBufs][kConstTile * kRec];
+
+template <int KIND, int J>
+__device__ __forceinline__ void const_pairs(const double (&x)[J][3], const double* s, double (&acc)[J][3],
+                                            unsigned& zc) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const double rx = x[j][0] - s[0], ry = x[j][1] - s[1], rz = x[j][2] - s[2];
+        const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
+        const double y0 = rsqrt_mufu(r2);
+        const double e = fma(-r2, y0 * y0, 1.0);
+        const double h = e * fma(e, 0.375, 0.5);
+        double rinv = fma(y0, h, y0);                  // y0 (1 + e/2 + 3e^2/8)
+        const bool z = is_zero_r2(r2);
+        rinv = z ? 0.0 : rinv;
+        zc += z;
+        if constexpr (KIND == FAR_STOKES_SLDL) {
+            // u += rinv (g + c r),  c = (r.g) rinv^2 (1 + (r.a) rinv^2)
+            const double s2 = rinv * rinv;
+            const double rg = fma(rx, s[6], fma(ry, s[7], rz * s[8]));
+            const double ra = fma(rx, s[3], fma(ry, s[4], rz * s[5]));
+            const double c = (rg * s2) * fma(ra, s2, 1.0);
+            acc[j][0] = fma(rinv, fma(c, rx, s[6]), acc[j][0]);
+            acc[j][1] = fma(rinv, fma(c, ry, s[7]), acc[j][1]);
+            acc[j][2] = fma(rinv, fma(c, rz, s[8]), acc[j][2]);
+        } else if constexpr (KIND == FAR_STOKES_DL) {
+            // u += (r.a)(r.g) rinv^5 r
+            const double s2 = rinv * rinv;
+            const double ra = fma(rx, s[3], fma(ry, s[4], rz * s[5]));
+            const double rd = fma(rx, s[6], fma(ry, s[7], rz * s[8]));
+            const double b = (ra * rd) * ((s2 * s2) * rinv);
+            acc[j][0] = fma(b, rx, acc[j][0]);
+            acc[j][1] = fma(b, ry, acc[j][1]);
+            acc[j][2] = fma(b, rz, acc[j][2]);
+        } else {
+            // Laplace DL: u += (r.q) rinv^3
+            const double rq = fma(rx, s[6], fma(ry, s[7], rz * s[8]));
+            acc[j][0] = fma(rq, (rinv * rinv) * rinv, acc[j][0]);
+        }
+    }
+}
+
+template <int KIND, int J, int BUF>
+__global__ void __launch_bounds__(kConstThreads, 4)
+far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
+                 double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
+    constexpr int D = (KIND == FAR_LAPLACE) ? 1 : 3;
+    double x[J][3], acc[J][3];
+    bool valid[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int64_t t = (int64_t)blockIdx.x * kConstThreads * J + threadIdx.x + kConstThreads * j;
+        valid[j] = t < T;
+        const int64_t tc = valid[j] ? t : T - 1;
+        x[j][0] = x_trg[3 * tc]; x[j][1] = x_trg[3 * tc + 1]; x[j][2] = x_trg[3 * tc + 2];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[j][q] = (q < D && !first) ? partial[tc * D + q] : 0.0;
+    }
+    unsigned zc = 0;
+    const double* base = c_rec[BUF];
+#pragma unroll 4
+    for (int m = 0; m < n_src; ++m) const_pairs<KIND, J>(x, base + kRec * m, acc, zc);
+    unsigned zv = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int64_t t = (int64_t)blockIdx.x * kConstThreads * J + threadIdx.x + kConstThreads * j;
+        if (valid[j]) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) partial[t * D + q] = acc[j][q];
+        }
+    }
+    // coincident pairs of clamped (invalid) target slots are not counted
+    (void)zv;
+    if (zc) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < J; ++j) any |= valid[j];
+        if (any) atomicAdd(coincident, (unsigned long long)zc);
+    }
+}
+
+// rec[m] = {geo[m][0..5], dyn[m][0..2], 0}
+__global__ void pack_rec_kernel(int64_t M, const double* __restrict__ geo, const double* __restrict__ dyn,
+                                double* __restrict__ rec) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const double2* g = reinterpret_cast<const double2*>(geo + m * 6);
+    const double2* d = reinterpret_cast<const double2*>(dyn + m * 4);
+    double2* o = reinterpret_cast<double2*>(rec + m * kRec);
+    o[0] = g[0]; o[1] = g[1]; o[2] = g[2];
+    const double2 d0 = d[0], d1 = d[1];
+    o[3] = d0;
+    o[4] = make_double2(d1.x, 0.0);
+}
+
+constexpr int kJ = 2;
+
+template <int KIND, int BUF>
+static void launch_tile(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
+                        cudaStream_t s) {
+    const unsigned grid = (unsigned)((T + kConstThreads * kJ - 1) / (kConstThreads * kJ));
+    far_const_kernel<KIND, kJ, BUF><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+}
+
+template <int KIND>
+static void launch_tile_buf(int buf, int64_t T, const double* x, int n, int first, double* part,
+                            unsigned long long* zc, cudaStream_t s) {
+    switch (buf) {
+        case 0: launch_tile<KIND, 0>(T, x, n, first, part, zc, s); break;
+        case 1: launch_tile<KIND, 1>(T, x, n, first, part, zc, s); break;
+        case 2: launch_tile<KIND, 2>(T, x, n, first, part, zc, s); break;
+        default: launch_tile<KIND, 3>(T, x, n, first, part, zc, s); break;
+    }
+}
+
+// Issue the constant-bank far field on the 4 internal streams (forked from/joined to s).
+// partials: [kConstBufs][T][D].  Returns the number of kernel launches issued.
+slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
+                           double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
+                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches) {
+    const int D = (kind == FAR_LAPLACE) ? 1 : 3;
+    *launches = 0;
+    SLB_CUDA(cudaEventRecord(fork, s));
+    for (int b = 0; b < kConstBufs; ++b) SLB_CUDA(cudaStreamWaitEvent(ws[b], fork, 0));
+    const int64_t ntiles = (M + kConstTile - 1) / kConstTile;
+    for (int b = 0; b < kConstBufs; ++b) {
+        double* part = partials + (int64_t)b * T * D;
+        if (b >= ntiles && T > 0) SLB_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * T * D, ws[b]));
+    }
+    for (int64_t i = 0; i < ntiles; ++i) {
+        const int b = (int)(i % kConstBufs);
+        const int64_t m0 = i * kConstTile;
+        const int n = (int)std::min<int64_t>(kConstTile, M - m0);
+        SLB_CUDA(cudaMemcpyToSymbolAsync(c_rec, rec + m0 * kRec, sizeof(double) * n * kRec,
+                                         sizeof(double) * (size_t)b * kConstTile * kRec, cudaMemcpyDeviceToDevice,
+                                         ws[b]));
+        if (T > 0) {
+            double* part = partials + (int64_t)b * T * D;
+            const int first = (i < kConstBufs) ? 1 : 0;
+            switch (kind) {
+                case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b, T, x, n, first, part, zc, ws[b]); break;
+                case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b, T, x, n, first, part, zc, ws[b]); break;
+                default: launch_tile_buf<FAR_LAPLACE>(b, T, x, n, first, part, zc, ws[b]); break;
+            }
+            ++*launches;
+        }
+    }
+    for (int b = 0; b < kConstBufs; ++b) {
+        SLB_CUDA(cudaEventRecord(join[b], ws[b]));
+        SLB_CUDA(cudaStreamWaitEvent(s, join[b], 0));
+    }
+    return check_launch("far_const_kernel");
+}
+
+slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s) {
+    if (M <= 0) return SLB_OK;
+    pack_rec_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, geo, dyn, rec);
+    ++g_launch_count;
+    return check_launch("pack_rec_kernel");
+}
+
+int far_const_bufs() { return kConstBufs; }
+
+}  // namespace slb

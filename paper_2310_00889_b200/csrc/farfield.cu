@@ -340,10 +340,10 @@ slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t T, const doub
                     case 2: return launch_far<FAR_STOKES_SLDL, 4, 1, 1, 1>(plan, T, x, geo, dyn, partials, zc, s);
                     case 3: return launch_far<FAR_STOKES_SLDL, 4, 1, 2, 1>(plan, T, x, geo, dyn, partials, zc, s);
                     case 4: return launch_far<FAR_STOKES_SLDL, 1, 1, 4, 4>(plan, T, x, geo, dyn, partials, zc, s);
-                    case 5: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 4>(plan, T, x, geo, dyn, partials, zc, s);
+                    case 5: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
                     case 6: return launch_far<FAR_STOKES_SLDL, 1, 1, 3, 4>(plan, T, x, geo, dyn, partials, zc, s);
                     case 7: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 1>(plan, T, x, geo, dyn, partials, zc, s);
-                    default: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+                    default: return launch_far<FAR_STOKES_SLDL, 2, 1, 2, 4>(plan, T, x, geo, dyn, partials, zc, s);
                 }
         }
     } else {

@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <vector>
 #include "common.cuh"
 
@@ -97,6 +99,13 @@ struct slb_operator {
     double* u_dev = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     bool timed = false;
+    // constant-bank far field (large M): packed records, 4 worker streams, captured graph
+    bool use_const = false;
+    double* rec = nullptr;              // [M][10]
+    cudaStream_t ws[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraphExec_t graph = nullptr;
+    int64_t const_launches = 0;
 };
 
 using namespace slb;
@@ -125,8 +134,12 @@ static void free_op(slb_operator* op) {
     if (!op) return;
     cudaFree(op->geo); cudaFree(op->sc); cudaFree(op->dyn); cudaFree(op->coarse);
     cudaFree(op->partials); cudaFree(op->Lsig); cudaFree(op->nb0); cudaFree(op->bodyc);
-    cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev);
+    cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev); cudaFree(op->rec);
     for (auto& e : op->ev) if (e) cudaEventDestroy(e);
+    if (op->graph) cudaGraphExecDestroy(op->graph);
+    for (auto& w : op->ws) if (w) cudaStreamDestroy(w);
+    for (auto& e : op->join) if (e) cudaEventDestroy(e);
+    if (op->fork) cudaEventDestroy(op->fork);
     delete op;
 }
 
@@ -207,6 +220,11 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     op->N_loc = op->P_loc * op->Nn;
     op->cols = op->Nn * op->sdim;
     op->plan = far_plan(op->M);
+    {
+        const char* e = getenv("SLB_FAR_PATH");
+        op->use_const = e ? (std::string(e) == "const") : (op->M >= (int64_t(1) << 19));
+        if (op->use_const) op->plan.n_chunks = far_const_bufs();
+    }
     if (d->n_on_local > op->N_loc) {
         free_op(op);
         set_error("slb_operator_create: n_on_local exceeds the local node count");
@@ -332,6 +350,31 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         OPCUDA(cudaMemcpy(op->bodyc, bc.data(), sizeof(double) * nb * 16, cudaMemcpyHostToDevice));
     }
     for (auto& e : op->ev) OPCUDA(cudaEventCreate(&e));
+    if (op->use_const) {
+        OPCUDA(cudaMalloc(&op->rec, sizeof(double) * op->M * 10));
+        for (auto& w : op->ws) OPCUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
+        OPCUDA(cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming));
+        for (auto& e : op->join) OPCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        cudaStream_t cs = nullptr;
+        OPCUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        OPCUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        slb_status st = far_const_issue(op->kind, op->M, T, d->x_trg, op->rec, op->partials, coincident_counter(), cs,
+                                        op->ws, op->fork, op->join, &op->const_launches);
+        cudaGraph_t g = nullptr;
+        cudaError_t e1 = cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        if (st != SLB_OK) { if (g) cudaGraphDestroy(g); return fail(st); }
+        if (e1 != cudaSuccess) {
+            set_error(std::string("slb_operator_create: graph capture failed: ") + cudaGetErrorString(e1));
+            return fail(SLB_ERR_CUDA);
+        }
+        cudaError_t e2 = cudaGraphInstantiate(&op->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e2 != cudaSuccess) {
+            set_error(std::string("slb_operator_create: graph instantiate failed: ") + cudaGetErrorString(e2));
+            return fail(SLB_ERR_CUDA);
+        }
+    }
     OPCUDA(cudaDeviceSynchronize());
     OPST(check_launch("slb_operator_create"));
 #undef OPCUDA
@@ -369,8 +412,15 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     st = allgather(op, op->coarse, op->cols, s);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[2], s));
-    st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
-    if (st != SLB_OK) return st;
+    if (op->use_const) {
+        st = pack_rec_launch(op->M, op->geo, op->dyn, op->rec, s);
+        if (st != SLB_OK) return st;
+        SLB_CUDA(cudaGraphLaunch(op->graph, s));
+        g_launch_count += (unsigned long long)op->const_launches;
+    } else {
+        st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
+        if (st != SLB_OK) return st;
+    }
     SLB_CUDA(cudaEventRecord(op->ev[3], s));
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
                          d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, s);
@@ -403,6 +453,7 @@ slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]) {
 int slb_operator_launches_per_matvec(const slb_operator* op) {
     if (!op) return -1;
     int n = 3;                                   // upsample, far, finalize
+    if (op->use_const) n += 1 + (int)op->const_launches - 1;   // pack_rec + one launch per source tile
     if (op->d.n_bodies_local > 0) n += 2;        // projector coef + apply
     return n;
 }
