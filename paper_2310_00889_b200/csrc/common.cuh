@@ -154,6 +154,7 @@ slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, 
                            cudaEvent_t fork, cudaEvent_t* join, int64_t* launches);
 slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s);
 int far_const_bufs();
+slb_status far_const_prepare();
 
 // ---- packing kernels (farfield.cu) ----
 slb_status pack_geo(FarKind kind, int64_t M, const double* y, const double* n, const double* eta_src,

@@ -189,4 +189,22 @@ slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, doub
 
 int far_const_bufs() { return kConstBufs; }
 
+// Load this module's kernels and constant symbol eagerly (lazy module loading must not happen
+// inside a stream capture).
+slb_status far_const_prepare() {
+    void* p = nullptr;
+    SLB_CUDA(cudaGetSymbolAddress(&p, c_rec));
+    cudaFuncAttributes fa;
+#define PREP(K) SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 0>)); \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 1>));             \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 2>));             \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 3>));
+    PREP(FAR_STOKES_SLDL)
+    PREP(FAR_STOKES_DL)
+    PREP(FAR_LAPLACE)
+#undef PREP
+    SLB_CUDA(cudaFuncGetAttributes(&fa, pack_rec_kernel));
+    return SLB_OK;
+}
+
 }  // namespace slb

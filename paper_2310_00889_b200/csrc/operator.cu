@@ -355,25 +355,27 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         for (auto& w : op->ws) OPCUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
         OPCUDA(cudaEventCreateWithFlags(&op->fork, cudaEventDisableTiming));
         for (auto& e : op->join) OPCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        OPST(far_const_prepare());
+        OPCUDA(cudaDeviceSynchronize());
+        // capture the tile sequence once; if capture is not possible, slb_matvec issues it directly
         cudaStream_t cs = nullptr;
         OPCUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        OPCUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        slb_status st = far_const_issue(op->kind, op->M, T, d->x_trg, op->rec, op->partials, coincident_counter(), cs,
-                                        op->ws, op->fork, op->join, &op->const_launches);
         cudaGraph_t g = nullptr;
-        cudaError_t e1 = cudaStreamEndCapture(cs, &g);
+        bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            slb_status st = far_const_issue(op->kind, op->M, T, d->x_trg, op->rec, op->partials, coincident_counter(),
+                                            cs, op->ws, op->fork, op->join, &op->const_launches);
+            cudaError_t e1 = cudaStreamEndCapture(cs, &g);
+            ok = (st == SLB_OK && e1 == cudaSuccess && g != nullptr);
+            if (ok) ok = cudaGraphInstantiate(&op->graph, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+        }
         cudaStreamDestroy(cs);
-        if (st != SLB_OK) { if (g) cudaGraphDestroy(g); return fail(st); }
-        if (e1 != cudaSuccess) {
-            set_error(std::string("slb_operator_create: graph capture failed: ") + cudaGetErrorString(e1));
-            return fail(SLB_ERR_CUDA);
+        if (!ok) {
+            op->graph = nullptr;
+            cudaGetLastError();            // clear the capture error; fall back to direct issue
         }
-        cudaError_t e2 = cudaGraphInstantiate(&op->graph, g, 0);
-        cudaGraphDestroy(g);
-        if (e2 != cudaSuccess) {
-            set_error(std::string("slb_operator_create: graph instantiate failed: ") + cudaGetErrorString(e2));
-            return fail(SLB_ERR_CUDA);
-        }
+        op->const_launches = (T > 0) ? (op->M + 199) / 200 : 0;
     }
     OPCUDA(cudaDeviceSynchronize());
     OPST(check_launch("slb_operator_create"));
@@ -415,8 +417,16 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     if (op->use_const) {
         st = pack_rec_launch(op->M, op->geo, op->dyn, op->rec, s);
         if (st != SLB_OK) return st;
-        SLB_CUDA(cudaGraphLaunch(op->graph, s));
-        g_launch_count += (unsigned long long)op->const_launches;
+        if (op->graph) {
+            SLB_CUDA(cudaGraphLaunch(op->graph, s));
+            g_launch_count += (unsigned long long)op->const_launches;
+        } else {
+            int64_t nl = 0;
+            st = far_const_issue(op->kind, op->M, d.n_trg_local, d.x_trg, op->rec, op->partials, zc, s, op->ws,
+                                 op->fork, op->join, &nl);
+            if (st != SLB_OK) return st;
+            g_launch_count += (unsigned long long)nl;
+        }
     } else {
         st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
         if (st != SLB_OK) return st;
