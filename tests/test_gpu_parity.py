@@ -244,3 +244,23 @@ def test_matvec_parity_full_size_sampled(S, name):
                                      np.array([0, pr.T - 1])]))
     err, u, _ = _matvec_vs_oracle(S, pr, rows)
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c2", dict(panels=4)), ("c4", dict(n_loops=2, panels=8)),
+                                     ("c5", dict(n_loops=3, panels=9, box=5.0))])
+@pytest.mark.parametrize("path", ["const", "tma"])
+def test_matvec_both_far_paths(S, name, kw, path, monkeypatch):
+    """Both far-field engines (constant-bank tiles / TMA smem ring) on small problems, including
+    fewer source tiles than constant buffers (c2 with 4 panels: 10240 sources = 52 tiles; c1)."""
+    monkeypatch.setenv("SLB_FAR_PATH", path)
+    pr = make_config(name, **kw)
+    err, u, u2 = _matvec_vs_oracle(S, pr)
+    assert err <= TOL, err
+    assert np.array_equal(u, u2)
+
+
+def test_const_path_fewer_tiles_than_buffers(S, monkeypatch):
+    monkeypatch.setenv("SLB_FAR_PATH", "const")
+    pr = make_config("c1", panels=1, n_extra=5)      # 1 panel: 480 fine sources = 3 tiles < 4 buffers
+    err, u, _ = _matvec_vs_oracle(S, pr)
+    assert err <= TOL, err
