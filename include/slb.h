@@ -134,6 +134,19 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
 slb_status slb_fill_blocks(uint64_t seed, uint64_t first, int64_t count, double s_blk,
                            double* blocks, cudaStream_t s);
 
+/* (NEXT N3, setup) Near-list construction: CSR over targets of
+ *   near(t) = { k : sqrt(min_j |x_t - y_kj|^2) < radius[k] }  U  { own_panel[t] }   (R15;
+ *   stands in for the paper's sphere/Morton near-region search, §3.3),
+ *   distances evaluated exactly in fp64 as ((dx*dx + dy*dy) + dz*dz), panels ascending per row.
+ *   x_trg: [n_trg][3]; y_nodes: [n_panels][nodes_per_panel][3]; radius: [n_panels];
+ *   own_panel: [n_trg] (-1 = none) or NULL.  row_ptr: [n_trg+1] (written).  panel_idx: NULL to
+ *   only count, else [capacity] (written when capacity >= nnz).  *nnz_out (host) = nnz.
+ *   Synchronises s (the count is returned to the host). */
+slb_status slb_near_build(int64_t n_trg, const double* x_trg, int64_t n_panels, int nodes_per_panel,
+                          const double* y_nodes, const double* radius, const int64_t* own_panel,
+                          int64_t* row_ptr, int32_t* panel_idx, int64_t capacity, int64_t* nnz_out,
+                          cudaStream_t s);
+
 /* ---------------- full operator (single- or multi-GPU) ---------------- */
 typedef struct slb_comm slb_comm;
 typedef struct slb_operator slb_operator;

@@ -104,6 +104,21 @@ def slb_fill_blocks(seed, first, count, s_blk, out):
     return out
 
 
+def slb_near_build(x_trg, y_nodes, radius, own_panel=None):
+    """Near-list CSR on the GPU (R15): returns (row_ptr int64 [T+1], panel_idx int32 [nnz])."""
+    T = x_trg.shape[0]
+    P, Nn = y_nodes.shape[0], y_nodes.shape[1]
+    row_ptr = torch.empty(T + 1, dtype=torch.int64, device=x_trg.device)
+    nnz = ctypes.c_int64(0)
+    args = (T, _dev(x_trg, "x_trg"), P, Nn, _dev(y_nodes, "y_nodes"), _dev(radius, "radius"),
+            _dev(own_panel, "own_panel", torch.int64, allow_none=True), _dev(row_ptr, "row_ptr", torch.int64))
+    check(lib().slb_near_build(*args, None, 0, ctypes.byref(nnz), _stream()))
+    panel_idx = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=x_trg.device)
+    check(lib().slb_near_build(*args, _dev(panel_idx, "panel_idx", torch.int32), panel_idx.numel(),
+                               ctypes.byref(nnz), _stream()))
+    return row_ptr, panel_idx[:nnz.value]
+
+
 def slb_bench_dfma(iters=20000):
     g = ctypes.c_double(0.0)
     check(lib().slb_bench_dfma(int(iters), ctypes.byref(g), _stream()))

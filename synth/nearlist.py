@@ -43,8 +43,10 @@ def build_near_csr(x_trg, y_panels, ring_xc, rho_ring, L, own_panel, forced_rows
         lim = 2 * L[k]
         hi = np.min(d + rr, axis=1)
         lo = np.min(d - rr, axis=1)
-        sure = hi < lim
-        maybe = np.nonzero((~sure) & (lo < lim))[0]
+        # shortcuts only where the bound clears the threshold by a relative 1e-9, so every decision
+        # equals the exact rule  sqrt(min_j ((dx^2 + dy^2) + dz^2)) < 2 L_k  evaluated in fp64
+        sure = hi < lim * (1 - 1e-9)
+        maybe = np.nonzero((~sure) & (lo < lim * (1 + 1e-9)))[0]
         res = sure
         if maybe.size:
             Y = y_panels[k[maybe]]             # [m, Nn, 3]

@@ -1,0 +1,50 @@
+"""(NEXT N3) GPU near-list construction vs the input generator's CPU rule (R15):
+integer output, so the CSR must match bit for bit on every config."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import make_config  # noqa: E402
+
+
+def cu(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c2", {}), ("c3", {}), ("c4", {}), ("c5", dict(n_loops=64, box=8.0)),
+                                     ("c5", {})])
+def test_near_build_matches_generator(name, kw):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_00889_b200 import slb_near_build
+    pr = make_config(name, **kw)
+    radius = cu(2.0 * pr.panel_len)
+    y = cu(pr.y_c.reshape(pr.P, pr.Nn, 3))
+    if name == "c1":   # node targets follow the forced {k-1,k,k+1} rule; compare the off-surface rows
+        rows = np.arange(pr.n_on, pr.T)
+        own = None
+    else:
+        rows = np.arange(pr.T)
+        own = cu(np.repeat(np.arange(pr.P), pr.Nn).astype(np.int64), torch.int64)
+    rp, pi = slb_near_build(cu(pr.x_trg[rows]), y, radius, own)
+    rp, pi = rp.cpu().numpy(), pi.cpu().numpy()
+    ref_rp = pr.row_ptr[rows[0]:rows[-1] + 2] - pr.row_ptr[rows[0]]
+    ref_pi = pr.panel_idx[pr.row_ptr[rows[0]]:pr.row_ptr[rows[-1] + 1]]
+    assert np.array_equal(rp, ref_rp)
+    assert np.array_equal(pi, ref_pi)
+
+
+def test_near_build_edge_cases():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_00889_b200 import slb_near_build
+    y = cu(np.random.default_rng(0).standard_normal((3, 4, 3)))
+    # no targets
+    rp, pi = slb_near_build(cu(np.zeros((0, 3))), y, cu(np.ones(3)))
+    assert rp.cpu().tolist() == [0] and pi.numel() == 0
+    # far target: empty row; own panel forced even when far
+    x = cu(np.array([[100.0, 0, 0], [100.0, 0, 0]]))
+    rp, pi = slb_near_build(x, y, cu(np.ones(3)), cu(np.array([-1, 2]), torch.int64))
+    assert rp.cpu().tolist() == [0, 0, 1] and pi.cpu().tolist() == [2]
