@@ -204,6 +204,16 @@ int slb_operator_launches_per_matvec(const slb_operator* op);
 
 slb_status slb_operator_destroy(slb_operator* op);
 
+/* (NEXT N2) Restarted GMRES(restart) for  A x = rhs  with A = slb_matvec,
+ * e.g. the CFIEs (I/2 + D + eta S) sigma = u0 and the mobility BIE (K(I-L) + L) sigma = rhs.
+ * Requires a square operator (targets = the local nodes).  rhs, x: [local nodes][sdim] device;
+ * x holds the initial guess on entry and the solution on return.  Stops when the true residual
+ * ||rhs - A x|| <= tol ||rhs|| (checked at restarts) or after max_iters matvecs.  CGS2
+ * orthogonalisation, fixed-order reductions (NCCL all-reduce across ranks): reproducible.
+ * Collective across the operator's ranks; synchronises s.  iters_out, relres_out: host, may be NULL. */
+slb_status slb_gmres(slb_operator* op, const double* rhs, double* x, int restart, int max_iters,
+                     double tol, int* iters_out, double* relres_out, cudaStream_t s);
+
 /* Microbenchmark: sustained FP64 FMA throughput (GFLOP/s, FMA = 2 flops) of this device,
  * measured with dependent-chain-free DFMA streams over all SMs for ~iters iterations. */
 slb_status slb_bench_dfma(int64_t iters, double* gflops, cudaStream_t s);

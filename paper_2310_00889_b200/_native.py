@@ -49,6 +49,7 @@ _SIGS = {
     "slb_operator_last_timings": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
     "slb_operator_launches_per_matvec": (I32, [P]),
     "slb_operator_destroy": (I32, [P]),
+    "slb_gmres": (I32, [P, P, P, I32, I32, D, ctypes.POINTER(I32), ctypes.POINTER(D), P]),
     "slb_bench_dfma": (I32, [I64, ctypes.POINTER(D), P]),
 }
 

@@ -199,6 +199,15 @@ class Operator:
                                     ctypes.c_void_p(out_host.data_ptr()), _stream()))
         return out_host
 
+    def gmres(self, rhs, x0=None, restart=50, max_iters=1000, tol=1e-12):
+        """Solve A x = rhs with slb_gmres; returns (x, iterations, relative residual)."""
+        x = torch.zeros_like(rhs) if x0 is None else x0.clone()
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        check(lib().slb_gmres(self.h, _dev(rhs, "rhs"), _dev(x, "x"), int(restart), int(max_iters), float(tol),
+                              ctypes.byref(it), ctypes.byref(rr), _stream()))
+        return x, it.value, rr.value
+
     def timings(self):
         arr = (ctypes.c_float * 4)()
         check(lib().slb_operator_last_timings(self.h, arr))

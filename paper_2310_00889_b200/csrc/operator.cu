@@ -9,104 +9,13 @@
 //   finalize: partials + folded near blocks E sigma' + c_I sigma' [+ L sigma]  (Eq. e:nystrom-correction,
 //                                                                              P:L1750/1868/2009)
 // NCCL is loaded at run time (dlopen "libnccl.so.2": the copy torch already loaded is reused).
-#include <dlfcn.h>
-#include <nccl.h>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
 #include <string>
 #include <vector>
-#include "common.cuh"
-
-namespace slb {
-
-// ------------------------------------------------------------------ NCCL (dlopen)
-struct NcclApi {
-    bool ok = false;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
-    ncclResult_t (*CommDestroy)(ncclComm_t);
-    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
-    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
-    ncclResult_t (*GroupStart)();
-    ncclResult_t (*GroupEnd)();
-    const char* (*GetErrorString)(ncclResult_t);
-};
-
-static NcclApi& nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (tried) return api;
-    tried = true;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return api;
-#define LOADSYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
-    LOADSYM(GetUniqueId, "ncclGetUniqueId");
-    LOADSYM(CommInitRank, "ncclCommInitRank");
-    LOADSYM(CommDestroy, "ncclCommDestroy");
-    LOADSYM(AllGather, "ncclAllGather");
-    LOADSYM(Broadcast, "ncclBroadcast");
-    LOADSYM(GroupStart, "ncclGroupStart");
-    LOADSYM(GroupEnd, "ncclGroupEnd");
-    LOADSYM(GetErrorString, "ncclGetErrorString");
-#undef LOADSYM
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.Broadcast &&
-             api.GroupStart && api.GroupEnd && api.GetErrorString;
-    return api;
-}
-
-#define SLB_NCCL(call)                                                                        \
-    do {                                                                                      \
-        ncclResult_t r_ = (call);                                                             \
-        if (r_ != ncclSuccess) {                                                              \
-            ::slb::set_error(std::string(__func__) + ": " #call ": " + nccl().GetErrorString(r_)); \
-            return SLB_ERR_NCCL;                                                              \
-        }                                                                                     \
-    } while (0)
-
-}  // namespace slb
-
-struct slb_comm {
-    ncclComm_t comm = nullptr;
-    int nranks = 1, rank = 0;
-};
-
-struct slb_operator {
-    slb_operator_desc d;
-    slb_comm* comm = nullptr;
-    slb::FarKind kind;
-    int tdim = 1, sdim = 1;
-    slb::FarPlan plan;
-    slb::InterpParams ip;
-    int64_t P_loc = 0, N_loc = 0, Nn = 0, Mn = 0, M = 0, cols = 0;
-    std::vector<int64_t> ranges;        // panel offsets of all ranks [R+1]
-    bool equal_shards = true;
-    // device buffers owned by the operator
-    double* geo = nullptr;              // [M][6]
-    double* sc = nullptr;               // local fine scales [M_loc] or [M_loc][3]
-    double* dyn = nullptr;              // [M][4] global fine records
-    double* coarse = nullptr;           // [P_global][Nn][sdim] global sigma'
-    double* partials = nullptr;         // [n_chunks][T_loc][tdim]
-    double* Lsig = nullptr;             // [N_loc][3]
-    int64_t* nb0 = nullptr;             // [nb+1] local node offsets of bodies
-    double* bodyc = nullptr;            // [nb][16]
-    double* coef = nullptr;             // [nb][6]
-    int64_t max_nodes_body = 0;
-    double* sig_dev = nullptr;          // host-variant staging
-    double* u_dev = nullptr;
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    bool timed = false;
-    // constant-bank far field (large M): packed records, 4 worker streams, captured graph
-    bool use_const = false;
-    double* rec = nullptr;              // [M][10]
-    cudaStream_t ws[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaGraphExec_t graph = nullptr;
-    int64_t const_launches = 0;
-};
+#include "operator_impl.cuh"
 
 using namespace slb;
 
