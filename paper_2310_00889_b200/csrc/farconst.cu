@@ -28,9 +28,9 @@ constexpr int kConstThreads = 128;
 
 __constant__ double c_rec[kConstBufs][kConstTile * kRec];
 
-template <int KIND, int J>
+template <int KIND, int J, int CM>
 __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const double* s, double (&acc)[J][3],
-                                            unsigned& zc) {
+                                            bool& anyz, unsigned& zc) {
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const double rx = x[j][0] - s[0], ry = x[j][1] - s[1], rz = x[j][2] - s[2];
@@ -41,7 +41,8 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
         double rinv = fma(y0, h, y0);                  // y0 (1 + e/2 + 3e^2/8)
         const bool z = is_zero_r2(r2);
         rinv = z ? 0.0 : rinv;
-        zc += z;
+        if (CM == 0) anyz |= z;                        // rare: exact recount after the loop
+        else zc += z;
         if constexpr (KIND == FAR_STOKES_SLDL) {
             // u += rinv (g + c r),  c = (r.g) rinv^2 (1 + (r.a) rinv^2)
             const double s2 = rinv * rinv;
@@ -68,7 +69,7 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
     }
 }
 
-template <int KIND, int J, int BUF>
+template <int KIND, int J, int BUF, int CM>
 __global__ void __launch_bounds__(kConstThreads, 4)
 far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
                  double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
@@ -84,11 +85,17 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
 #pragma unroll
         for (int q = 0; q < 3; ++q) acc[j][q] = (q < D && !first) ? partial[tc * D + q] : 0.0;
     }
-    unsigned zc = 0;
+    bool anyz = false;
+    unsigned zc0 = 0;
     const double* base = c_rec[BUF];
 #pragma unroll 4
-    for (int m = 0; m < n_src; ++m) const_pairs<KIND, J>(x, base + kRec * m, acc, zc);
-    unsigned zv = 0;
+    for (int m = 0; m < n_src; ++m) const_pairs<KIND, J, CM>(x, base + kRec * m, acc, anyz, zc0);
+    if (CM == 1 && zc0) {
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < J; ++j) any |= valid[j];
+        if (any) atomicAdd(coincident, (unsigned long long)zc0);
+    }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int64_t t = (int64_t)blockIdx.x * kConstThreads * J + threadIdx.x + kConstThreads * j;
@@ -97,13 +104,17 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
             for (int q = 0; q < D; ++q) partial[t * D + q] = acc[j][q];
         }
     }
-    // coincident pairs of clamped (invalid) target slots are not counted
-    (void)zv;
-    if (zc) {
-        bool any = false;
+    // coincident (r = 0) pairs: recount exactly, only in threads that saw one (valid targets only)
+    if (anyz) {
+        unsigned long long zc = 0;
+        for (int m = 0; m < n_src; ++m)
 #pragma unroll
-        for (int j = 0; j < J; ++j) any |= valid[j];
-        if (any) atomicAdd(coincident, (unsigned long long)zc);
+            for (int j = 0; j < J; ++j) {
+                const double rx = x[j][0] - base[kRec * m], ry = x[j][1] - base[kRec * m + 1],
+                             rz = x[j][2] - base[kRec * m + 2];
+                zc += (valid[j] && is_zero_r2(fma(rx, rx, fma(ry, ry, rz * rz)))) ? 1 : 0;
+            }
+        if (zc) atomicAdd(coincident, zc);
     }
 }
 
@@ -123,11 +134,20 @@ __global__ void pack_rec_kernel(int64_t M, const double* __restrict__ geo, const
 
 constexpr int kJ = 2;
 
+static int const_count_mode() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("SLB_CONST_COUNT"); v = (e && e[0] == '1') ? 1 : 0; }
+    return v;
+}
+
 template <int KIND, int BUF>
 static void launch_tile(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
                         cudaStream_t s) {
     const unsigned grid = (unsigned)((T + kConstThreads * kJ - 1) / (kConstThreads * kJ));
-    far_const_kernel<KIND, kJ, BUF><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+    if (const_count_mode() == 1)
+        far_const_kernel<KIND, kJ, BUF, 1><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+    else
+        far_const_kernel<KIND, kJ, BUF, 0><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
 }
 
 template <int KIND>
@@ -195,14 +215,16 @@ slb_status far_const_prepare() {
     void* p = nullptr;
     SLB_CUDA(cudaGetSymbolAddress(&p, c_rec));
     cudaFuncAttributes fa;
-#define PREP(K) SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 0>)); \
-    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 1>));             \
-    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 2>));             \
-    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 3>));
+#define PREP1(K, C) SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 0, C>)); \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 1, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 2, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 3, C>));
+#define PREP(K) PREP1(K, 0) PREP1(K, 1)
     PREP(FAR_STOKES_SLDL)
     PREP(FAR_STOKES_DL)
     PREP(FAR_LAPLACE)
 #undef PREP
+#undef PREP1
     SLB_CUDA(cudaFuncGetAttributes(&fa, pack_rec_kernel));
     return SLB_OK;
 }
