@@ -29,85 +29,110 @@ __device__ __forceinline__ double warp_sum(double v) {
 //   MODE 0 (slb_nearcorr_apply):  u[t] += near(t)
 //   MODE 1 (slb_matvec finalize): u[t]  = (sum_c partials[c][t] + near(t)) + c_id sigma'_t [t < n_on] + (L sigma)_t
 constexpr int kNearStages = 3;
+constexpr int kNearWarps = 4;
 
+// Persistent streaming: each warp owns a contiguous range of targets chosen so that
+// (blocks + targets) is balanced across warps; the TMA ring runs continuously across target
+// boundaries (block i of the warp's range always goes to slot i % STG), so short rows do not
+// drain the pipeline.
 template <int TD, int MODE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kNearWarps * 32)
 near_stream_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
                    const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
                    const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
                    int64_t n_on, double c_id, const double* __restrict__ sig_local,
                    const double* __restrict__ Lsig, double* __restrict__ u) {
     extern __shared__ __align__(128) double2 ring[];      // [warps][STG][TD*cols2]
-    __shared__ __align__(8) uint64_t bars[4 * kNearStages];
-    const int nw = blockDim.x >> 5;
+    __shared__ __align__(8) uint64_t bars[kNearWarps * kNearStages];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = TD * cols2;                          // double2 per block
     const uint32_t bytes = (uint32_t)slot * 16u;
     double2* myring = ring + (size_t)w * kNearStages * slot;
     uint64_t* mybar = bars + w * kNearStages;
-    const int64_t t = (int64_t)blockIdx.x * nw + w;
-    const bool active = t < T;
     if (lane == 0) {
         for (int q = 0; q < kNearStages; ++q) mbar_init(&mybar[q], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    if (!active) return;
-    const int64_t p0 = row_ptr[t], nb = row_ptr[t + 1] - p0;
+    // balanced target range of this warp: cost(t) = row_ptr[t] + t
+    const int64_t W = (int64_t)gridDim.x * kNearWarps;
+    const int64_t gw = (int64_t)blockIdx.x * kNearWarps + w;
+    const int64_t total = row_ptr[T] + T;
+    auto first_target = [&](int64_t c) {      // smallest t with row_ptr[t] + t >= c
+        int64_t lo = 0, hi = T;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (row_ptr[mid] + mid < c) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    int64_t ta = 0, tb = 0;
+    if (lane == 0) {
+        ta = first_target((total * gw) / W);
+        tb = first_target((total * (gw + 1)) / W);
+    }
+    ta = __shfl_sync(0xffffffffu, ta, 0);
+    tb = __shfl_sync(0xffffffffu, tb, 0);
+    if (ta >= tb) return;
+    const int64_t pa = row_ptr[ta], pb = row_ptr[tb];
     const double2* B = reinterpret_cast<const double2*>(blocks);
     if (lane == 0) {
-        for (int q = 0; q < kNearStages && q < nb; ++q) {
+        for (int q = 0; q < kNearStages && pa + q < pb; ++q) {
             mbar_expect_tx(&mybar[q], bytes);
-            bulk_g2s(myring + (size_t)q * slot, B + (p0 + q) * slot, bytes, &mybar[q]);
+            bulk_g2s(myring + (size_t)q * slot, B + (pa + q) * slot, bytes, &mybar[q]);
         }
     }
-    double acc[TD];
-#pragma unroll
-    for (int r = 0; r < TD; ++r) acc[r] = 0.0;
     const double2* S2 = reinterpret_cast<const double2*>(sigma_c);
-    for (int64_t i = 0; i < nb; ++i) {
-        const int st = (int)(i % kNearStages);
-        const int64_t k = panel_idx[p0 + i];
-        const double2* Sk = S2 + k * cols2;
-        mbar_wait(&mybar[st], (uint32_t)((i / kNearStages) & 1));
-        const double2* R = myring + (size_t)st * slot;
-#pragma unroll 2
-        for (int c = lane; c < cols2; c += 32) {
-            const double2 sv = __ldg(Sk + c);
+    int64_t i = 0;                                        // block counter within [pa, pb)
+    for (int64_t t = ta; t < tb; ++t) {
+        double acc[TD];
 #pragma unroll
-            for (int r = 0; r < TD; ++r) {
-                const double2 bv = R[r * cols2 + c];
-                acc[r] = fma(bv.x, sv.x, fma(bv.y, sv.y, acc[r]));
+        for (int r = 0; r < TD; ++r) acc[r] = 0.0;
+        const int64_t p1 = row_ptr[t + 1];
+        for (int64_t p = row_ptr[t]; p < p1; ++p, ++i) {
+            const int st = (int)(i % kNearStages);
+            const int64_t k = panel_idx[p];
+            const double2* Sk = S2 + k * cols2;
+            mbar_wait(&mybar[st], (uint32_t)((i / kNearStages) & 1));
+            const double2* R = myring + (size_t)st * slot;
+#pragma unroll 2
+            for (int c = lane; c < cols2; c += 32) {
+                const double2 sv = __ldg(Sk + c);
+#pragma unroll
+                for (int r = 0; r < TD; ++r) {
+                    const double2 bv = R[r * cols2 + c];
+                    acc[r] = fma(bv.x, sv.x, fma(bv.y, sv.y, acc[r]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && pa + i + kNearStages < pb) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(&mybar[st], bytes);
+                bulk_g2s(myring + (size_t)st * slot, B + (pa + i + kNearStages) * slot, bytes, &mybar[st]);
             }
         }
-        __syncwarp();
-        if (lane == 0 && i + kNearStages < nb) {
-            fence_proxy_async_smem();
-            mbar_expect_tx(&mybar[st], bytes);
-            bulk_g2s(myring + (size_t)st * slot, B + (p0 + i + kNearStages) * slot, bytes, &mybar[st]);
-        }
-    }
-    double far[TD];
+        double far[TD];
 #pragma unroll
-    for (int r = 0; r < TD; ++r) far[r] = 0.0;
-    if (MODE == 1)
-        for (int64_t c = lane; c < n_chunks; c += 32)
+        for (int r = 0; r < TD; ++r) far[r] = 0.0;
+        if (MODE == 1)
+            for (int64_t c = lane; c < n_chunks; c += 32)
 #pragma unroll
-            for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
+                for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
 #pragma unroll
-    for (int r = 0; r < TD; ++r) {
-        const double nv = warp_sum(acc[r]);
-        const double fv = MODE == 1 ? warp_sum(far[r]) : 0.0;
-        if (lane == r) {
-            if (MODE == 0) {
-                u[t * TD + r] += nv;
-            } else {
-                double v = fv + nv;
-                if (t < n_on) {
-                    v += c_id * sig_local[t * TD + r];
-                    if (Lsig) v += Lsig[t * TD + r];
+        for (int r = 0; r < TD; ++r) {
+            const double nv = warp_sum(acc[r]);
+            const double fv = MODE == 1 ? warp_sum(far[r]) : 0.0;
+            if (lane == r) {
+                if (MODE == 0) {
+                    u[t * TD + r] += nv;
+                } else {
+                    double v = fv + nv;
+                    if (t < n_on) {
+                        v += c_id * sig_local[t * TD + r];
+                        if (Lsig) v += Lsig[t * TD + r];
+                    }
+                    u[t * TD + r] = v;
                 }
-                u[t * TD + r] = v;
             }
         }
     }
@@ -119,18 +144,18 @@ static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, co
                                      const double* sig_local, const double* Lsig, double* u, cudaStream_t s) {
     if (T <= 0) return SLB_OK;
     const int cols2 = cols / 2;
-    const size_t per_warp = (size_t)kNearStages * tdim * cols2 * 16;
-    int nw = 4;
-    while (nw > 1 && per_warp * nw > 200 * 1024) nw >>= 1;
-    SLB_REQUIRE(per_warp * nw <= 227 * 1024, SLB_ERR_UNSUPPORTED, "near blocks too large for the smem ring");
-    const size_t smem = per_warp * nw;
-    const unsigned grid = (unsigned)((T + nw - 1) / nw);
+    const size_t smem = (size_t)kNearWarps * kNearStages * tdim * cols2 * 16;
+    SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "near blocks too large for the smem ring");
+    const int per_sm = std::max(1, (int)((227 * 1024) / std::max<size_t>(smem, 1)));
+    const int64_t want = (T + kNearWarps - 1) / kNearWarps;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * std::min(per_sm, 4)));
 #define NEAR_LAUNCH(TD, MODE)                                                                               \
     do {                                                                                                    \
         SLB_CUDA(cudaFuncSetAttribute(near_stream_kernel<TD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                       (int)smem));                                                          \
-        near_stream_kernel<TD, MODE><<<grid, nw * 32, smem, s>>>(T, cols2, row_ptr, panel_idx, blocks, sigma_c, \
-                                                                 partials, n_chunks, n_on, c_id, sig_local, Lsig, u); \
+        near_stream_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(T, cols2, row_ptr, panel_idx, blocks,  \
+                                                                         sigma_c, partials, n_chunks, n_on, c_id, \
+                                                                         sig_local, Lsig, u);               \
     } while (0)
     if (tdim == 1) {
         if (mode == 0) NEAR_LAUNCH(1, 0); else NEAR_LAUNCH(1, 1);
