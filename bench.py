@@ -237,6 +237,11 @@ def main():
     T_loc = dp.rows.size
     far_flops = T_loc * pr.M * FLOPS_PER_PAIR[pr.kernel]
     near_bytes = dp.nnz * (8 * pr.block_len + 4) + T_loc * 8 * (pr.tdim + 2)
+    n_loc_nodes = (dp.pe - dp.pb) * pr.Nn
+    m_loc = (dp.pe - dp.pb) * pr.Mn
+    # upsample (+projector) algorithmic bytes: sigma read + sigma' write (+ L sigma), fine scale read, records written
+    up_bytes = (n_loc_nodes * pr.sdim * 8 * (2 + (2 if pr.projector else 0)) + m_loc * 8 * (3 if pr.kernel == 1 else 1)
+                + m_loc * 8 * 3)
     dfma = None
     if rank == 0:
         try:
@@ -287,6 +292,10 @@ def main():
             "roofline_near": {"bound": "hbm", "kernel": "finalize_kernel (near blocks + chunk reduce)",
                               "achieved": near_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": near_gbs / hbm_peak,
                               "bytes_per_launch": near_bytes, "launch_ms": fin_ms},
+            "roofline_upsample": {"bound": "hbm", "kernel": "upsample_dmma_kernel (+ projector, DMMA m8n8k4)",
+                                  "achieved": up_bytes / (st_mean[0] * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": up_bytes / (st_mean[0] * 1e-3) / 1e9 / hbm_peak,
+                                  "bytes_per_launch": up_bytes, "launch_ms": st_mean[0]},
             "stage_ms": {"projector_upsample": st_mean[0], "allgather": st_mean[1], "far": far_ms,
                          "finalize_near": fin_ms},
             "cpu_baseline": cpu_base,

@@ -136,7 +136,8 @@ constexpr int kJ = 2;
 
 static int const_count_mode() {
     static int v = -1;
-    if (v < 0) { const char* e = getenv("SLB_CONST_COUNT"); v = (e && e[0] == '1') ? 1 : 0; }
+    // 1 (default): per-pair count -- measured faster than flag+recount (profiles/r01_bench_c4_cm*.json)
+    if (v < 0) { const char* e = getenv("SLB_CONST_COUNT"); v = (e && e[0] == '0') ? 0 : 1; }
     return v;
 }
 

@@ -11,6 +11,7 @@
 // with a fixed xor-butterfly, so the result is deterministic.  HBM-bound: bytes per (t,k) =
 // 8 tdim sdim N_n (+4 index).
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace slb {
@@ -31,17 +32,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 constexpr int kNearStages = 3;
 constexpr int kNearWarps = 4;
 
-// Persistent streaming: each warp owns a contiguous range of targets chosen so that
-// (blocks + targets) is balanced across warps; the TMA ring runs continuously across target
-// boundaries (block i of the warp's range always goes to slot i % STG), so short rows do not
-// drain the pipeline.
+// Each warp owns G consecutive targets (G chosen so a warp streams ~48 blocks); the TMA ring runs
+// continuously across the group's row boundaries (block i of the group always goes to slot
+// i % STG), so short rows do not drain the pipeline, while CTAs still run in target order --
+// the warps active at any moment read a narrow window of the block array (a persistent,
+// range-partitioned variant spread 1184 concurrent streams over 125 GB and thrashed the TLB).
 template <int TD, int MODE>
 __global__ void __launch_bounds__(kNearWarps * 32)
 near_stream_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
                    const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
                    const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
                    int64_t n_on, double c_id, const double* __restrict__ sig_local,
-                   const double* __restrict__ Lsig, double* __restrict__ u) {
+                   const double* __restrict__ Lsig, double* __restrict__ u, int G) {
     extern __shared__ __align__(128) double2 ring[];      // [warps][STG][TD*cols2]
     __shared__ __align__(8) uint64_t bars[kNearWarps * kNearStages];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -54,25 +56,9 @@ near_stream_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
         fence_mbar_init();
     }
     __syncwarp();
-    // balanced target range of this warp: cost(t) = row_ptr[t] + t
-    const int64_t W = (int64_t)gridDim.x * kNearWarps;
     const int64_t gw = (int64_t)blockIdx.x * kNearWarps + w;
-    const int64_t total = row_ptr[T] + T;
-    auto first_target = [&](int64_t c) {      // smallest t with row_ptr[t] + t >= c
-        int64_t lo = 0, hi = T;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (row_ptr[mid] + mid < c) lo = mid + 1; else hi = mid;
-        }
-        return lo;
-    };
-    int64_t ta = 0, tb = 0;
-    if (lane == 0) {
-        ta = first_target((total * gw) / W);
-        tb = first_target((total * (gw + 1)) / W);
-    }
-    ta = __shfl_sync(0xffffffffu, ta, 0);
-    tb = __shfl_sync(0xffffffffu, tb, 0);
+    const int64_t ta = gw * G;
+    const int64_t tb = ta + G < T ? ta + G : T;
     if (ta >= tb) return;
     const int64_t pa = row_ptr[ta], pb = row_ptr[tb];
     const double2* B = reinterpret_cast<const double2*>(blocks);
@@ -141,21 +127,20 @@ near_stream_kernel(int64_t T, int cols2, const int64_t* __restrict__ row_ptr,
 static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, const int64_t* row_ptr,
                                      const int32_t* panel_idx, const double* blocks, const double* sigma_c,
                                      const double* partials, int64_t n_chunks, int64_t n_on, double c_id,
-                                     const double* sig_local, const double* Lsig, double* u, cudaStream_t s) {
+                                     const double* sig_local, const double* Lsig, double* u, int G, cudaStream_t s) {
     if (T <= 0) return SLB_OK;
     const int cols2 = cols / 2;
     const size_t smem = (size_t)kNearWarps * kNearStages * tdim * cols2 * 16;
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "near blocks too large for the smem ring");
-    const int per_sm = std::max(1, (int)((227 * 1024) / std::max<size_t>(smem, 1)));
-    const int64_t want = (T + kNearWarps - 1) / kNearWarps;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * std::min(per_sm, 4)));
+    G = std::max(1, G);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
 #define NEAR_LAUNCH(TD, MODE)                                                                               \
     do {                                                                                                    \
         SLB_CUDA(cudaFuncSetAttribute(near_stream_kernel<TD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                       (int)smem));                                                          \
         near_stream_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(T, cols2, row_ptr, panel_idx, blocks,  \
                                                                          sigma_c, partials, n_chunks, n_on, c_id, \
-                                                                         sig_local, Lsig, u);               \
+                                                                         sig_local, Lsig, u, G);            \
     } while (0)
     if (tdim == 1) {
         if (mode == 0) NEAR_LAUNCH(1, 0); else NEAR_LAUNCH(1, 1);
@@ -170,15 +155,15 @@ static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, co
 slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr, const int32_t* panel_idx,
                              const double* blocks, const double* sigma_c, double* u, cudaStream_t s) {
     return near_stream_launch(0, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c, nullptr, 0, 0, 0.0, nullptr,
-                              nullptr, u, s);
+                              nullptr, u, 4, s);
 }
 
 slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, const double* partials,
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
                            const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
-                           const double* Lsig, double* u, cudaStream_t s) {
+                           const double* Lsig, double* u, int G, cudaStream_t s) {
     return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
-                              n_on, c_id, sig_local, Lsig, u, s);
+                              n_on, c_id, sig_local, Lsig, u, G, s);
 }
 
 // ------------------------------------------------------------------ fold (setup)
@@ -300,3 +285,13 @@ extern "C" slb_status slb_fill_blocks(uint64_t seed, uint64_t first, int64_t cou
     ++g_launch_count;
     return check_launch("fill_blocks_kernel");
 }
+
+namespace slb {
+// targets per warp for the streaming near kernel: about 48 blocks of streaming per warp
+int near_group_size(int64_t T, int64_t nnz) {
+    if (const char* e = getenv("SLB_NEAR_G")) return std::max(1, atoi(e));
+    if (T <= 0) return 1;
+    const double avg = (double)nnz / (double)T;
+    return (int)std::min<double>(16.0, std::max<double>(1.0, std::floor(48.0 / std::max(avg, 1e-9))));
+}
+}  // namespace slb

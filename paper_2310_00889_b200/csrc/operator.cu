@@ -259,6 +259,11 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         OPCUDA(cudaMemcpy(op->bodyc, bc.data(), sizeof(double) * nb * 16, cudaMemcpyHostToDevice));
     }
     for (auto& e : op->ev) OPCUDA(cudaEventCreate(&e));
+    if (T > 0) {
+        int64_t nnz = 0;
+        OPCUDA(cudaMemcpy(&nnz, d->row_ptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        op->near_G = near_group_size(T, nnz);
+    }
     if (op->use_const) {
         OPCUDA(cudaMalloc(&op->rec, sizeof(double) * op->M * 10));
         for (auto& w : op->ws) OPCUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
@@ -342,7 +347,7 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     }
     SLB_CUDA(cudaEventRecord(op->ev[3], s));
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
-                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, s);
+                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, op->near_G, s);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[4], s));
     op->timed = true;

@@ -96,5 +96,6 @@ struct slb_operator {
     cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaGraphExec_t graph = nullptr;
     int64_t const_launches = 0;
+    int near_G = 1;                     // targets per warp in the near stream kernel
 };
 
