@@ -292,6 +292,6 @@ int near_group_size(int64_t T, int64_t nnz) {
     if (const char* e = getenv("SLB_NEAR_G")) return std::max(1, atoi(e));
     if (T <= 0) return 1;
     const double avg = (double)nnz / (double)T;
-    return (int)std::min<double>(16.0, std::max<double>(1.0, std::floor(48.0 / std::max(avg, 1e-9))));
+    return (int)std::min<double>(16.0, std::max<double>(1.0, std::round(48.0 / std::max(avg, 1e-9))));
 }
 }  // namespace slb
