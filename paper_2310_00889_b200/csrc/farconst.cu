@@ -69,8 +69,8 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
     }
 }
 
-template <int KIND, int J, int BUF, int CM>
-__global__ void __launch_bounds__(kConstThreads, 4)
+template <int KIND, int J, int BUF, int CM, int UNR = 4, int MINB = 4>
+__global__ void __launch_bounds__(kConstThreads, MINB)
 far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
                  double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
     constexpr int D = (KIND == FAR_LAPLACE) ? 1 : 3;
@@ -88,7 +88,7 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
     bool anyz = false;
     unsigned zc0 = 0;
     const double* base = c_rec[BUF];
-#pragma unroll 4
+#pragma unroll UNR
     for (int m = 0; m < n_src; ++m) const_pairs<KIND, J, CM>(x, base + kRec * m, acc, anyz, zc0);
     if (CM == 1 && zc0) {
         bool any = false;
@@ -141,10 +141,32 @@ static int const_count_mode() {
     return v;
 }
 
+static int const_variant() {
+    static int v = -1;
+    if (v < 0) { const char* e = getenv("SLB_CONST_VARIANT"); v = e ? atoi(e) : 0; }
+    return v;
+}
+
+template <int KIND, int BUF, int J, int UNR, int MINB>
+static void launch_tile_v(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
+                          cudaStream_t s) {
+    const unsigned grid = (unsigned)((T + kConstThreads * J - 1) / (kConstThreads * J));
+    far_const_kernel<KIND, J, BUF, 1, UNR, MINB><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+}
+
 template <int KIND, int BUF>
 static void launch_tile(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
                         cudaStream_t s) {
     const unsigned grid = (unsigned)((T + kConstThreads * kJ - 1) / (kConstThreads * kJ));
+    if (KIND == FAR_STOKES_SLDL && const_variant() != 0) {
+        switch (const_variant()) {
+            case 1: launch_tile_v<KIND, BUF, 2, 2, 4>(T, x, n, first, part, zc, s); return;
+            case 2: launch_tile_v<KIND, BUF, 2, 8, 4>(T, x, n, first, part, zc, s); return;
+            case 3: launch_tile_v<KIND, BUF, 3, 2, 3>(T, x, n, first, part, zc, s); return;
+            case 4: launch_tile_v<KIND, BUF, 1, 8, 8>(T, x, n, first, part, zc, s); return;
+            default: launch_tile_v<KIND, BUF, 4, 1, 2>(T, x, n, first, part, zc, s); return;
+        }
+    }
     if (const_count_mode() == 1)
         far_const_kernel<KIND, kJ, BUF, 1><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
     else
