@@ -183,6 +183,7 @@ slb_status finalize_launch(const FarPlan& plan, int64_t n_trg, int tdim, int col
                            double c_id, const double* sig_local, const double* Lsig, double* u,
                            int G, cudaStream_t s);
 int near_group_size(int64_t T, int64_t nnz);
+slb_status csr_check(int64_t T, const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels);
 slb_status fold_launch(FarKind kind, int64_t n_trg, const double* x_trg, const int64_t* row_ptr,
                        const int32_t* panel_idx, const InterpParams& ip, const double* y_fine,
                        const double* n_fine, const double* w_fine, const double* eta_fine,

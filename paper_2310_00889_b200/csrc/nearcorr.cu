@@ -295,3 +295,35 @@ int near_group_size(int64_t T, int64_t nnz) {
     return (int)std::min<double>(16.0, std::max<double>(1.0, std::round(48.0 / std::max(avg, 1e-9))));
 }
 }  // namespace slb
+
+namespace slb {
+// CSR sanity check (setup): flags[0] |= 1 if row_ptr[0] != 0 or not monotone, |= 2 if a panel id is
+// outside [0, n_panels).
+__global__ void csr_check_kernel(int64_t T, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
+                                 int64_t n_panels, int* __restrict__ flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0 && row_ptr[0] != 0) atomicOr(flags, 1);
+    if (i < T && row_ptr[i + 1] < row_ptr[i]) atomicOr(flags, 1);
+    if (i < T) {
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1] && p >= row_ptr[i]; ++p) {
+            const int64_t k = panel_idx[p];
+            if (k < 0 || k >= n_panels) { atomicOr(flags, 2); break; }
+        }
+    }
+}
+
+slb_status csr_check(int64_t T, const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels) {
+    int* f = nullptr;
+    SLB_CUDA(cudaMalloc(&f, sizeof(int)));
+    SLB_CUDA(cudaMemset(f, 0, sizeof(int)));
+    csr_check_kernel<<<(unsigned)((T + 256) / 256), 256>>>(T, row_ptr, panel_idx, n_panels, f);
+    ++g_launch_count;
+    int h = 0;
+    cudaError_t e = cudaMemcpy(&h, f, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(f);
+    if (e != cudaSuccess) { set_error(std::string("csr_check: ") + cudaGetErrorString(e)); return SLB_ERR_CUDA; }
+    if (h & 1) { set_error("row_ptr must start at 0 and be nondecreasing"); return SLB_ERR_INVALID_ARG; }
+    if (h & 2) { set_error("panel_idx entry outside [0, n_panels_global)"); return SLB_ERR_INVALID_ARG; }
+    return SLB_OK;
+}
+}  // namespace slb

@@ -201,6 +201,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     OPCUDA(cudaMalloc(&op->u_dev, sizeof(double) * std::max<int64_t>(T * op->tdim, 1)));
     OPCUDA(cudaMemset(op->dyn, 0, sizeof(double) * op->M * 4));
     OPCUDA(cudaMemset(op->coarse, 0, sizeof(double) * d->n_panels_global * op->cols));
+    if (T > 0) OPST(csr_check(T, d->row_ptr, d->panel_idx, d->n_panels_global));
     const int64_t f0 = d->panel_begin * op->Mn;
     OPST(pack_geo(op->kind, op->M, d->y_fine, d->n_fine, d->eta_fine, d->eta, op->geo, s));
     OPST(pack_scale(op->kind, Mloc, d->n_fine + 3 * f0, d->w_fine + f0, d->eta_fine ? d->eta_fine + f0 : nullptr,

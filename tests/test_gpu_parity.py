@@ -264,3 +264,23 @@ def test_const_path_fewer_tiles_than_buffers(S, monkeypatch):
     pr = make_config("c1", panels=1, n_extra=5)      # 1 panel: 480 fine sources = 3 tiles < 4 buffers
     err, u, _ = _matvec_vs_oracle(S, pr)
     assert err <= TOL, err
+
+
+def test_operator_rejects_bad_csr(S):
+    from paper_2310_00889_b200 import Operator, SlbError
+    pr = make_config("c2", panels=4)
+    rp = pr.row_ptr.copy()
+    pi = pr.panel_idx.copy()
+    pi[5] = pr.P + 3                          # panel id out of range
+    blocks = torch.zeros(pr.nnz * pr.block_len, dtype=torch.float64, device="cuda")
+    kw = dict(kernel=pr.kernel, ns=pr.Ns, nt=pr.Nt, ms=pr.Ms, mt=pr.Mt, n_panels_global=pr.P, panel_begin=0,
+              panel_end=pr.P, x_trg=cu(pr.x_trg), n_on=pr.n_on, y_fine=cu(pr.y_f), n_fine=cu(pr.n_f),
+              w_fine=cu(pr.w_f), blocks=blocks, eta_fine=cu(pr.eta_f))
+    with pytest.raises(SlbError, match="panel_idx"):
+        Operator(row_ptr=cu(rp, torch.int64), panel_idx=cu(pi, torch.int32), **kw)
+    rp2 = rp.copy()
+    rp2[10] = rp2[11] + 1                     # non-monotone
+    with pytest.raises(SlbError, match="row_ptr"):
+        Operator(row_ptr=cu(rp2, torch.int64), panel_idx=cu(pr.panel_idx, torch.int32), **kw)
+    with pytest.raises(SlbError):
+        S.slb_farfield_stokes_sldl(cu(pr.x_trg), cu(pr.y_f), cu(pr.n_f), cu(pr.w_f), cu(np.zeros((pr.M, 3))), eta=-1.0)
