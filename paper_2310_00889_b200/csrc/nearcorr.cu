@@ -304,8 +304,10 @@ __global__ void csr_check_kernel(int64_t T, const int64_t* __restrict__ row_ptr,
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0 && row_ptr[0] != 0) atomicOr(flags, 1);
     if (i < T && row_ptr[i + 1] < row_ptr[i]) atomicOr(flags, 1);
-    if (i < T) {
-        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1] && p >= row_ptr[i]; ++p) {
+    const int64_t nnz = row_ptr[T];
+    if (i < T && (row_ptr[i + 1] > nnz || row_ptr[i] < 0)) atomicOr(flags, 1);
+    if (i < T && row_ptr[i] >= 0 && row_ptr[i + 1] <= nnz) {
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
             const int64_t k = panel_idx[p];
             if (k < 0 || k >= n_panels) { atomicOr(flags, 2); break; }
         }
