@@ -3,7 +3,7 @@ of one rank's slb_operator (no method arithmetic here: slicing, copying, seeded 
 import numpy as np
 import torch
 
-from paper_2310_00889_b200 import Operator, partition_panels, slb_fill_blocks
+from paper_2310_00889_b200 import Operator, partition_panels, slb_fill_blocks, slb_nearcorr_quad
 
 
 def local_rows(pr, rank, nranks):
@@ -27,7 +27,9 @@ def _segments(rows):
 
 
 class DeviceProblem:
-    def __init__(self, pr, rank=0, nranks=1, device="cuda", fold=True, comm=None, blocks=None):
+    def __init__(self, pr, rank=0, nranks=1, device="cuda", fold=True, comm=None, blocks=None, quad=None):
+        """blocks: None -> seeded synthetic B (R10); quad=dict(order=.., beta=..) -> special-quadrature
+        B computed on the GPU by slb_nearcorr_quad (N1)."""
         self.pr = pr
         rows, pb, pe, n_on, ranges = local_rows(pr, rank, nranks)
         self.rows, self.pb, self.pe, self.n_on, self.ranges = rows, pb, pe, n_on, ranges
@@ -41,7 +43,9 @@ class DeviceProblem:
         pidx = np.concatenate([pr.panel_idx[rp[a]:rp[b]] for a, b in segs]) if segs else np.zeros(0, np.int32)
         self.nnz = int(row_ptr[-1])
         blen = pr.block_len
-        if blocks is None:
+        if quad is not None:
+            self.blocks = torch.empty(max(self.nnz * blen, 2), dtype=torch.float64, device=dev)
+        elif blocks is None:
             self.blocks = torch.empty(max(self.nnz * blen, 2), dtype=torch.float64, device=dev)
             off = 0
             for a, b in segs:
@@ -52,8 +56,17 @@ class DeviceProblem:
         else:
             self.blocks = blocks
         self.x_trg = f64(pr.x_trg[rows])
+        if quad is not None and self.nnz > 0:
+            trg_node = torch.from_numpy(np.where(rows < pr.n_on, rows, -1).astype(np.int64)).to(dev)
+            eta_panel = f64(pr.eta_body[pr.body_of_panel]) if pr.kernel == 2 else None
+            rp_d = torch.from_numpy(row_ptr).to(dev)
+            pi_d = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
+            slb_nearcorr_quad(pr.kernel, self.x_trg, rp_d, pi_d, pr.Ns, pr.Nt,
+                              f64(pr.y_c.reshape(pr.P, pr.Nn, 3)), self.blocks, trg_node=trg_node,
+                              eta_panel=eta_panel, order=quad.get("order", 12), beta=quad.get("beta", 0.6))
         self.y_f, self.n_f, self.w_f = f64(pr.y_f), f64(pr.n_f), f64(pr.w_f)
-        self.eta_f = f64(pr.eta_f) if pr.kernel == 2 else None
+        # pure double layer (all eta = 0) runs the DL kernel: eta_fine must then be NULL
+        self.eta_f = f64(pr.eta_f) if (pr.kernel == 2 and np.any(pr.eta_f != 0)) else None
         self.row_ptr = torch.from_numpy(row_ptr).to(dev)
         self.panel_idx = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
         sig = pr.sigma.reshape(pr.N, pr.sdim)[pb * pr.Nn:pe * pr.Nn]

@@ -128,6 +128,20 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
                              const double* w_fine, const double* eta_fine, double eta,
                              double* blocks, cudaStream_t s);
 
+/* (NEXT N1, setup) Special-quadrature blocks B for the CSR pairs (§3.2.3-3.2.4,
+ * P:L1195-1354): B_{t,k}[r][(i,j,c)] = int int_{Gamma_k} K_rc(x_t - y; n) l_i(s) C_j(th) J ds dth, the
+ * exact action of the layer potential on panel k's interpolant, by a singularity-resolving
+ * adaptive rule: geometry interpolated from the panel's coarse nodes
+ * y_coarse [n_panels][ns][nt][3]; trg_node[t] = global coarse node id if target t is that node
+ * (on-surface, singular) else -1 (may be NULL: all off-surface); eta_panel [n_panels] (Stokes
+ * eta S + D; NULL for Laplace DL); order = GL points per cell direction (4..24), beta = accepted
+ * distance / cell diameter.  blocks [nnz][tdim][ns*nt*sdim] written (unfolded B).  Synchronises s.
+ * SLB_ERR_UNSUPPORTED if a target is too close for the cell budget. */
+slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                             const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
+                             const double* y_coarse, const double* eta_panel, int order, double beta,
+                             double* blocks, cudaStream_t s);
+
 /* Synthetic special-quadrature blocks (input generation, R10):
  *   blocks[q] = ((2 u_q - 1) sqrt(3)) s_blk,  u_q = (splitmix64(seed, first + q) >> 11) 2^-53,
  *   q in [0, count).  Bit-identical to the oracle's definition. */

@@ -39,6 +39,7 @@ _SIGS = {
     "slb_nearcorr_apply": (I32, [I64, I32, I32, I32, P, P, P, P, P, P]),
     "slb_nearcorr_fold": (I32, [I32, I64, P, P, P, I32, I32, I32, I32, P, P, P, P, D, P, P]),
     "slb_fill_blocks": (I32, [ctypes.c_uint64, ctypes.c_uint64, I64, D, P, P]),
+    "slb_nearcorr_quad": (I32, [I32, I64, P, P, P, P, I32, I32, P, P, I32, D, P, P]),
     "slb_near_build": (I32, [I64, P, I64, I32, P, P, P, P, P, I64, ctypes.POINTER(I64), P]),
     "slb_comm_unique_id": (I32, [P]),
     "slb_comm_create": (I32, [P, I32, I32, ctypes.POINTER(P)]),

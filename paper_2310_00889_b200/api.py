@@ -98,6 +98,17 @@ def slb_nearcorr_fold(kernel, x_trg, row_ptr, panel_idx, ns, nt, ms, mt, y_fine,
     return blocks
 
 
+def slb_nearcorr_quad(kernel, x_trg, row_ptr, panel_idx, ns, nt, y_coarse, blocks, trg_node=None, eta_panel=None,
+                      order=12, beta=0.6):
+    """Special-quadrature blocks B for the CSR pairs (unfolded), written into `blocks`."""
+    T = row_ptr.shape[0] - 1
+    check(lib().slb_nearcorr_quad(kernel, T, _dev(x_trg, "x_trg"), _dev(trg_node, "trg_node", torch.int64, True),
+                                  _dev(row_ptr, "row_ptr", torch.int64), _dev(panel_idx, "panel_idx", torch.int32),
+                                  ns, nt, _dev(y_coarse, "y_coarse"), _dev(eta_panel, "eta_panel", allow_none=True),
+                                  int(order), float(beta), _dev(blocks, "blocks"), _stream()))
+    return blocks
+
+
 def slb_fill_blocks(seed, first, count, s_blk, out):
     check(lib().slb_fill_blocks(ctypes.c_uint64(seed), ctypes.c_uint64(first), count, float(s_blk),
                                 _dev(out, "blocks"), _stream()))

@@ -1,0 +1,408 @@
+// nearquad.cu -- (NEXT N1, setup) special-quadrature correction blocks.
+//
+// PAPER.md §3.2.3-3.2.4: for a target x near element Gamma_k (or on it), the
+// correction E_ij(x) = (special quadrature of K against the interpolation basis) - G(x, y_ij) w_ij.
+// This kernel computes the first part,
+//     B_{t,k}[r][(i,j,c)] = int_{I_k} int_0^{2pi} K_rc(x_t - y(s,th); n(s,th)) l_i(s) C_j(th) J(s,th) dth ds,
+// i.e. the exact action of the layer potential on the panel's interpolant (P:L1233-1239 with the
+// adaptive rule written out), for every (target, near panel) pair of a CSR; the operator folds
+// the smooth-rule part in at creation as for any B (E = B - G U).
+//
+// The paper's rules (toroidal Green's-function modal sums with generalized Chebyshev tables,
+// App. B) are replaced by a singularity-resolving adaptive rule built on the fly:
+//   * geometry y(s,th), y_s, y_th from the panel's coarse nodes by the same Lagrange x trig
+//     interpolation the paper uses to represent the surface;
+//   * closest point (t*, th*) by Gauss-Newton from the nearest node;
+//   * quadtree cells in the locally scaled parameter plane (a = S_t (t - t*), b = S_th (th - th*)),
+//     accepted when sqrt(d^2 + dist(cell)^2) >= beta * diag(cell) (flat-surface proxy), split otherwise;
+//   * on-surface targets (d = 0): the four cells meeting at the node are integrated with the Duffy
+//     transform (two triangles each, Jacobian u cancels the 1/r singularity), refined until their
+//     aspect ratio and size are moderate;
+//   * q x q Gauss-Legendre per regular cell, 2 q_d^2 nodes per Duffy cell; the contraction with
+//     the basis is batched (128 nodes at a time) through shared memory.
+// One CTA per target row; fixed summation order -> deterministic.
+#include <algorithm>
+#include <cmath>
+#include "common.cuh"
+
+namespace slb {
+
+constexpr int kQThreads = 128;
+constexpr int kMaxCells = 768;
+constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
+
+struct QuadParams {
+    int ns, nt, q, qd;
+    double beta;
+    double tgl[kMaxNsQ];      // panel GL nodes on [-1,1]
+    double lam[kMaxNsQ];      // barycentric weights
+    double gx[kMaxQ], gw[kMaxQ];        // q-point GL on [-1,1]
+    double dx[kMaxQ], dw[kMaxQ];        // qd-point GL on [0,1]
+};
+
+struct Cell {
+    double t0, t1, h0, h1;    // parameter rectangle (t in [-1,1], th relative to th*)
+    int duffy;                // 0 regular; 1 Duffy with singular corner (t*, th*)
+    int nodes;
+    int offset;
+};
+
+// Lagrange basis l_i(t) and l_i'(t) (barycentric second form + derivative formula)
+__device__ void lagrange_eval(const QuadParams& P, double t, double* l, double* dl) {
+    const int n = P.ns;
+    int hit = -1;
+    for (int i = 0; i < n; ++i)
+        if (fabs(t - P.tgl[i]) < 1e-15) hit = i;
+    if (hit >= 0) {
+        // l_i(t_k) = delta; l_i'(t_k) = (lam_i/lam_k)/(t_k - t_i) (i != k), l_k'(t_k) = -sum_{i != k} l_i'(t_k)
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) {
+            l[i] = (i == hit) ? 1.0 : 0.0;
+            if (i != hit) {
+                dl[i] = (P.lam[i] / P.lam[hit]) / (P.tgl[hit] - P.tgl[i]);
+                s += dl[i];
+            }
+        }
+        dl[hit] = -s;
+        return;
+    }
+    double den = 0.0, dden = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double c = P.lam[i] / (t - P.tgl[i]);
+        den += c;
+        dden -= c / (t - P.tgl[i]);
+    }
+    for (int i = 0; i < n; ++i) {
+        const double c = P.lam[i] / (t - P.tgl[i]);
+        const double dc = -c / (t - P.tgl[i]);
+        l[i] = c / den;
+        dl[i] = (dc * den - c * dden) / (den * den);
+    }
+}
+
+// trig cardinal C_j(th) and C_j'(th), th_j = 2 pi j / N (real interpolant with the Nyquist cosine)
+__device__ void trig_eval(int N, double th, double* C, double* dC) {
+    for (int j = 0; j < N; ++j) {
+        const double p = th - 2.0 * kPi * j / N;
+        double sv = 1.0, dv = 0.0;
+        double c1, s1;
+        sincos(p, &s1, &c1);
+        double ck = c1, sk = s1;      // cos(l p), sin(l p) by rotation
+        for (int l = 1; l < N / 2; ++l) {
+            sv += 2.0 * ck;
+            dv -= 2.0 * l * sk;
+            const double cn = ck * c1 - sk * s1, sn = sk * c1 + ck * s1;
+            ck = cn; sk = sn;
+        }
+        // l = N/2 term (ck, sk now hold cos/sin((N/2) p))
+        sv += ck;
+        dv -= 0.5 * N * sk;
+        C[j] = sv / N;
+        dC[j] = dv / N;
+    }
+}
+
+// surface point and tangents from the panel's nodes Y[i][j][3]
+__device__ void geom_eval(const QuadParams& P, const double* Y, double t, double th, double* y, double* yt,
+                          double* yh, double* lbuf, double* dlbuf, double* Cb, double* dCb) {
+    lagrange_eval(P, t, lbuf, dlbuf);
+    trig_eval(P.nt, th, Cb, dCb);
+    for (int c = 0; c < 3; ++c) { y[c] = 0.0; yt[c] = 0.0; yh[c] = 0.0; }
+    for (int i = 0; i < P.ns; ++i) {
+        double a[3] = {0, 0, 0}, ad[3] = {0, 0, 0};
+        for (int j = 0; j < P.nt; ++j) {
+            const double* Yij = Y + (i * P.nt + j) * 3;
+            for (int c = 0; c < 3; ++c) { a[c] = fma(Cb[j], Yij[c], a[c]); ad[c] = fma(dCb[j], Yij[c], ad[c]); }
+        }
+        for (int c = 0; c < 3; ++c) {
+            y[c] = fma(lbuf[i], a[c], y[c]);
+            yt[c] = fma(dlbuf[i], a[c], yt[c]);
+            yh[c] = fma(lbuf[i], ad[c], yh[c]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kQThreads)
+nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ trg_node,
+                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
+                const double* __restrict__ y_coarse, const double* __restrict__ eta_panel,
+                const __grid_constant__ QuadParams P, double* __restrict__ blocks, int* __restrict__ status) {
+    extern __shared__ double sm[];
+    const int ns = P.ns, nt = P.nt, Nn = ns * nt;
+    const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
+    const int NG = TD * TD;
+    const int tid = threadIdx.x;
+    // shared layout
+    double* Y = sm;                                   // [Nn][3]
+    double* Bacc = Y + Nn * 3;                        // [NG][ns][nt]
+    double* Gs = Bacc + NG * Nn;                      // [128][NG]
+    double* Ls = Gs + kQThreads * NG;                 // [128][ns]
+    double* Cs = Ls + kQThreads * ns;                 // [128][nt]
+    Cell* cells = reinterpret_cast<Cell*>(Cs + kQThreads * nt);
+    __shared__ double s_par[8];                       // t*, th*, d, St, Sh, node-singular flag
+    __shared__ int s_ncell, s_ntot, s_fail;
+    // per-thread scratch for the interpolation (registers / local)
+    double lb[kMaxNsQ], dlb[kMaxNsQ], Cb[kMaxNtQ], dCb[kMaxNtQ];
+
+    const int64_t t = blockIdx.x;
+    if (t >= T) return;
+    const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
+    const int64_t node = trg_node ? trg_node[t] : -1;
+    for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
+        const int64_t k = panel_idx[p];
+        const double eta = (kind == FAR_STOKES_SLDL) ? eta_panel[k] : 0.0;
+        for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[k * Nn * 3 + e];
+        for (int e = tid; e < NG * Nn; e += kQThreads) Bacc[e] = 0.0;
+        __syncthreads();
+        // ---------------- closest point and the cell list (thread 0)
+        if (tid == 0) {
+            s_fail = 0;
+            const bool singular = (node >= k * Nn && node < (k + 1) * Nn);
+            double ts, hs;
+            if (singular) {
+                const int loc = (int)(node - k * Nn);
+                ts = P.tgl[loc / nt];
+                hs = 2.0 * kPi * (loc % nt) / nt;
+            } else {
+                double best = 1e300;
+                ts = 0.0; hs = 0.0;
+                for (int i = 0; i < ns; ++i)
+                    for (int j = 0; j < nt; ++j) {
+                        const double* Yij = Y + (i * nt + j) * 3;
+                        const double d2 = (x0 - Yij[0]) * (x0 - Yij[0]) + (x1 - Yij[1]) * (x1 - Yij[1]) +
+                                          (x2 - Yij[2]) * (x2 - Yij[2]);
+                        if (d2 < best) { best = d2; ts = P.tgl[i]; hs = 2.0 * kPi * j / nt; }
+                    }
+                // Gauss-Newton on |x - y(t,th)|^2, t clamped to [-1, 1]
+                for (int it = 0; it < 12; ++it) {
+                    double y[3], yt[3], yh[3];
+                    geom_eval(P, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb);
+                    const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
+                    const double a11 = yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2];
+                    const double a22 = yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2];
+                    const double a12 = yt[0] * yh[0] + yt[1] * yh[1] + yt[2] * yh[2];
+                    const double g1 = r[0] * yt[0] + r[1] * yt[1] + r[2] * yt[2];
+                    const double g2 = r[0] * yh[0] + r[1] * yh[1] + r[2] * yh[2];
+                    const double det = a11 * a22 - a12 * a12;
+                    if (!(det > 0.0)) break;
+                    double dt = (a22 * g1 - a12 * g2) / det, dh = (a11 * g2 - a12 * g1) / det;
+                    const double tn = fmin(1.0, fmax(-1.0, ts + dt));
+                    if (tn != ts + dt) dh = g2 / a22;      // on the boundary: 1-D step in th
+                    dt = tn - ts;
+                    ts = tn;
+                    hs += dh;
+                    if (fabs(dt) + fabs(dh) < 1e-15) break;
+                }
+            }
+            double y[3], yt[3], yh[3];
+            geom_eval(P, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb);
+            const double d = singular ? 0.0
+                                      : sqrt((x0 - y[0]) * (x0 - y[0]) + (x1 - y[1]) * (x1 - y[1]) +
+                                             (x2 - y[2]) * (x2 - y[2]));
+            const double St = sqrt(yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2]);
+            const double Sh = sqrt(yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2]);
+            s_par[0] = ts; s_par[1] = hs; s_par[2] = d; s_par[3] = St; s_par[4] = Sh;
+            // quadtree over the parameter rectangle [-1,1] x [hs - pi, hs + pi], split at (ts, hs)
+            Cell stack[64];
+            int sp = 0, nc = 0, ntot = 0;
+            const double T0[2] = {-1.0, ts}, T1[2] = {ts, 1.0};
+            const double H0[2] = {-kPi, 0.0}, H1[2] = {0.0, kPi};
+            for (int a = 0; a < 2; ++a)
+                for (int b = 0; b < 2; ++b) {
+                    if (T1[a] - T0[a] <= 0.0) continue;
+                    Cell c;
+                    c.t0 = T0[a]; c.t1 = T1[a]; c.h0 = H0[b]; c.h1 = H1[b];
+                    c.duffy = singular ? 1 : 0;
+                    stack[sp++] = c;
+                }
+            const double cap = 2.0 * Sh;   // ~ tube diameter: keeps the opposite wall resolved
+            while (sp > 0) {
+                Cell c = stack[--sp];
+                const double wa = (c.t1 - c.t0) * St, wb = (c.h1 - c.h0) * Sh;
+                const double diag = sqrt(wa * wa + wb * wb);
+                bool accept;
+                if (c.duffy) {
+                    accept = (fmax(wa, wb) <= 2.5 * fmin(wa, wb)) && diag <= cap;
+                } else {
+                    // distance from (t*, th*) to the cell in scaled coordinates, plus the normal offset
+                    const double da = (c.t0 > ts) ? (c.t0 - ts) * St : ((c.t1 < ts) ? (ts - c.t1) * St : 0.0);
+                    const double db = (c.h0 > 0.0) ? c.h0 * Sh : ((c.h1 < 0.0) ? -c.h1 * Sh : 0.0);
+                    const double dist = sqrt(d * d + da * da + db * db);
+                    accept = dist >= P.beta * diag && diag <= 2.0 * cap;
+                }
+                if (accept) {
+                    if (nc >= kMaxCells) { s_fail = 1; break; }
+                    c.nodes = c.duffy ? 2 * P.qd * P.qd : P.q * P.q;
+                    c.offset = ntot;
+                    ntot += c.nodes;
+                    cells[nc++] = c;
+                    continue;
+                }
+                if (sp + 4 > 64) { s_fail = 2; break; }
+                // split: the longer side in two (or both if comparable); Duffy keeps its corner cell
+                const bool sa = wa >= 0.5 * wb, sb = wb >= 0.5 * wa;
+                const double tm = 0.5 * (c.t0 + c.t1), hm = 0.5 * (c.h0 + c.h1);
+                const double ta[3] = {c.t0, sa ? tm : c.t1, c.t1};
+                const double ha[3] = {c.h0, sb ? hm : c.h1, c.h1};
+                for (int a = 0; a < (sa ? 2 : 1); ++a)
+                    for (int b = 0; b < (sb ? 2 : 1); ++b) {
+                        Cell s;
+                        s.t0 = ta[a]; s.t1 = ta[a + 1]; s.h0 = ha[b]; s.h1 = ha[b + 1];
+                        // the singular corner is (ts, 0): a sub-cell keeps Duffy if it touches it
+                        const bool touch = (s.t0 == ts || s.t1 == ts) && (s.h0 == 0.0 || s.h1 == 0.0);
+                        s.duffy = c.duffy && touch;
+                        stack[sp++] = s;
+                    }
+            }
+            s_ncell = nc;
+            s_ntot = ntot;
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) atomicOr(status, s_fail);
+            __syncthreads();
+            continue;
+        }
+        const double ts = s_par[0], hs = s_par[1];
+        const int nc = s_ncell, ntot = s_ntot;
+        // ---------------- quadrature nodes in batches of kQThreads
+        for (int base = 0; base < ntot; base += kQThreads) {
+            const int g = base + tid;
+            double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            if (g < ntot) {
+                int lo = 0, hi = nc - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (cells[mid].offset <= g) lo = mid; else hi = mid - 1;
+                }
+                const Cell c = cells[lo];
+                const int li = g - c.offset;
+                double tt, hh, W;
+                if (!c.duffy) {
+                    const int a = li / P.q, b = li % P.q;
+                    const double ht = 0.5 * (c.t1 - c.t0), hh2 = 0.5 * (c.h1 - c.h0);
+                    tt = c.t0 + ht * (P.gx[a] + 1.0);
+                    hh = c.h0 + hh2 * (P.gx[b] + 1.0);
+                    W = P.gw[a] * P.gw[b] * ht * hh2;
+                } else {
+                    // rectangle with the singular corner at (ts, 0): corner C0, opposite corners
+                    const double ct = (c.t0 == ts) ? c.t0 : c.t1, ch = (c.h0 == 0.0) ? c.h0 : c.h1;
+                    const double ot = (c.t0 == ts) ? c.t1 : c.t0, oh = (c.h0 == 0.0) ? c.h1 : c.h0;
+                    const int tri = li / (P.qd * P.qd), r = li % (P.qd * P.qd);
+                    const int ia = r / P.qd, ib = r % P.qd;
+                    const double u = P.dx[ia], v = P.dx[ib];
+                    // triangle 0: C0, (ot, ch), (ot, oh); triangle 1: C0, (ot, oh), (ct, oh)
+                    double At, Ah, Bt, Bh;
+                    if (tri == 0) { At = ot - ct; Ah = 0.0; Bt = ot - ct; Bh = oh - ch; }
+                    else { At = ot - ct; Ah = oh - ch; Bt = 0.0; Bh = oh - ch; }
+                    tt = ct + u * (At + v * (Bt - At));
+                    hh = ch + u * (Ah + v * (Bh - Ah));
+                    W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
+                }
+                double y[3], yt[3], yh[3];
+                geom_eval(P, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb);
+                // outward normal (R8): n = y_th x y_t / |.|, J = |y_th x y_t|
+                const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
+                                      yh[0] * yt[1] - yh[1] * yt[0]};
+                const double J = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+                const double nrm[3] = {cr[0] / J, cr[1] / J, cr[2] / J};
+                const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
+                const double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+                const double wJ = W * J;
+                if (r2 > 0.0) {
+                    const double ir = 1.0 / sqrt(r2);
+                    const double rn = r[0] * nrm[0] + r[1] * nrm[1] + r[2] * nrm[2];
+                    if (kind == FAR_LAPLACE) {
+                        G[0] = rn * ir * ir * ir / (4.0 * kPi) * wJ;
+                    } else {
+                        const double ir3 = ir * ir * ir;
+                        const double sl = eta / (8.0 * kPi), dl = 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
+                        for (int a = 0; a < 3; ++a)
+                            for (int b = 0; b < 3; ++b)
+                                G[a * 3 + b] = (sl * ((a == b ? ir : 0.0) + r[a] * r[b] * ir3) + dl * r[a] * r[b]) * wJ;
+                    }
+                }
+                for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = G[q2];
+                for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = lb[i];
+                for (int j = 0; j < nt; ++j) Cs[tid * nt + j] = Cb[j];
+            } else {
+                for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = 0.0;
+                for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = 0.0;
+                for (int j = 0; j < nt; ++j) Cs[tid * nt + j] = 0.0;
+            }
+            __syncthreads();
+            const int nb = min(kQThreads, ntot - base);
+            for (int o = tid; o < NG * Nn; o += kQThreads) {
+                const int q2 = o / Nn, ij = o % Nn, i = ij / nt, j = ij % nt;
+                double acc = Bacc[o];
+                for (int n = 0; n < nb; ++n) acc = fma(Gs[n * NG + q2] * Ls[n * ns + i], Cs[n * nt + j], acc);
+                Bacc[o] = acc;
+            }
+            __syncthreads();
+        }
+        // ---------------- write the block: [tdim][node (i,j)][sdim]
+        double* Bp = blocks + p * (int64_t)TD * Nn * TD;
+        for (int o = tid; o < NG * Nn; o += kQThreads) {
+            const int q2 = o / Nn, ij = o % Nn;
+            const int a = q2 / TD, b = q2 % TD;
+            Bp[(a * Nn + ij) * TD + b] = Bacc[o];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace slb
+
+using namespace slb;
+
+extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                                        const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
+                                        const double* y_coarse, const double* eta_panel, int order, double beta,
+                                        double* blocks, cudaStream_t s) {
+    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL, SLB_ERR_INVALID_ARG, "bad kernel");
+    SLB_REQUIRE(n_trg >= 0 && ns >= 2 && nt >= 4 && nt % 2 == 0, SLB_ERR_INVALID_ARG, "bad sizes");
+    SLB_REQUIRE(ns <= kMaxNsQ && nt <= kMaxNtQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
+    SLB_REQUIRE(order >= 4 && order <= kMaxQ && beta > 0.0, SLB_ERR_INVALID_ARG, "need 4 <= order <= 24, beta > 0");
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes needs eta_panel");
+    SLB_REQUIRE(n_trg <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets");
+    static QuadParams P;
+    P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
+    double w[kMaxNsQ];
+    gl_nodes(ns, P.tgl, w);
+    for (int i = 0; i < ns; ++i) {
+        double pr = 1.0;
+        for (int l = 0; l < ns; ++l) if (l != i) pr *= (P.tgl[i] - P.tgl[l]);
+        P.lam[i] = 1.0 / pr;
+    }
+    gl_nodes(P.q, P.gx, P.gw);
+    gl_nodes(P.qd, P.dx, P.dw);
+    for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
+    const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
+    const int Nn = ns * nt;
+    const size_t smem = sizeof(double) * ((size_t)Nn * 3 + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns + nt)) +
+                        sizeof(Cell) * kMaxCells;
+    SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
+    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int* st = nullptr;
+    SLB_CUDA(cudaMallocAsync(&st, sizeof(int), s));
+    SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
+    const FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE : FAR_STOKES_SLDL;
+    nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem, s>>>((int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx,
+                                                             y_coarse, eta_panel, P, blocks, st);
+    ++g_launch_count;
+    slb_status r = check_launch("nearquad_kernel");
+    int h = 0;
+    if (r == SLB_OK) {
+        cudaError_t e = cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { set_error(std::string("nearquad: ") + cudaGetErrorString(e)); r = SLB_ERR_CUDA; }
+    }
+    cudaFreeAsync(st, s);
+    if (r == SLB_OK && h) {
+        set_error("nearquad: adaptive cell budget exceeded (target extremely close to a panel?)");
+        r = SLB_ERR_UNSUPPORTED;
+    }
+    return r;
+}

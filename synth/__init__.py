@@ -13,9 +13,9 @@ Every input is seeded; recipes are stated in DESIGN.md ("Input recipe").
 from .rng import splitmix64, splitmix64_u01, block_entry_reference
 from .geometry import (Body, torus_body, trefoil_body, discretize, gauss_legendre_np,
                        random_rotation)
-from .configs import CONFIGS, make_config, Problem, pin_torus
+from .configs import CONFIGS, make_config, make_torus_problem, Problem, pin_torus
 from .nearlist import build_near_csr
 
 __all__ = ["splitmix64", "splitmix64_u01", "block_entry_reference", "Body", "torus_body",
            "trefoil_body", "discretize", "gauss_legendre_np", "random_rotation", "CONFIGS",
-           "make_config", "Problem", "pin_torus", "build_near_csr"]
+           "make_config", "make_torus_problem", "Problem", "pin_torus", "build_near_csr"]

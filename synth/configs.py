@@ -198,6 +198,20 @@ def _place_loops(rng, n, R_of, rho_of, lo_hi_of, gap_of, max_tries=200000):
 CONFIGS = ("c1", "c2", "c3", "c4", "c5", "c5alt")
 
 
+def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_DL, eta=None, extra_targets=None,
+                       seed_offset=0):
+    """Single torus (axis z, centre 0) with the 2 L_k near rule -- pin problems for the special
+    quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes; eta=0 -> pure DL."""
+    seed = BASE_SEED + 100 + seed_offset
+    rng = np.random.default_rng(seed)
+    b = torus_body(R, rho)
+    pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng)
+    if kernel == STOKES_SLDL and eta is not None:
+        pr.eta_body[:] = eta
+        pr.eta_f[:] = eta
+    return pr
+
+
 def make_config(name: str, **kw) -> Problem:
     """Build one of the BASELINE configs.  Keyword overrides shrink a config for tests
     (n_loops, panels) while keeping its shape and recipe."""
