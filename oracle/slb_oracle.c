@@ -161,6 +161,24 @@ void or_upsample(long n_panels, int ns, int nt, int ms, int mt, int nc,
     free(sg); free(wg); free(sf); free(wf); free(Ps); free(F);
 }
 
+/* Ragged grids (NEXT N4; §3.1: element k has N_s x N_th^(k) nodes):
+ * panel k's coarse block starts at node sum_{k'<k} ns nt[k'], its fine block at
+ * sum_{k'<k} ms mt[k']; each panel is interpolated with its own (nt[k], mt[k]) matrices. */
+void or_upsample_ragged(long n_panels, int ns, const int* nt, int ms, const int* mt, int nc,
+                        const double* sigma_c, double* sigma_f) {
+    long* c0 = malloc(sizeof(long) * (n_panels + 1));
+    long* f0 = malloc(sizeof(long) * (n_panels + 1));
+    c0[0] = f0[0] = 0;
+    for (long p = 0; p < n_panels; ++p) {
+        c0[p + 1] = c0[p] + (long)ns * nt[p];
+        f0[p + 1] = f0[p] + (long)ms * mt[p];
+    }
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (long p = 0; p < n_panels; ++p)
+        or_upsample(1, ns, nt[p], ms, mt[p], nc, sigma_c + c0[p] * nc, sigma_f + f0[p] * nc);
+    free(c0); free(f0);
+}
+
 /* ------------------------------------------------------------------ */
 /* Kernels, written out as their matrices.  r = x - y (target minus source).  */
 /* ------------------------------------------------------------------ */
@@ -349,20 +367,41 @@ typedef struct {
     const int* body_of_node;   /* [N] */
     const double* y_c;         /* [N][3] */
     const double* w_c;         /* [N] */
+    /* ragged angular orders per panel (NEXT N4), or NULL: every panel has (nt, mt) */
+    const int* panel_nt;       /* [n_panels] */
+    const int* panel_mt;       /* [n_panels] */
 } or_problem;
+
+/* node offsets of panel k (coarse c0, fine f0), k = 0..n_panels */
+static void or_offsets(const or_problem* pb, long* c0, long* f0) {
+    c0[0] = f0[0] = 0;
+    for (long k = 0; k < pb->n_panels; ++k) {
+        int nt = pb->panel_nt ? pb->panel_nt[k] : pb->nt;
+        int mt = pb->panel_mt ? pb->panel_mt[k] : pb->mt;
+        c0[k + 1] = c0[k] + (long)pb->ns * nt;
+        f0[k + 1] = f0[k] + (long)pb->ms * mt;
+    }
+}
 
 /* Precompute sigma' (= sigma or sigma - L sigma), its fine upsample, and L sigma. */
 void or_prepare(const or_problem* pb, const double* sigma, double* sigma_p,
                 double* sigma_f, double* Lsigma) {
     int d = kind_dim(pb->kind);
-    long N = pb->n_panels * pb->ns * pb->nt;
+    long* c0 = malloc(sizeof(long) * (pb->n_panels + 1));
+    long* f0 = malloc(sizeof(long) * (pb->n_panels + 1));
+    or_offsets(pb, c0, f0);
+    long N = c0[pb->n_panels];
     if (pb->n_bodies > 0) {
         or_projector(N, pb->y_c, pb->w_c, pb->body_of_node, pb->n_bodies, sigma, Lsigma);
         for (long q = 0; q < N * d; ++q) sigma_p[q] = sigma[q] - Lsigma[q];
     } else {
         for (long q = 0; q < N * d; ++q) { sigma_p[q] = sigma[q]; if (Lsigma) Lsigma[q] = 0.0; }
     }
-    or_upsample(pb->n_panels, pb->ns, pb->nt, pb->ms, pb->mt, d, sigma_p, sigma_f);
+    if (pb->panel_nt)
+        or_upsample_ragged(pb->n_panels, pb->ns, pb->panel_nt, pb->ms, pb->panel_mt, d, sigma_p, sigma_f);
+    else
+        or_upsample(pb->n_panels, pb->ns, pb->nt, pb->ms, pb->mt, d, sigma_p, sigma_f);
+    free(c0); free(f0);
 }
 
 /* u for the listed global target rows; near-correction smooth re-sum done literally. */
@@ -370,9 +409,18 @@ void or_apply_rows(const or_problem* pb, const double* sigma_p, const double* si
                    const double* Lsigma, long n_rows, const long* rows, double* u,
                    double* u_far, double* u_near) {
     int d = kind_dim(pb->kind);
-    long Nn = (long)pb->ns * pb->nt, Mn = (long)pb->ms * pb->mt;
-    long M = pb->n_panels * Mn;
-    long blen = (long)d * Nn * d;
+    long* c0 = malloc(sizeof(long) * (pb->n_panels + 1));
+    long* f0 = malloc(sizeof(long) * (pb->n_panels + 1));
+    or_offsets(pb, c0, f0);
+    long M = f0[pb->n_panels];
+    /* first flat entry of every near block: block p = [d][N_n^(k) d], k = panel_idx[p] */
+    long nnz = pb->row_ptr[pb->n_trg];
+    long* b0 = malloc(sizeof(long) * (nnz + 1));
+    b0[0] = 0;
+    for (long p = 0; p < nnz; ++p) {
+        long k = pb->panel_idx[p];
+        b0[p + 1] = b0[p] + (long)d * (c0[k + 1] - c0[k]) * d;
+    }
     #pragma omp parallel for schedule(dynamic, 1)
     for (long q = 0; q < n_rows; ++q) {
         long t = rows[q];
@@ -382,17 +430,18 @@ void or_apply_rows(const or_problem* pb, const double* sigma_p, const double* si
         or_acc nr[3] = {{0, 0}, {0, 0}, {0, 0}};
         for (long p = pb->row_ptr[t]; p < pb->row_ptr[t + 1]; ++p) {
             long k = pb->panel_idx[p];
+            long Nn = c0[k + 1] - c0[k];
             /* + B_{t,k} sigma'_k */
             for (int i = 0; i < d; ++i)
                 for (long col = 0; col < Nn * d; ++col) {
-                    long flat = p * blen + i * Nn * d + col;
+                    long flat = b0[p] + i * Nn * d + col;
                     double b = pb->blocks ? pb->blocks[flat]
                                           : or_block_entry(pb->blk_seed, (uint64_t)flat, pb->s_blk);
-                    acc_add(&nr[i], b * sigma_p[k * Nn * d + col]);
+                    acc_add(&nr[i], b * sigma_p[c0[k] * d + col]);
                 }
             /* - smooth contribution of panel k's fine nodes (already inside the far sum) */
             or_acc sm[3] = {{0, 0}, {0, 0}, {0, 0}};
-            far_range(pb->kind, x, k * Mn, (k + 1) * Mn, pb->y_f, pb->n_f, pb->w_f, pb->eta_f,
+            far_range(pb->kind, x, f0[k], f0[k + 1], pb->y_f, pb->n_f, pb->w_f, pb->eta_f,
                       sigma_f, sm);
             for (int i = 0; i < d; ++i) acc_add(&nr[i], -acc_val(&sm[i]));
         }
@@ -410,6 +459,7 @@ void or_apply_rows(const or_problem* pb, const double* sigma_p, const double* si
             if (u_near) u_near[q * d + i] = nv;
         }
     }
+    free(c0); free(f0); free(b0);
 }
 
 /* Near correction alone with explicit blocks (pin P11: gather-apply == dense product). */

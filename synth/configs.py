@@ -6,6 +6,7 @@ is what the operator takes as input; nothing here evaluates the operator.
   c1  Laplace DL, torus R=1 rho=0.1, 8 x 10 x 12 -> 2x upsampled, T = 960 nodes + 200 points
   c2  Stokes eta S + D, trefoil (R17) rho(s)=0.05(1+0.3cos 6 pi s), 32 x 10 x 16
   c3  Stokes, two tori R=1 rho=0.05 at gap 0.0025 (R19), 64 x 12 x 20 each
+  c3v c3's geometry with per-panel N_th in {12, 24, 40, 64} by distance to the gap (NEXT N4)
   c4  Stokes mobility (K(I-L)+L), 64 random loops in [0,8]^3, 32 x 10 x 12 each
   c5  Stokes, 512 loops R=1 rho=0.05 in [0,16]^3, 9 x 10 x 12 each (R16); c5alt: 36 panels
 """
@@ -14,7 +15,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .geometry import (Body, torus_body, trefoil_body, discretize, random_rotation,
+from .geometry import (Body, torus_body, trefoil_body, discretize, discretize_ragged, random_rotation,
                        panel_arclength, centerline_min_distance)
 from .nearlist import build_near_csr
 
@@ -64,6 +65,35 @@ class Problem:
     panel_len: Optional[np.ndarray] = None
     body_center: Optional[np.ndarray] = None
     extra: dict = field(default_factory=dict)
+    # ragged angular orders (NEXT N4, P:L770-781): N_th^(k) per panel, fine M_th^(k) = q_th N_th^(k)
+    # with q_th = Mt // Nt (Nt, Mt then hold the base pair).  None: every panel has Nt.
+    panel_nt: Optional[np.ndarray] = None
+
+    @property
+    def ragged(self):
+        return self.panel_nt is not None
+
+    def nt_of_panel(self):
+        return self.panel_nt.astype(np.int64) if self.ragged else np.full(self.P, self.Nt, np.int64)
+
+    def mt_of_panel(self):
+        return self.nt_of_panel() * (self.Mt // self.Nt) if self.ragged else np.full(self.P, self.Mt, np.int64)
+
+    def node_off(self):
+        """[P+1] first coarse node of each panel"""
+        return np.concatenate([[0], np.cumsum(self.Ns * self.nt_of_panel())]).astype(np.int64)
+
+    def fine_off(self):
+        """[P+1] first fine node of each panel"""
+        return np.concatenate([[0], np.cumsum(self.Ms * self.mt_of_panel())]).astype(np.int64)
+
+    def blk_off(self):
+        """[nnz+1] first entry of each near block [t_dim][N_n^(k) s_dim] in the flat block array"""
+        bl = self.tdim * self.sdim * self.Ns * self.nt_of_panel()[self.panel_idx]
+        return np.concatenate([[0], np.cumsum(bl)]).astype(np.int64)
+
+    def n_blocks_entries(self):
+        return int(self.blk_off()[-1]) if self.ragged else self.nnz * self.block_len
 
     @property
     def P(self):
@@ -79,19 +109,21 @@ class Problem:
 
     @property
     def Nn(self):
+        assert not self.ragged, "ragged problem: use node_off()"
         return self.Ns * self.Nt
 
     @property
     def Mn(self):
+        assert not self.ragged, "ragged problem: use fine_off()"
         return self.Ms * self.Mt
 
     @property
     def N(self):
-        return self.P * self.Nn
+        return int(self.node_off()[-1]) if self.ragged else self.P * self.Nn
 
     @property
     def M(self):
-        return self.P * self.Mn
+        return int(self.fine_off()[-1]) if self.ragged else self.P * self.Mn
 
     @property
     def T(self):
@@ -103,6 +135,7 @@ class Problem:
 
     @property
     def block_len(self):
+        assert not self.ragged, "ragged problem: use blk_off()"
         return self.tdim * self.Nn * self.sdim
 
     def pairs(self):
@@ -110,21 +143,30 @@ class Problem:
 
 
 def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 2),
-              extra_targets=None, c1_rule=False, projector=False, rng=None):
+              extra_targets=None, c1_rule=False, projector=False, rng=None, nt_panels=None):
+    """nt_panels: optional list (per body) of per-panel angular orders (ragged, NEXT N4); Nt is
+    then the base order and q[1] the fine factor of every panel."""
     Ms, Mt = q[0] * Ns, q[1] * Nt
-    coarse = [discretize(b, P, Ns, Nt) for b, P in zip(bodies, P_per_body)]
-    fine = [discretize(b, P, Ms, Mt) for b, P in zip(bodies, P_per_body)]
+    if nt_panels is None:
+        coarse = [discretize(b, P, Ns, Nt) for b, P in zip(bodies, P_per_body)]
+        fine = [discretize(b, P, Ms, Mt) for b, P in zip(bodies, P_per_body)]
+    else:
+        coarse = [discretize_ragged(b, P, Ns, nt) for b, P, nt in zip(bodies, P_per_body, nt_panels)]
+        fine = [discretize_ragged(b, P, Ms, q[1] * np.asarray(nt)) for b, P, nt in zip(bodies, P_per_body, nt_panels)]
     cat = lambda L, a: np.ascontiguousarray(np.concatenate([getattr(g, a) for g in L], axis=0))
     y_c, n_c, w_c = cat(coarse, "y"), cat(coarse, "n"), cat(coarse, "w")
     y_f, n_f, w_f = cat(fine, "y"), cat(fine, "n"), cat(fine, "w")
     body_of_panel = np.concatenate([np.full(P, b, np.int32) for b, P in enumerate(P_per_body)])
     Ptot = int(body_of_panel.shape[0])
-    Nn, Mn = Ns * Nt, Ms * Mt
+    panel_nt = None if nt_panels is None else np.concatenate([np.asarray(v, np.int32) for v in nt_panels])
+    nt_k = np.full(Ptot, Nt, np.int64) if panel_nt is None else panel_nt.astype(np.int64)
+    node_off = np.concatenate([[0], np.cumsum(Ns * nt_k)])
+    fine_per_panel = Ms * q[1] * nt_k
     if kernel == STOKES_SLDL:
         eta_body = np.array([eta_cfie_input(b.rho_min) for b in bodies])
     else:
         eta_body = np.zeros(len(bodies))
-    eta_f = np.repeat(eta_body[body_of_panel], Mn).astype(np.float64)
+    eta_f = np.repeat(eta_body[body_of_panel], fine_per_panel).astype(np.float64)
     n_on = y_c.shape[0]
     x_trg = y_c.copy()
     if extra_targets is not None:
@@ -132,19 +174,31 @@ def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 
     sdim = 1 if kernel == LAPLACE_DL else 3
     sigma = rng.standard_normal((y_c.shape[0], sdim))
     L = np.concatenate([panel_arclength(b, P) for b, P in zip(bodies, P_per_body)])
-    ring_xc = cat(coarse, "xc").reshape(Ptot, Ns, Nt, 3)[:, :, 0, :]
-    rho_ring = np.concatenate([np.broadcast_to(b.rho(g.s.reshape(P, Ns, Nt)[:, :, 0]), (P, Ns))
-                               for b, g, P in zip(bodies, coarse, P_per_body)]).reshape(Ptot, Ns)
+    # first node of every GL ring: its centerline point and radius (ragged-safe)
+    ring_first = (node_off[:-1, None] + np.arange(Ns)[None, :] * nt_k[:, None]).reshape(-1)
+    ring_xc = cat(coarse, "xc")[ring_first].reshape(Ptot, Ns, 3)
+    s_all = np.concatenate([g.s for g in coarse])
+    S_ring = s_all[ring_first].reshape(Ptot, Ns)
+    rho_ring = np.empty((Ptot, Ns))
+    for bi, b in enumerate(bodies):
+        m = body_of_panel == bi
+        rho_ring[m] = np.broadcast_to(b.rho(S_ring[m]), (int(m.sum()), Ns))
     own = np.full(x_trg.shape[0], -1, np.int64)
-    own[:n_on] = np.repeat(np.arange(Ptot), Nn)
+    own[:n_on] = np.repeat(np.arange(Ptot), Ns * nt_k)
     forced = None
     if c1_rule:
         # config 1 node targets: panels {k-1, k, k+1} mod P of their own body (R15)
         P0 = P_per_body[0]
-        k = np.repeat(np.arange(P0), Nn)
+        k = np.repeat(np.arange(P0), Ns * Nt)
         forced = np.stack([(k - 1) % P0, k, (k + 1) % P0], axis=1)
-    row_ptr, panel_idx = build_near_csr(x_trg, y_c.reshape(Ptot, Nn, 3), ring_xc, rho_ring, L,
-                                        own, forced_rows=forced)
+    if panel_nt is None:
+        y_panels = y_c.reshape(Ptot, Ns * Nt, 3)
+    else:   # pad every panel to the largest node count with copies of its first node (min unchanged)
+        nmax = int((Ns * nt_k).max())
+        j = np.arange(nmax)[None, :]
+        idx = node_off[:-1, None] + np.where(j < Ns * nt_k[:, None], j, 0)
+        y_panels = y_c[idx]
+    row_ptr, panel_idx = build_near_csr(x_trg, y_panels, ring_xc, rho_ring, L, own, forced_rows=forced)
     # coincident-pair guard (R14): no target may sit on a fine source
     _assert_separated(x_trg, y_f)
     blk_seed = (seed * 0x9E3779B1 + 0xB10C) & ((1 << 64) - 1)
@@ -156,7 +210,7 @@ def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 
                    w_f=w_f, eta_f=eta_f, eta_body=eta_body, x_trg=x_trg, n_on=n_on,
                    c_identity=0.5, sigma=sigma, row_ptr=row_ptr, panel_idx=panel_idx,
                    blk_seed=blk_seed, s_blk=s_blk, projector=projector, panel_len=L,
-                   body_center=centers)
+                   body_center=centers, panel_nt=panel_nt)
 
 
 def _assert_separated(x, y, tol=1e-9):
@@ -195,17 +249,18 @@ def _place_loops(rng, n, R_of, rho_of, lo_hi_of, gap_of, max_tries=200000):
     return bodies, tries
 
 
-CONFIGS = ("c1", "c2", "c3", "c4", "c5", "c5alt")
+CONFIGS = ("c1", "c2", "c3", "c3v", "c4", "c5", "c5alt")
 
 
 def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_DL, eta=None, extra_targets=None,
-                       seed_offset=0):
+                       seed_offset=0, nt_panels=None):
     """Single torus (axis z, centre 0) with the 2 L_k near rule -- pin problems for the special
     quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes; eta=0 -> pure DL."""
     seed = BASE_SEED + 100 + seed_offset
     rng = np.random.default_rng(seed)
     b = torus_body(R, rho)
-    pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng)
+    pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng,
+                   nt_panels=None if nt_panels is None else [np.asarray(nt_panels)])
     if kernel == STOKES_SLDL and eta is not None:
         pr.eta_body[:] = eta
         pr.eta_f[:] = eta
@@ -215,7 +270,7 @@ def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_D
 def make_config(name: str, **kw) -> Problem:
     """Build one of the BASELINE configs.  Keyword overrides shrink a config for tests
     (n_loops, panels) while keeping its shape and recipe."""
-    idx = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4, "c5alt": 4}[name]
+    idx = {"c1": 0, "c2": 1, "c3": 2, "c3v": 2, "c4": 3, "c5": 4, "c5alt": 4}[name]
     seed = BASE_SEED + idx + kw.pop("seed_offset", 0)
     rng = np.random.default_rng(seed)
     if name == "c1":
@@ -234,6 +289,23 @@ def make_config(name: str, **kw) -> Problem:
         b0 = torus_body(1.0, rho, (0.0, 0.0, 0.0))
         b1 = torus_body(1.0, rho, (2.0 + 2 * rho + gap, 0.0, 0.0))
         return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 20, rng=rng)
+    if name == "c3v":
+        # c3 with per-panel angular orders (NEXT N4; the paper's close-touching mesh is adaptive in
+        # N_th up to 88): N_th by the distance from the panel's centerline midpoint to the
+        # other ring's centerline -- 64 within 0.15, 40 within 0.4, 24 within 0.8, else 12 (base 12, q = 2)
+        P = kw.get("panels", 64)
+        rho, gap = 0.05, 0.0025
+        c1x = 2.0 + 2 * rho + gap
+        b0 = torus_body(1.0, rho, (0.0, 0.0, 0.0))
+        b1 = torus_body(1.0, rho, (c1x, 0.0, 0.0))
+        mid = (np.arange(P) + 0.5) / P
+        nts = []
+        for b, other in ((b0, b1), (b1, b0)):
+            xm = b.xc(mid)
+            so = np.arange(720) / 720
+            d = np.min(np.linalg.norm(xm[:, None, :] - other.xc(so)[None, :, :], axis=-1), axis=1)
+            nts.append(np.select([d < 0.15, d < 0.4, d < 0.8], [64, 40, 24], 12).astype(np.int32))
+        return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 12, rng=rng, nt_panels=nts)
     if name == "c4":
         n = kw.get("n_loops", 64)
         P = kw.get("panels", 32)

@@ -362,3 +362,95 @@ def test_eta_printed_values():
             continue
         name, rho, val, tol, _ = l.split()
         assert abs(O.eta_cfie(float(rho)) - float(val)) <= float(tol) * float(val)
+
+
+# ---------------------------------------------------------------- N4: ragged angular orders
+# PAPER.md §3.1: element k carries its own N_th^(k).  The oracle's ragged bookkeeping
+# (per-panel interpolation, node / fine / block offsets) is pinned by exactness, by the physics of
+# a ragged refined torus, and by an independent dense assembly from the generator's offsets.
+def test_n4_ragged_upsample_exactness():
+    ns, ms = 10, 20
+    nts = np.array([12, 4, 20, 8, 12, 16])
+    mts = 2 * nts
+    rng = np.random.default_rng(11)
+    coef = rng.standard_normal((nts.size, ns))
+    sc, _ = O.gauss_legendre(ns)
+    sf, _ = O.gauss_legendre(ms)
+    cs, fs = [], []
+    for p, (nt, mt) in enumerate(zip(nts, mts)):
+        a = rng.standard_normal(nt // 2)
+        b = rng.standard_normal(nt // 2)
+        ny = rng.standard_normal()
+        f = lambda t, th: np.polynomial.polynomial.polyval(t, coef[p]) * (
+            sum(a[l] * np.cos(l * th) + b[l] * np.sin(l * th) for l in range(nt // 2)) + ny * np.cos(nt * th / 2))
+        cs.append(f(sc[:, None], 2 * np.pi * np.arange(nt)[None, :] / nt).reshape(-1))
+        fs.append(f(sf[:, None], 2 * np.pi * np.arange(mt)[None, :] / mt).reshape(-1))
+    c, f = np.concatenate(cs), np.concatenate(fs)
+    for nc in (1, 3):
+        out = O.upsample_ragged(np.repeat(c[:, None], nc, 1) * (1 + np.arange(nc)), ns, nts, ms, mts, nc)
+        np.testing.assert_allclose(out.reshape(-1, nc), np.repeat(f[:, None], nc, 1) * (1 + np.arange(nc)),
+                                   rtol=0, atol=1e-13 * np.abs(f).max())
+
+
+def test_n4_ragged_gauss_law():
+    """Laplace DL of sigma = 1 on a refined torus whose panels alternate N_th in {32, 48, 64}:
+    -1 inside, 0 outside.  sigma_f comes from the oracle's ragged upsample."""
+    from synth.geometry import discretize_ragged
+    b = torus_body(1.0, 0.1)
+    P = 192
+    nts = np.array([32, 48, 64])[np.arange(P) % 3]
+    g = discretize_ragged(b, P, 10, 2 * nts)
+    sf = O.upsample_ragged(np.ones(10 * int(nts.sum())), 10, nts, 10, 2 * nts, 1)   # ms = ns: identity in s
+    assert np.abs(sf - 1).max() < 1e-14
+    xin, xout = _interior_exterior()
+    u = O.farfield(1, np.concatenate([xin, xout]), g.y, g.n, g.w, sf)
+    np.testing.assert_allclose(u[:len(xin)], -1.0, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(u[len(xin):], 0.0, rtol=0, atol=1e-12)
+
+
+def test_n4_ragged_uniform_reduces_to_uniform():
+    """all N_th^(k) equal: the ragged bookkeeping must give the uniform operator bit for bit"""
+    pr = make_config("c2", panels=6)
+    import copy
+    rg = copy.deepcopy(pr)
+    rg.panel_nt = np.full(pr.P, pr.Nt, np.int32)
+    rows = np.arange(0, pr.T, 7)
+    a = O.Oracle(pr).apply_rows(pr.sigma, rows)
+    b = O.Oracle(rg).apply_rows(rg.sigma, rows)
+    assert np.array_equal(a, b)
+
+
+def test_n4_ragged_operator_vs_dense_assembly():
+    """c3v (ragged): near term = dense B sigma (blocks placed from the GENERATOR's offsets and the
+    generator's counter rule) minus the far sum over the near panels' fine nodes; far + near =
+    far over the non-near panels + B sigma."""
+    from synth.rng import block_entries_array
+    pr = make_config("c3v", panels=8)
+    assert pr.ragged and len(set(pr.panel_nt.tolist())) > 1
+    no, fo, bo = pr.node_off(), pr.fine_off(), pr.blk_off()
+    d = pr.sdim
+    orc = O.Oracle(pr)
+    rows = np.arange(0, pr.T, 97)
+    sp, sf, _ = orc.prepare(pr.sigma)
+    _, uf, un = orc.apply_rows(pr.sigma, rows, parts=True, prepared=(sp, sf, None))
+    # fine density: per-panel uniform upsample with that panel's orders
+    sf_ref = np.concatenate([O.upsample(pr.sigma[no[k]:no[k + 1]].reshape(-1), 1, pr.Ns, int(pr.panel_nt[k]),
+                                        pr.Ms, 2 * int(pr.panel_nt[k]), d) for k in range(pr.P)]).reshape(-1, d)
+    np.testing.assert_array_equal(sf.reshape(-1, d), sf_ref)
+    for q, t in enumerate(rows):
+        bsig = np.zeros(d)
+        ms = []
+        for p in range(pr.row_ptr[t], pr.row_ptr[t + 1]):
+            k = pr.panel_idx[p]
+            nn = no[k + 1] - no[k]
+            B = block_entries_array(pr.blk_seed, np.arange(bo[p], bo[p + 1]), pr.s_blk).reshape(d, nn * d)
+            bsig += B @ pr.sigma[no[k]:no[k + 1]].reshape(-1)
+            ms.append(np.arange(fo[k], fo[k + 1]))
+        m = np.concatenate(ms)
+        eta = pr.eta_f
+        sm = O.farfield(2, pr.x_trg[t:t + 1], pr.y_f[m], pr.n_f[m], pr.w_f[m], sf_ref[m], eta=eta[m])[0]
+        np.testing.assert_allclose(un[q], bsig - sm, rtol=0, atol=1e-12 * (1 + np.abs(bsig).max()))
+        keep = np.setdiff1d(np.arange(pr.M), m)
+        ffar = O.farfield(2, pr.x_trg[t:t + 1], pr.y_f[keep], pr.n_f[keep], pr.w_f[keep], sf_ref[keep],
+                          eta=eta[keep])[0]
+        np.testing.assert_allclose(uf[q] + un[q], ffar + bsig, rtol=0, atol=1e-11 * (1 + np.abs(ffar).max()))
