@@ -27,11 +27,17 @@ def _segments(rows):
 
 
 class DeviceProblem:
-    def __init__(self, pr, rank=0, nranks=1, device="cuda", fold=True, comm=None, blocks=None, quad=None):
+    def __init__(self, pr, rank=0, nranks=1, device="cuda", fold=True, comm=None, blocks=None, quad=None,
+                 slice_only=False):
         """blocks: None -> seeded synthetic B (R10); quad=dict(order=.., beta=..) -> special-quadrature
-        B computed on the GPU by slb_nearcorr_quad (N1)."""
+        B computed on the GPU by slb_nearcorr_quad (N1).
+        slice_only: a ONE-GPU operator over rank `rank`'s target rows of an `nranks` partition with all
+        source panels (no communicator, identity term off) -- the per-rank compute of the sharded
+        operator, for timing projections (tools/scaling_projection.py)."""
         self.pr = pr
         rows, pb, pe, n_on, ranges = local_rows(pr, rank, nranks)
+        if slice_only:
+            pb, pe, n_on = 0, pr.P, 0
         self.rows, self.pb, self.pe, self.n_on, self.ranges = rows, pb, pe, n_on, ranges
         dev = torch.device(device)
         f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
@@ -82,7 +88,8 @@ class DeviceProblem:
         self.op = Operator(kernel=pr.kernel, ns=pr.Ns, nt=pr.Nt, ms=pr.Ms, mt=pr.Mt, n_panels_global=pr.P,
                            panel_begin=pb, panel_end=pe, x_trg=self.x_trg, n_on=n_on, y_fine=self.y_f,
                            n_fine=self.n_f, w_fine=self.w_f, row_ptr=self.row_ptr, panel_idx=self.panel_idx,
-                           blocks=self.blocks, c_identity=pr.c_identity, eta_fine=self.eta_f, eta=0.0,
+                           blocks=self.blocks, c_identity=0.0 if slice_only else pr.c_identity,
+                           eta_fine=self.eta_f, eta=0.0,
                            folded=not fold, n_bodies=nb, body_of_panel=bop, y_coarse=y_c, w_coarse=w_c,
                            comm=comm)
 

@@ -228,7 +228,14 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     const double da = (c.t0 > ts) ? (c.t0 - ts) * St : ((c.t1 < ts) ? (ts - c.t1) * St : 0.0);
                     const double db = (c.h0 > 0.0) ? c.h0 * Sh : ((c.h1 < 0.0) ? -c.h1 * Sh : 0.0);
                     const double dist = sqrt(d * d + da * da + db * db);
-                    accept = dist >= P.beta * diag && diag <= 2.0 * cap;
+                    if (da >= 2.0 * cap) {
+                        // far along the fiber (more than two tube diameters): the whole cross-section
+                        // is at true distance >= da - cap >= da / 2, so no size cap -- cells grow
+                        // geometrically along t (slender panels, rho << panel length)
+                        accept = fmax(0.5 * da, d) >= P.beta * diag;
+                    } else {
+                        accept = dist >= P.beta * diag && diag <= 2.0 * cap;
+                    }
                 }
                 if (accept) {
                     if (nc >= kMaxCells) { s_fail = 1; break; }

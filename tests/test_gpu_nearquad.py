@@ -83,8 +83,8 @@ def test_stokes_dl_rigid_motion_with_special_blocks(mode):
 # ------------------------------------------------------------------ independent integrator
 def _exact_panel_integral(body, P, k, Ns, Nt, sig_panel, x, kind, eta, t0=None, h0=None):
     """int int K(x - y(t,th)) sigma_interp(t,th) J dt dth over panel k, t in [-1,1] local, polar
-    coordinates around (t0, h0) (the singular node or the closest point), scipy adaptive GK."""
-    from scipy.integrate import quad
+    coordinates around (t0, h0) (the singular node or the closest point), scipy adaptive GK
+    (quad_vec: all components share one adaptive subdivision, max-norm error control)."""
     H = 1e-30
     tg, _ = O.gauss_legendre(Ns)
 
@@ -132,15 +132,13 @@ def _exact_panel_integral(body, P, k, Ns, Nt, sig_panel, x, kind, eta, t0=None, 
         return min(rs)
 
     corners = sorted(np.mod([np.arctan2(b, a) for a in (amin, amax) for b in (bmin, bmax)], 2 * np.pi))
-    dim = 1 if kind == 1 else 3
-    out = np.zeros(dim)
-    for comp in range(dim):
-        def inner(phi):
-            c, s = np.cos(phi), np.sin(phi)
-            g = lambda rho: np.atleast_1d(F(t0 + rho * c / St, h0 + rho * s / Sh))[comp] * rho / (St * Sh)
-            return quad(g, 0, R(phi), epsabs=1e-14, epsrel=1e-12, limit=200)[0]
-        out[comp] = quad(inner, 0, 2 * np.pi, points=corners, epsabs=1e-14, epsrel=1e-12, limit=400)[0]
-    return out
+    from scipy.integrate import quad_vec
+
+    def inner(phi):     # all components at once: one adaptive rule per ray
+        c, s = np.cos(phi), np.sin(phi)
+        g = lambda rho: np.atleast_1d(F(t0 + rho * c / St, h0 + rho * s / Sh)) * rho / (St * Sh)
+        return quad_vec(g, 0, R(phi), epsabs=1e-13, epsrel=1e-11, norm="max", limit=200)[0]
+    return quad_vec(inner, 0, 2 * np.pi, points=corners, epsabs=1e-13, epsrel=1e-10, norm="max", limit=400)[0]
 
 
 @pytest.mark.parametrize("kind", [1, 2])

@@ -1,0 +1,99 @@
+"""Throughput of the setup steps and the solve around the operator (NEXT rows N1-N3) on one B200.
+
+For each workload: GPU near-list build (N3, slb_near_build), special-quadrature correction
+blocks (N1, slb_nearcorr_quad) at two rule orders, operator creation (packing + fold
+E = B - G U), and a GMRES solve (N2, slb_gmres) of the CFIE with the special blocks.  Every
+time is CUDA-event (device) time after one warm-up call; rates are in the paper's units
+(unknowns per second of quadrature setup, P:L2315 / P:L2353 / P:L2527 / P:L2629).
+
+usage: python tools/setup_bench.py [names...]   (default: torus c2 c3) -> JSON lines on stdout
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2310_00889_b200 as S  # noqa: E402
+from harness import DeviceProblem  # noqa: E402
+from synth import make_config, make_torus_problem  # noqa: E402
+
+
+def cu(a, dt=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+def timed(fn, reps=1):
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        out = fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out
+
+
+def problem(name):
+    if name == "torus":
+        return make_torus_problem(rho=0.1, panels=16, kernel=2)
+    if name == "torus_slender":
+        return make_torus_problem(rho=1e-3, panels=24, Nt=8, kernel=2)
+    return make_config(name)
+
+
+def run(name):
+    pr = problem(name)
+    d = pr.sdim
+    res = {"workload": name, "nodes": pr.N, "unknowns": pr.N * d, "panels": pr.P, "grid": [pr.Ns, pr.Nt],
+           "near_pairs": pr.nnz, "block_shape": [pr.tdim, pr.Nn * d]}
+    # N3: near lists on the GPU (2 L_k rule + own panel)
+    own = cu(np.where(np.arange(pr.T) < pr.n_on, np.arange(pr.T) // pr.Nn, -1).astype(np.int64), torch.int64)
+    x, y, rad = cu(pr.x_trg), cu(pr.y_c.reshape(pr.P, pr.Nn, 3)), cu(2.0 * pr.panel_len)
+    ms, (rp, pi) = timed(lambda: S.slb_near_build(x, y, rad, own))
+    res["near_build_ms"] = ms
+    res["near_build_target_panel_tests_per_s"] = pr.T * pr.P / (ms * 1e-3)
+    # N1: special-quadrature blocks, two rule orders
+    trg_node = cu(np.where(np.arange(pr.T) < pr.n_on, np.arange(pr.T), -1).astype(np.int64), torch.int64)
+    eta_panel = cu(pr.eta_body[pr.body_of_panel]) if pr.kernel == 2 else None
+    blocks = torch.empty(pr.nnz * pr.block_len, dtype=torch.float64, device="cuda")
+    rp_d, pi_d = cu(pr.row_ptr, torch.int64), cu(pr.panel_idx, torch.int32)
+    for order in (8, 14):
+        ms, _ = timed(lambda: S.slb_nearcorr_quad(pr.kernel, x, rp_d, pi_d, pr.Ns, pr.Nt, y, blocks,
+                                                  trg_node=trg_node, eta_panel=eta_panel, order=order, beta=0.6))
+        res[f"quad_order{order}_ms"] = ms
+        res[f"quad_order{order}_unknowns_per_s"] = pr.N * d / (ms * 1e-3)
+        res[f"quad_order{order}_blocks_per_s"] = pr.nnz / (ms * 1e-3)
+    del blocks
+    torch.cuda.empty_cache()
+    # operator creation with the special blocks (fold included) and one apply
+    quad = dict(order=14, beta=0.6)
+    t0 = time.perf_counter()
+    dp = DeviceProblem(pr, quad=quad)
+    torch.cuda.synchronize()
+    res["operator_create_s_incl_quad"] = time.perf_counter() - t0
+    ms, _ = timed(lambda: dp.matvec(), reps=5)
+    res["matvec_ms"] = ms
+    # N2: GMRES on the CFIE with a smooth right-hand side (a rigid translation field)
+    rhs = cu(np.tile(np.array([1.0, 0.5, -0.25])[:d], (pr.T, 1)))
+    t0 = time.perf_counter()
+    xs, it, rr = dp.op.gmres(rhs, restart=100, max_iters=600, tol=1e-12)
+    torch.cuda.synchronize()
+    res["gmres_s"] = time.perf_counter() - t0
+    res["gmres_iters"] = it
+    res["gmres_rel_residual"] = rr
+    res["gmres_ms_per_iter"] = res["gmres_s"] * 1e3 / max(it, 1)
+    dp.close()
+    return res
+
+
+if __name__ == "__main__":
+    for nm in sys.argv[1:] or ["torus", "torus_slender", "c2", "c3"]:
+        print(json.dumps(run(nm)), flush=True)
