@@ -118,9 +118,13 @@ def cpu_baseline_run(pr, seconds_target=15.0, rows_n=None):
 def config_info(pr, world, l2_note):
     return {"workload": pr.name, "kernel": "laplace_dl" if pr.kernel == 1 else "stokes_sl+dl",
             "operator": "K(I-L)+L mobility" if pr.projector else ("I/2 + D" if pr.kernel == 1 else "I/2 + D + eta S"),
-            "bodies": pr.n_bodies, "panels": pr.P, "coarse_grid": [pr.Ns, pr.Nt], "fine_grid": [pr.Ms, pr.Mt],
+            "bodies": pr.n_bodies, "panels": pr.P,
+            "coarse_grid": [pr.Ns, pr.Nt] if not pr.ragged else
+            [pr.Ns, {int(k): int(v) for k, v in zip(*np.unique(pr.panel_nt, return_counts=True))}],
+            "fine_grid": [pr.Ms, pr.Mt] if not pr.ragged else [pr.Ms, f"{pr.Mt // pr.Nt} x N_th per panel"],
             "nodes": pr.N, "unknowns": pr.N * pr.sdim, "fine_sources": pr.M, "targets": pr.T,
-            "pairs_per_apply": pr.pairs(), "near_blocks": pr.nnz, "block_shape": [pr.tdim, pr.Nn * pr.sdim],
+            "pairs_per_apply": pr.pairs(), "near_blocks": pr.nnz,
+            "block_shape": [pr.tdim, pr.Nn * pr.sdim] if not pr.ragged else [pr.tdim, "N_n^(k) s_dim (ragged)"],
             "parallelism": f"targets sharded over {world} GPU(s), all-gather of fine density",
             "l2": l2_note, "seed": pr.seed}
 
@@ -217,7 +221,8 @@ def main():
     fin_ms = st_mean[3]
 
     # e2e through the public API with host buffers (H2D sigma, D2H u inside the timed region)
-    sig_h = torch.from_numpy(pr.sigma.reshape(pr.N, pr.sdim)[dp.pb * pr.Nn:dp.pe * pr.Nn].copy()).pin_memory()
+    no, fo = pr.node_off(), pr.fine_off()
+    sig_h = torch.from_numpy(pr.sigma.reshape(pr.N, pr.sdim)[no[dp.pb]:no[dp.pe]].copy()).pin_memory()
     u_h = torch.empty((dp.rows.size, pr.tdim), dtype=torch.float64).pin_memory()
     e2e_steps = max(1, min(args.steps, 5))
     barrier()
@@ -236,9 +241,9 @@ def main():
     # roofline quantities per rank -> report rank 0's (targets are balanced)
     T_loc = dp.rows.size
     far_flops = T_loc * pr.M * FLOPS_PER_PAIR[pr.kernel]
-    near_bytes = dp.nnz * (8 * pr.block_len + 4) + T_loc * 8 * (pr.tdim + 2)
-    n_loc_nodes = (dp.pe - dp.pb) * pr.Nn
-    m_loc = (dp.pe - dp.pb) * pr.Mn
+    near_bytes = dp.n_entries * 8 + dp.nnz * 4 + T_loc * 8 * (pr.tdim + 2)
+    n_loc_nodes = int(no[dp.pe] - no[dp.pb])
+    m_loc = int(fo[dp.pe] - fo[dp.pb])
     # upsample (+projector) algorithmic bytes: sigma read + sigma' write (+ L sigma), fine scale read, records written
     up_bytes = (n_loc_nodes * pr.sdim * 8 * (2 + (2 if pr.projector else 0)) + m_loc * 8 * (3 if pr.kernel == 1 else 1)
                 + m_loc * 8 * 3)
@@ -278,9 +283,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_info(pr, world, "inputs larger than L2 (fine sources "
-                                  f"{pr.M * 80 / 1e6:.0f} MB, near blocks {pr.nnz * pr.block_len * 8 / 1e9:.1f} GB)"),
+                                  f"{pr.M * 80 / 1e6:.0f} MB, near blocks {pr.n_blocks_entries() * 8 / 1e9:.1f} GB)"),
             "pairs_per_s": pr.pairs() * value,
-            "roofline": {"bound": "alu", "kernel": "far_kernel (FP64 DFMA pipe)", "achieved": far_tf,
+            "roofline": {"bound": "alu", "kernel": "far_const_kernel (FP64 DFMA pipe; far_kernel below M = 2^19)", "achieved": far_tf,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": far_tf / FP64_PEAK_TFLOPS,
                          "traffic": traffic,
                          "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (no FP64 entry in "

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define SLB_ABI_VERSION 1
+#define SLB_ABI_VERSION 2
 
 typedef enum {
     SLB_OK = 0,
@@ -56,7 +56,9 @@ typedef enum {
     SLB_ERR_UNSUPPORTED = 5
 } slb_status;
 
-typedef enum { SLB_LAPLACE_DL = 1, SLB_STOKES_SLDL = 2 } slb_kernel;
+/* SLB_STOKES_SL (pure single layer S, weight 1) is accepted by slb_nearcorr_quad[_ragged] only; the
+ * operator evaluates S as SLB_STOKES_SLDL with eta = 1 and zero normals. */
+typedef enum { SLB_LAPLACE_DL = 1, SLB_STOKES_SLDL = 2, SLB_STOKES_SL = 3 } slb_kernel;
 
 /* Compiled limits (SLB_ERR_UNSUPPORTED beyond them). */
 #define SLB_MAX_NS 32
@@ -78,6 +80,12 @@ void slb_coincident_reset(void);
 
 /* Number of kernels this library has launched since it was loaded (launch accounting). */
 unsigned long long slb_launch_count(void);
+
+/* (a, NEXT N4) Ragged upsample: panel p is ns x nt[p] -> ms x mt[p] (HOST arrays [n_panels]),
+ * nodes of consecutive panels back to back in both arrays.  Otherwise as
+ * slb_upsample.  Synchronises s (uploads the panel tables). */
+slb_status slb_upsample_ragged(int64_t n_panels, int ns, const int32_t* nt, int ms, const int32_t* mt, int ncomp,
+                               const double* sigma_coarse, double* sigma_fine, cudaStream_t s);
 
 /* (a) Upsample a density from the coarse Nystrom grid to the fine smooth-quadrature grid,
  *   sigma_fine[p][a][b][c] = sum_i sum_j P_s[a][i] F_th[b][j] sigma_coarse[p][i][j][c],
@@ -142,6 +150,14 @@ slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_t
                              const double* y_coarse, const double* eta_panel, int order, double beta,
                              double* blocks, cudaStream_t s);
 
+/* (NEXT N1 + N4) Same for ragged angular orders: panel k has ns x panel_nt[k] nodes (HOST array
+ * [n_panels], even, <= 64), y_coarse is the per-panel node blocks back to back,
+ * block p = [tdim][ns*panel_nt[k]*sdim] packed back to back in CSR order.  Synchronises s. */
+slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                                    const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels, int ns,
+                                    const int32_t* panel_nt, const double* y_coarse, const double* eta_panel,
+                                    int order, double beta, double* blocks, cudaStream_t s);
+
 /* Synthetic special-quadrature blocks (input generation, R10):
  *   blocks[q] = ((2 u_q - 1) sqrt(3)) s_blk,  u_q = (splitmix64(seed, first + q) >> 11) 2^-53,
  *   q in [0, count).  Bit-identical to the oracle's definition. */
@@ -194,6 +210,14 @@ typedef struct {
     const int32_t* body_of_panel_local; /* [panel_end-panel_begin] local body id, nondecreasing */
     const double* y_coarse;             /* [local nodes][3] */
     const double* w_coarse;             /* [local nodes] */
+    /* (NEXT N4) ragged angular orders, §3.1 P:L770-781 ("element k ... Fourier order
+     * N_th^(k)"): HOST arrays [n_panels_global], or both NULL for uniform panels.  Panel k then has
+     * ns x panel_nt[k] coarse and ms x panel_mt[k] fine nodes (each even, within the compiled
+     * limits; nt and mt are ignored).  Every node array is the per-panel blocks back to back in
+     * panel order; near block p is [tdim][ns*panel_nt[k]*sdim] with k = panel_idx[p], the blocks
+     * packed back to back in CSR order.  Read during slb_operator_create only. */
+    const int32_t* panel_nt;
+    const int32_t* panel_mt;
 } slb_operator_desc;
 
 /* Borrows every descriptor pointer (they must outlive the operator); owns only its scratch
@@ -227,6 +251,22 @@ slb_status slb_operator_destroy(slb_operator* op);
  * Collective across the operator's ranks; synchronises s.  iters_out, relres_out: host, may be NULL. */
 slb_status slb_gmres(slb_operator* op, const double* rhs, double* x, int restart, int max_iters,
                      double tol, int* iters_out, double* relres_out, cudaStream_t s);
+
+/* (NEXT N2) Stokes mobility solve, PAPER.md "Stokes slender mobility CFIE":
+ * given per-body force F_b and torque T_b (about the body's quadrature-weighted centroid c_b),
+ *   nu = alpha_b + beta_b x (x - c_b), int nu = F_b, int nu x (x - c_b) = T_b    (completion flow, P:L1903-1912;
+ *        closed form alpha_b = F_b / |Omega_b|, beta_b = -I_b^-1 T_b with the projector's moments)
+ *   (K(I - L) + L) sigma = -S[nu]                                                  (Eq. e:new-mobility-bie)
+ *   V = -L sigma = v_b + omega_b x (x - c_b)                                       (Eq. e:recover-rigidbody-motion)
+ * mob: mobility operator (Stokes CFIE kernel, projector enabled, square); sl: operator of the
+ * same local nodes and targets evaluating the pure single layer S (SLB_STOKES_SLDL, eta = 1, zero
+ * normals, c_identity = 0, blocks from slb_nearcorr_quad(SLB_STOKES_SL, ...)).
+ * force_torque: HOST [n_bodies_local][6] = (F, T); rigid_out: HOST [n_bodies_local][6] = (v, omega)
+ * written; sigma: device [local nodes][3], initial guess in, density out.  Other arguments as
+ * slb_gmres.  Collective across the ranks; synchronises s. */
+slb_status slb_mobility_solve(slb_operator* mob, slb_operator* sl, const double* force_torque, double* rigid_out,
+                              double* sigma, int restart, int max_iters, double tol, int* iters_out,
+                              double* relres_out, cudaStream_t s);
 
 /* Microbenchmark: sustained FP64 FMA throughput (GFLOP/s, FMA = 2 flops) of this device,
  * measured with dependent-chain-free DFMA streams over all SMs for ~iters iterations. */

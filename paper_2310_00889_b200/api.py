@@ -12,6 +12,7 @@ from ._native import lib, check, OperatorDesc, SlbError
 
 LAPLACE_DL = 1
 STOKES_SLDL = 2
+STOKES_SL = 3        # slb_nearcorr_quad only: pure single-layer blocks
 
 
 def _stream():
@@ -60,6 +61,28 @@ def slb_upsample(sigma_coarse, n_panels, ns, nt, ms, mt, ncomp, out=None):
     return out
 
 
+def _host_i32(a, name):
+    import numpy as np
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    if arr.ndim != 1:
+        raise SlbError(f"{name} must be a 1-D integer array")
+    return arr
+
+
+def slb_upsample_ragged(sigma_coarse, ns, nt_panels, ms, mt_panels, ncomp, out=None):
+    """(NEXT N4) per-panel angular orders: panel p is ns x nt[p] -> ms x mt[p] (host int arrays)."""
+    nt = _host_i32(nt_panels, "nt_panels")
+    mt = _host_i32(mt_panels, "mt_panels")
+    if nt.shape != mt.shape:
+        raise SlbError("nt_panels and mt_panels differ in length")
+    if out is None:
+        out = torch.empty(int((ms * mt.astype("int64")).sum()) * ncomp, dtype=torch.float64,
+                          device=sigma_coarse.device)
+    check(lib().slb_upsample_ragged(nt.size, ns, ctypes.c_void_p(nt.ctypes.data), ms, ctypes.c_void_p(mt.ctypes.data),
+                                    ncomp, _dev(sigma_coarse, "sigma_coarse"), _dev(out, "sigma_fine"), _stream()))
+    return out
+
+
 def slb_farfield_laplace_dl(x_trg, y, n, w, sigma, out=None):
     T = x_trg.shape[0]
     if out is None:
@@ -99,9 +122,20 @@ def slb_nearcorr_fold(kernel, x_trg, row_ptr, panel_idx, ns, nt, ms, mt, y_fine,
 
 
 def slb_nearcorr_quad(kernel, x_trg, row_ptr, panel_idx, ns, nt, y_coarse, blocks, trg_node=None, eta_panel=None,
-                      order=12, beta=0.6):
-    """Special-quadrature blocks B for the CSR pairs (unfolded), written into `blocks`."""
+                      order=12, beta=0.6, panel_nt=None):
+    """Special-quadrature blocks B for the CSR pairs (unfolded), written into `blocks`.
+    panel_nt (host int array [n_panels]): ragged angular orders (NEXT N4); nt is then ignored."""
     T = row_ptr.shape[0] - 1
+    if panel_nt is not None:
+        pnt = _host_i32(panel_nt, "panel_nt")
+        check(lib().slb_nearcorr_quad_ragged(kernel, T, _dev(x_trg, "x_trg"),
+                                             _dev(trg_node, "trg_node", torch.int64, True),
+                                             _dev(row_ptr, "row_ptr", torch.int64),
+                                             _dev(panel_idx, "panel_idx", torch.int32), pnt.size, ns,
+                                             ctypes.c_void_p(pnt.ctypes.data), _dev(y_coarse, "y_coarse"),
+                                             _dev(eta_panel, "eta_panel", allow_none=True), int(order), float(beta),
+                                             _dev(blocks, "blocks"), _stream()))
+        return blocks
     check(lib().slb_nearcorr_quad(kernel, T, _dev(x_trg, "x_trg"), _dev(trg_node, "trg_node", torch.int64, True),
                                   _dev(row_ptr, "row_ptr", torch.int64), _dev(panel_idx, "panel_idx", torch.int32),
                                   ns, nt, _dev(y_coarse, "y_coarse"), _dev(eta_panel, "eta_panel", allow_none=True),
@@ -166,7 +200,9 @@ class Operator:
 
     def __init__(self, *, kernel, ns, nt, ms, mt, n_panels_global, panel_begin, panel_end, x_trg, n_on,
                  y_fine, n_fine, w_fine, row_ptr, panel_idx, blocks, c_identity=0.5, eta_fine=None, eta=0.0,
-                 folded=False, n_bodies=0, body_of_panel=None, y_coarse=None, w_coarse=None, comm=None):
+                 folded=False, n_bodies=0, body_of_panel=None, y_coarse=None, w_coarse=None, comm=None,
+                 panel_nt=None, panel_mt=None):
+        """panel_nt / panel_mt (host int arrays [n_panels_global]): ragged angular orders (NEXT N4)."""
         self._keep = [x_trg, y_fine, n_fine, w_fine, eta_fine, row_ptr, panel_idx, blocks, body_of_panel,
                       y_coarse, w_coarse]
         d = OperatorDesc()
@@ -185,11 +221,19 @@ class Operator:
         if n_bodies:
             d.body_of_panel_local = _dev(body_of_panel, "body_of_panel", torch.int32)
             d.y_coarse, d.w_coarse = _dev(y_coarse, "y_coarse"), _dev(w_coarse, "w_coarse")
+        if (panel_nt is None) != (panel_mt is None):
+            raise SlbError("panel_nt and panel_mt must be given together")
+        if panel_nt is not None:
+            pnt, pmt = _host_i32(panel_nt, "panel_nt"), _host_i32(panel_mt, "panel_mt")
+            self._keep += [pnt, pmt]
+            d.panel_nt, d.panel_mt = pnt.ctypes.data, pmt.ctypes.data
+            self.n_loc_nodes = int(ns * pnt[panel_begin:panel_end].astype("int64").sum())
+        else:
+            self.n_loc_nodes = (panel_end - panel_begin) * ns * nt
         self.desc = d
         self.kernel = kernel
         self.tdim = 1 if kernel == LAPLACE_DL else 3
         self.n_trg = x_trg.shape[0]
-        self.n_loc_nodes = (panel_end - panel_begin) * ns * nt
         self.comm = comm
         h = ctypes.c_void_p()
         check(lib().slb_operator_create(ctypes.byref(d), comm.h if comm is not None else None, ctypes.byref(h)))
@@ -218,6 +262,22 @@ class Operator:
         check(lib().slb_gmres(self.h, _dev(rhs, "rhs"), _dev(x, "x"), int(restart), int(max_iters), float(tol),
                               ctypes.byref(it), ctypes.byref(rr), _stream()))
         return x, it.value, rr.value
+
+    def mobility_solve(self, sl, force_torque, sigma0=None, restart=100, max_iters=1000, tol=1e-12):
+        """slb_mobility_solve: force_torque [n_bodies][6] (host, F and T about each body's centroid) ->
+        (rigid [n_bodies][6] = (v, omega), sigma, iterations, relative residual).  `sl` is the
+        single-layer Operator on the same nodes."""
+        import numpy as np
+        ft = np.ascontiguousarray(np.asarray(force_torque, dtype=np.float64).reshape(-1, 6))
+        rig = np.empty_like(ft)
+        x = torch.zeros((self.n_loc_nodes, 3), dtype=torch.float64, device="cuda") if sigma0 is None \
+            else sigma0.clone()
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        check(lib().slb_mobility_solve(self.h, sl.h, ctypes.c_void_p(ft.ctypes.data), ctypes.c_void_p(rig.ctypes.data),
+                                       _dev(x, "sigma"), int(restart), int(max_iters), float(tol), ctypes.byref(it),
+                                       ctypes.byref(rr), _stream()))
+        return rig, x, it.value, rr.value
 
     def timings(self):
         arr = (ctypes.c_float * 4)()

@@ -2,6 +2,9 @@
 // error/status plumbing shared by the library.  See include/slb.h for the contract.
 #include <cmath>
 #include <string>
+#include <map>
+#include <string>
+#include <vector>
 #include "common.cuh"
 
 namespace slb {
@@ -91,9 +94,70 @@ slb_status slb_upsample(int64_t n_panels, int ns, int nt, int ms, int mt, int nc
     SLB_REQUIRE(sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(check_sticky("slb_upsample") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
     static InterpParams ip;   // 29 KB: not on the stack
-    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip), SLB_ERR_UNSUPPORTED,
-                "interpolation matrices exceed the kernel-parameter budget (ms*ns + mt*nt <= 3600)");
-    return upsample_launch(FAR_STOKES_SLDL, n_panels, ip, ncomp, sigma_coarse, sigma_fine, nullptr, nullptr, s);
+    double* owned = nullptr;  // device copy of large interpolation matrices (freed after the launch)
+    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip, &owned), SLB_ERR_OOM, "interpolation matrices: allocation failed");
+    slb_status st = upsample_launch(FAR_STOKES_SLDL, n_panels, ip, ncomp, sigma_coarse, sigma_fine, nullptr, nullptr, s);
+    if (owned) { cudaStreamSynchronize(s); cudaFree(owned); }
+    return st;
+}
+
+slb_status slb_upsample_ragged(int64_t n_panels, int ns, const int32_t* nt, int ms, const int32_t* mt, int ncomp,
+                               const double* sigma_coarse, double* sigma_fine, cudaStream_t s) {
+    SLB_REQUIRE(n_panels >= 0, SLB_ERR_INVALID_ARG, "n_panels < 0");
+    SLB_REQUIRE(ncomp == 1 || ncomp == 3, SLB_ERR_INVALID_ARG, "ncomp must be 1 or 3");
+    SLB_REQUIRE(ns >= 1 && ms >= 1 && ns <= SLB_MAX_NS && ms <= SLB_MAX_MS, SLB_ERR_INVALID_ARG, "bad ns/ms");
+    if (n_panels == 0) return SLB_OK;
+    SLB_REQUIRE(nt && mt && sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(check_sticky("slb_upsample_ragged") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    std::vector<int64_t> c0(n_panels + 1, 0), f0(n_panels + 1, 0);
+    std::map<std::pair<int, int>, std::vector<int32_t>> groups;
+    for (int64_t p = 0; p < n_panels; ++p) {
+        SLB_REQUIRE(nt[p] >= 2 && nt[p] % 2 == 0 && nt[p] <= SLB_MAX_NT && mt[p] >= 2 && mt[p] <= SLB_MAX_MT,
+                    SLB_ERR_INVALID_ARG, "panel orders must be even and within the compiled limits");
+        c0[p + 1] = c0[p] + (int64_t)ns * nt[p];
+        f0[p + 1] = f0[p] + (int64_t)ms * mt[p];
+        groups[{nt[p], mt[p]}].push_back((int32_t)p);
+    }
+    int64_t *c0d = nullptr, *f0d = nullptr;
+    int32_t* pl = nullptr;
+    slb_status st = SLB_OK;
+    auto cleanup = [&]() { cudaFree(c0d); cudaFree(f0d); cudaFree(pl); };
+    if (cudaMalloc(&c0d, sizeof(int64_t) * (n_panels + 1)) != cudaSuccess ||
+        cudaMalloc(&f0d, sizeof(int64_t) * (n_panels + 1)) != cudaSuccess ||
+        cudaMalloc(&pl, sizeof(int32_t) * n_panels) != cudaSuccess) {
+        cleanup();
+        set_error("slb_upsample_ragged: out of device memory");
+        return SLB_ERR_OOM;
+    }
+    std::vector<int32_t> flat;
+    for (auto& g : groups) flat.insert(flat.end(), g.second.begin(), g.second.end());
+    cudaMemcpy(c0d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(f0d, f0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(pl, flat.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
+    static InterpParams ip;
+    std::vector<double*> owned;
+    int64_t off = 0;
+    for (auto& g : groups) {
+        double* o = nullptr;
+        if (!make_interp(ns, g.first.first, ms, g.first.second, &ip, &o)) {
+            set_error("slb_upsample_ragged: interpolation matrices: allocation failed");
+            st = SLB_ERR_OOM;
+            break;
+        }
+        if (o) owned.push_back(o);
+        st = upsample_launch(FAR_STOKES_SLDL, (int64_t)g.second.size(), ip, ncomp, sigma_coarse, sigma_fine,
+                             nullptr, nullptr, s, pl + off, c0d, f0d);
+        if (st != SLB_OK) break;
+        off += (int64_t)g.second.size();
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    cleanup();
+    for (double* o : owned) cudaFree(o);
+    if (st == SLB_OK && e != cudaSuccess) {
+        set_error(std::string("slb_upsample_ragged: ") + cudaGetErrorString(e));
+        st = SLB_ERR_CUDA;
+    }
+    return st;
 }
 
 static slb_status farfield_common(FarKind kind, int64_t n_trg, const double* x, int64_t n_src,
@@ -171,11 +235,14 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
     if (n_trg == 0) return SLB_OK;
     SLB_REQUIRE(x_trg && row_ptr && y_fine && n_fine && w_fine, SLB_ERR_INVALID_ARG, "null pointer");
     static InterpParams ip;
-    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip), SLB_ERR_UNSUPPORTED, "interpolation matrices too large");
+    double* owned = nullptr;
+    SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip, &owned), SLB_ERR_OOM, "interpolation matrices: allocation failed");
     FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE
                                             : ((eta_fine || eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL);
-    return fold_launch(kind, n_trg, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine, w_fine, eta_fine, eta,
-                       blocks, s);
+    slb_status st = fold_launch(kind, n_trg, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine, w_fine, eta_fine, eta,
+                                blocks, s);
+    if (owned) { cudaStreamSynchronize(s); cudaFree(owned); }
+    return st;
 }
 
 }  // extern "C"

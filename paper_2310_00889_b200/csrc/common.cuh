@@ -42,13 +42,18 @@ void bary_matrix(int nf, const double* xs, int nt, const double* xt, double* P);
 // d = 2 pi b / M - 2 pi j / N  (the real interpolant with the Nyquist cosine; N even).
 void trig_matrix(int N, int M, double* F);
 
-// Interpolation matrices passed BY VALUE as a kernel parameter (<= 32 KB param space).
+// Interpolation matrices passed BY VALUE as a kernel parameter (<= 32 KB param space); larger
+// grids (e.g. N_th = 64 -> M_th = 128) keep them in a device buffer pointed to by vg.
 constexpr int kMaxInterp = 3600;   // doubles: ms*ns + mt*nt
 struct InterpParams {
     int ns, nt, ms, mt;
+    const double* vg;              // device copy when the matrices exceed kMaxInterp, else nullptr
     double v[kMaxInterp];          // P_s [ms][ns] followed by F [mt][nt]
 };
-bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip);
+// Fills ip.  If the matrices do not fit the parameter budget and `owned` is given, they are copied
+// into a new device buffer (*owned; the caller frees it after the kernels using ip completed);
+// returns false if they do not fit and owned == nullptr, or on allocation failure.
+bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip, double** owned = nullptr);
 
 // ---- device helpers ----
 #ifdef __CUDACC__
@@ -168,26 +173,38 @@ slb_status pack_dyn(FarKind kind, int64_t M, const double* sc, const double* sig
 
 // ---- upsample (upsample.cu) ----
 // sigma_fine: written as plain values (dyn == nullptr) or packed into dyn records with sc.
+// Ragged panels (NEXT N4): plist = the bucket's panel ids (NULL: 0..n_panels-1), c_off / f_off =
+// first coarse / fine node of each panel id (NULL: uniform p*ns*nt / p*ms*mt).
 slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int ncomp,
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
-                           double* dyn, cudaStream_t s);
+                           double* dyn, cudaStream_t s, const int32_t* plist = nullptr,
+                           const int64_t* c_off = nullptr, const int64_t* f_off = nullptr);
 
 // ---- near (nearcorr.cu) ----
 slb_status near_apply_launch(int64_t n_trg, int tdim, int cols, const int64_t* row_ptr,
                              const int32_t* panel_idx, const double* blocks, const double* sigma_c,
                              double* u, cudaStream_t s);
+// Ragged near blocks (NEXT N4): device offsets, all NULL for uniform panels.
+struct RagNear {
+    const int64_t* cn0 = nullptr;    // [P_global+1] first coarse node of each panel
+    const int64_t* boff = nullptr;   // [nnz+1] first double of each block (CSR order)
+    int max_cols = 0;                // largest nodes_per_panel * sdim
+};
 // fused finalize: u[t] = sum_c partials[c][t] + near(t) + c_id * sig_loc[t] (t < n_on) + Lsig[t]
 slb_status finalize_launch(const FarPlan& plan, int64_t n_trg, int tdim, int cols,
                            const double* partials, const int64_t* row_ptr, const int32_t* panel_idx,
                            const double* blocks, const double* sigma_c_global, int64_t n_on,
                            double c_id, const double* sig_local, const double* Lsig, double* u,
-                           int G, cudaStream_t s);
+                           int G, cudaStream_t s, const RagNear& rag = RagNear());
 int near_group_size(int64_t T, int64_t nnz);
 slb_status csr_check(int64_t T, const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels);
+// Ragged (NEXT N4): only pairs whose panel has pbucket[k] == bucket are folded (pbucket NULL: all);
+// fn0 = first fine node of each global panel, boff = block offsets (NULL: uniform).
 slb_status fold_launch(FarKind kind, int64_t n_trg, const double* x_trg, const int64_t* row_ptr,
                        const int32_t* panel_idx, const InterpParams& ip, const double* y_fine,
                        const double* n_fine, const double* w_fine, const double* eta_fine,
-                       double eta, double* blocks, cudaStream_t s);
+                       double eta, double* blocks, cudaStream_t s, const int32_t* pbucket = nullptr,
+                       int bucket = 0, const int64_t* fn0 = nullptr, const int64_t* boff = nullptr);
 
 // ---- projector (projector.cu) ----
 slb_status body_moments_launch(int64_t n_bodies, const int64_t* node_begin, const double* y,
@@ -196,5 +213,10 @@ slb_status proj_launch(int64_t n_bodies, const int64_t* node_begin, const double
                        const double* w, const double* bodyc /*[nb][16]*/, const double* sigma,
                        double* coef /*[nb][6]*/, double* sigma_p, double* Lsig,
                        int64_t max_nodes_per_body, cudaStream_t s);
+
+slb_status completion_launch(int64_t n_bodies, const int64_t* nb0, const double* y, const double* bodyc,
+                             const double* ft /*[nb][6]*/, double* nu, int64_t max_nodes_per_body, cudaStream_t s);
+slb_status proj_coef_launch(int64_t n_bodies, const int64_t* nb0, const double* y, const double* w,
+                            const double* bodyc, const double* sigma, double* coef /*[nb][6]*/, cudaStream_t s);
 
 }  // namespace slb

@@ -198,3 +198,44 @@ extern "C" slb_status slb_gmres(slb_operator* op, const double* rhs, double* x, 
     SLB_CUDA(cudaStreamSynchronize(s));
     return SLB_OK;
 }
+
+extern "C" slb_status slb_mobility_solve(slb_operator* mob, slb_operator* sl, const double* force_torque,
+                                         double* rigid_out, double* sigma, int restart, int max_iters, double tol,
+                                         int* iters_out, double* relres_out, cudaStream_t s) {
+    SLB_REQUIRE(mob && sl && force_torque && rigid_out && sigma, SLB_ERR_INVALID_ARG, "null argument");
+    const int64_t nb = mob->d.n_bodies_local;
+    SLB_REQUIRE(mob->kind != FAR_LAPLACE && nb > 0 && mob->bodyc, SLB_ERR_INVALID_ARG,
+                "mob must be a Stokes operator with the rigid-motion projector");
+    SLB_REQUIRE(sl->kind != FAR_LAPLACE && sl->d.n_bodies_local == 0 && sl->N_loc == mob->N_loc &&
+                    sl->d.n_trg_local == mob->d.n_trg_local,
+                SLB_ERR_INVALID_ARG, "sl must be a Stokes operator (no projector) on the same nodes and targets");
+    const int64_t n = mob->N_loc * 3;
+    double *ft = nullptr, *nu = nullptr, *rhs = nullptr;
+    slb_status st = SLB_OK;
+    auto cleanup = [&]() { cudaFreeAsync(ft, s); cudaFreeAsync(nu, s); cudaFreeAsync(rhs, s); };
+#define MS(expr) do { st = (expr); if (st != SLB_OK) { cleanup(); return st; } } while (0)
+    SLB_CUDA(cudaMallocAsync(&ft, sizeof(double) * nb * 6, s));
+    SLB_CUDA(cudaMallocAsync(&nu, sizeof(double) * std::max<int64_t>(n, 1), s));
+    SLB_CUDA(cudaMallocAsync(&rhs, sizeof(double) * std::max<int64_t>(n, 1), s));
+    SLB_CUDA(cudaMemcpyAsync(ft, force_torque, sizeof(double) * nb * 6, cudaMemcpyHostToDevice, s));
+    // nu (completion flow), rhs = -S[nu]
+    MS(completion_launch(nb, mob->nb0, mob->d.y_coarse, mob->bodyc, ft, nu, mob->max_nodes_body, s));
+    MS(slb_matvec(sl, nu, rhs, s));
+    Gm g;
+    g.op = mob;
+    g.s = s;
+    g.n = n;
+    MS(g.axpby(-1.0, rhs, 0.0, nullptr, rhs));
+    // (K(I-L) + L) sigma = -S[nu]
+    MS(slb_gmres(mob, rhs, sigma, restart, max_iters, tol, iters_out, relres_out, s));
+    // V = -L sigma: rigid coefficients of L sigma per body, negated
+    MS(proj_coef_launch(nb, mob->nb0, mob->d.y_coarse, mob->d.w_coarse, mob->bodyc, sigma, mob->coef, s));
+    std::vector<double> c(nb * 6);
+    SLB_CUDA(cudaMemcpyAsync(c.data(), mob->coef, sizeof(double) * nb * 6, cudaMemcpyDeviceToHost, s));
+    SLB_CUDA(cudaStreamSynchronize(s));
+    for (int64_t q = 0; q < nb * 6; ++q) rigid_out[q] = -c[q];
+#undef MS
+    cleanup();
+    SLB_CUDA(cudaStreamSynchronize(s));
+    return SLB_OK;
+}

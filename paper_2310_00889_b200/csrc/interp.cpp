@@ -8,6 +8,7 @@
 // explicit real Fourier sum (reading R3).
 #include <cmath>
 #include <cstring>
+#include <vector>
 #include "common.cuh"
 
 namespace slb {
@@ -72,15 +73,31 @@ void trig_matrix(int N, int M, double* F) {
         }
 }
 
-bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip) {
+bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip, double** owned) {
     if (ns < 1 || ms < 1 || nt < 2 || mt < 2 || (nt & 1) || ns > 64 || ms > 64) return false;
-    if (ms * ns + mt * nt > kMaxInterp) return false;
     ip->ns = ns; ip->nt = nt; ip->ms = ms; ip->mt = mt;
+    ip->vg = nullptr;
     double xs[64], ws[64], xf[64], wf[64];
     gl_nodes(ns, xs, ws);
     gl_nodes(ms, xf, wf);
-    bary_matrix(ns, xs, ms, xf, ip->v);
-    trig_matrix(nt, mt, ip->v + ms * ns);
+    const int n = ms * ns + mt * nt;
+    if (n <= kMaxInterp) {
+        bary_matrix(ns, xs, ms, xf, ip->v);
+        trig_matrix(nt, mt, ip->v + ms * ns);
+        return true;
+    }
+    if (!owned) return false;
+    std::vector<double> h(n);
+    bary_matrix(ns, xs, ms, xf, h.data());
+    trig_matrix(nt, mt, h.data() + ms * ns);
+    double* d = nullptr;
+    if (cudaMalloc(&d, sizeof(double) * n) != cudaSuccess) return false;
+    if (cudaMemcpy(d, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return false;
+    }
+    *owned = d;
+    ip->vg = d;
     return true;
 }
 

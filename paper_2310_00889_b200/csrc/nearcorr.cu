@@ -152,6 +152,142 @@ static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, co
     return check_launch("near_stream_kernel");
 }
 
+
+// Ragged angular orders (NEXT N4): block p = [TD][ck] doubles at boff[p] (ck = its panel's nodes x
+// sdim, panel k's density at coarse node cn0[k]), blocks of very different widths (c3v: 10-55 KB).
+// The TMA ring holds fixed slots of S double2; a block streams through ceil(TD ck2 / S) slots
+// (chunks of its flat [row][col] layout).  Lane 0 produces chunks in the same (block, chunk) order
+// the warp consumes them.  Per row, every lane visits the columns c = lane (mod 32) in increasing
+// order exactly as near_stream_kernel does, so a ragged operator whose orders happen to be equal
+// returns the uniform operator's result bit for bit.
+template <int TD, int MODE>
+__global__ void __launch_bounds__(kNearWarps * 32)
+near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
+                          const int32_t* __restrict__ panel_idx, const double* __restrict__ blocks,
+                          const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
+                          int64_t n_on, double c_id, const double* __restrict__ sig_local,
+                          const double* __restrict__ Lsig, double* __restrict__ u, int G,
+                          const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff, int sdim) {
+    extern __shared__ __align__(128) double2 ring[];      // [warps][STG][S]
+    __shared__ __align__(8) uint64_t bars[kNearWarps * kNearStages];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* myring = ring + (size_t)w * kNearStages * S;
+    uint64_t* mybar = bars + w * kNearStages;
+    if (lane == 0) {
+        for (int q = 0; q < kNearStages; ++q) mbar_init(&mybar[q], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t gw = (int64_t)blockIdx.x * kNearWarps + w;
+    const int64_t ta = gw * G;
+    const int64_t tb = ta + G < T ? ta + G : T;
+    if (ta >= tb) return;
+    const int64_t pa = row_ptr[ta], pb = row_ptr[tb];
+    const double2* B = reinterpret_cast<const double2*>(blocks);
+    // producer cursor (lane 0): block pp, first double2 qq of the next chunk
+    int64_t pp = pa, qq = 0;
+    auto produce = [&](int st) {
+        if (pp >= pb) return;
+        const int64_t len2 = (boff[pp + 1] - boff[pp]) / 2;
+        const int64_t n2 = (len2 - qq) < S ? (len2 - qq) : S;
+        mbar_expect_tx(&mybar[st], (uint32_t)(n2 * 16));
+        bulk_g2s(myring + (size_t)st * S, B + boff[pp] / 2 + qq, (uint32_t)(n2 * 16), &mybar[st]);
+        qq += n2;
+        if (qq >= len2) { ++pp; qq = 0; }
+    };
+    if (lane == 0)
+        for (int q = 0; q < kNearStages; ++q) produce(q);
+    const double2* S2 = reinterpret_cast<const double2*>(sigma_c);
+    int64_t i = 0;                                        // chunk counter
+    for (int64_t t = ta; t < tb; ++t) {
+        double acc[TD];
+#pragma unroll
+        for (int r = 0; r < TD; ++r) acc[r] = 0.0;
+        const int64_t p1 = row_ptr[t + 1];
+        for (int64_t p = row_ptr[t]; p < p1; ++p) {
+            const int64_t k = panel_idx[p];
+            const int ck = (int)((cn0[k + 1] - cn0[k]) * sdim / 2);
+            const double2* Sk = S2 + cn0[k] * sdim / 2;
+            const int len2 = TD * ck;
+            for (int q0 = 0; q0 < len2; q0 += S, ++i) {
+                const int st = (int)(i % kNearStages);
+                const int n2 = (len2 - q0) < S ? (len2 - q0) : S;
+                mbar_wait(&mybar[st], (uint32_t)((i / kNearStages) & 1));
+                const double2* R = myring + (size_t)st * S - q0;   // R[f] = block flat index f
+#pragma unroll
+                for (int r = 0; r < TD; ++r) {
+                    const int lo = max(q0 - r * ck, 0), hi = min(q0 + n2 - r * ck, ck);
+                    if (lo >= hi) continue;
+                    for (int c = lo + ((lane - lo) & 31); c < hi; c += 32) {
+                        const double2 sv = __ldg(Sk + c);
+                        const double2 bv = R[r * ck + c];
+                        acc[r] = fma(bv.x, sv.x, fma(bv.y, sv.y, acc[r]));
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    fence_proxy_async_smem();
+                    produce(st);
+                }
+            }
+        }
+        double far[TD];
+#pragma unroll
+        for (int r = 0; r < TD; ++r) far[r] = 0.0;
+        if (MODE == 1)
+            for (int64_t c = lane; c < n_chunks; c += 32)
+#pragma unroll
+                for (int r = 0; r < TD; ++r) far[r] += partials[(c * T + t) * TD + r];
+#pragma unroll
+        for (int r = 0; r < TD; ++r) {
+            const double nv = warp_sum(acc[r]);
+            const double fv = MODE == 1 ? warp_sum(far[r]) : 0.0;
+            if (lane == r) {
+                if (MODE == 0) {
+                    u[t * TD + r] += nv;
+                } else {
+                    double v = fv + nv;
+                    if (t < n_on) {
+                        v += c_id * sig_local[t * TD + r];
+                        if (Lsig) v += Lsig[t * TD + r];
+                    }
+                    u[t * TD + r] = v;
+                }
+            }
+        }
+    }
+}
+
+static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_t* row_ptr, const int32_t* panel_idx,
+                                     const double* blocks, const double* sigma_c, const double* partials,
+                                     int64_t n_chunks, int64_t n_on, double c_id, const double* sig_local,
+                                     const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
+    if (T <= 0) return SLB_OK;
+    // slot: the widest block if 4 warps x 3 stages of it fit in ~150 KB, else a chunk of that size
+    const int widest2 = tdim * rag.max_cols / 2;
+    const int Smax = (int)(150 * 1024 / (kNearWarps * kNearStages * 16));
+    const int S = std::min(widest2, Smax);
+    const size_t smem = (size_t)kNearWarps * kNearStages * S * 16;
+    G = std::max(1, G);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
+#define RAG_LAUNCH(TD, MODE)                                                                                  \
+    do {                                                                                                      \
+        SLB_CUDA(cudaFuncSetAttribute(near_stream_ragged_kernel<TD, MODE>,                                    \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
+        near_stream_ragged_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(                              \
+            T, S, row_ptr, panel_idx, blocks, sigma_c, partials, n_chunks, n_on, c_id, sig_local, Lsig, u, G,  \
+            rag.cn0, rag.boff, tdim);                                                                         \
+    } while (0)
+    if (tdim == 1) {
+        if (mode == 0) RAG_LAUNCH(1, 0); else RAG_LAUNCH(1, 1);
+    } else {
+        if (mode == 0) RAG_LAUNCH(3, 0); else RAG_LAUNCH(3, 1);
+    }
+#undef RAG_LAUNCH
+    ++g_launch_count;
+    return check_launch("near_stream_ragged_kernel");
+}
+
 slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr, const int32_t* panel_idx,
                              const double* blocks, const double* sigma_c, double* u, cudaStream_t s) {
     return near_stream_launch(0, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c, nullptr, 0, 0, 0.0, nullptr,
@@ -161,7 +297,10 @@ slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_p
 slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, const double* partials,
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
                            const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
-                           const double* Lsig, double* u, int G, cudaStream_t s) {
+                           const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
+    if (rag.boff)
+        return near_ragged_launch(1, T, tdim, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
+                                  n_on, c_id, sig_local, Lsig, u, G, s, rag);
     return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
                               n_on, c_id, sig_local, Lsig, u, G, s);
 }
@@ -175,11 +314,13 @@ __global__ void __launch_bounds__(128)
 fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ row_ptr,
             const int32_t* __restrict__ panel_idx, const __grid_constant__ InterpParams ip,
             const double* __restrict__ y_f, const double* __restrict__ n_f, const double* __restrict__ w_f,
-            const double* __restrict__ eta_f, double eta, double* __restrict__ blocks) {
+            const double* __restrict__ eta_f, double eta, double* __restrict__ blocks,
+            const int32_t* __restrict__ pbucket, int bucket, const int64_t* __restrict__ fn0,
+            const int64_t* __restrict__ boff) {
     extern __shared__ double sm[];
     const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
-    const double* Ps = ip.v;
-    const double* F = ip.v + ms * ns;
+    const double* Ps = ip.vg ? ip.vg : ip.v;
+    const double* F = Ps + ms * ns;
     const int Mn = ms * mt, Nn = ns * nt;
     const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
     const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
@@ -190,8 +331,10 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
     const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
+        if (pbucket && pbucket[k] != bucket) continue;          // ragged: another launch's (nt, mt)
+        const int64_t mk0 = fn0 ? fn0[k] : k * (int64_t)Mn;
         for (int q = threadIdx.x; q < Mn; q += blockDim.x) {
-            const int64_t m = k * Mn + q;
+            const int64_t m = mk0 + q;
             double r[3] = {x0 - y_f[3 * m], x1 - y_f[3 * m + 1], x2 - y_f[3 * m + 2]};
             double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
             double nn[3] = {n_f[3 * m], n_f[3 * m + 1], n_f[3 * m + 2]};
@@ -227,7 +370,7 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
             H[q] = acc;
         }
         __syncthreads();
-        double* Bp = blocks + p * (int64_t)TD * Nn * TD;
+        double* Bp = blocks + (boff ? boff[p] : p * (int64_t)TD * Nn * TD);
         const int nE = TD * Nn * TD;
         for (int q = threadIdx.x; q < nE; q += blockDim.x) {
             int j = q % TD, node = (q / TD) % Nn, i = q / (TD * Nn);
@@ -246,7 +389,8 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
 slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64_t* row_ptr,
                        const int32_t* panel_idx, const InterpParams& ip, const double* y_fine,
                        const double* n_fine, const double* w_fine, const double* eta_fine, double eta,
-                       double* blocks, cudaStream_t s) {
+                       double* blocks, cudaStream_t s, const int32_t* pbucket, int bucket, const int64_t* fn0,
+                       const int64_t* boff) {
     if (T <= 0) return SLB_OK;
     SLB_REQUIRE(T <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets for fold");
     const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
@@ -254,7 +398,7 @@ slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "fold: grid too large for shared memory");
     SLB_CUDA(cudaFuncSetAttribute(fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fold_kernel<<<(unsigned)T, 128, smem, s>>>((int)kind, T, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine,
-                                              w_fine, eta_fine, eta, blocks);
+                                              w_fine, eta_fine, eta, blocks, pbucket, bucket, fn0, boff);
     ++g_launch_count;
     return check_launch("fold_kernel");
 }

@@ -23,6 +23,8 @@
 // One CTA per target row; fixed summation order -> deterministic.
 #include <algorithm>
 #include <cmath>
+#include <string>
+#include <vector>
 #include "common.cuh"
 
 namespace slb {
@@ -34,6 +36,7 @@ constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
 struct QuadParams {
     int ns, nt, q, qd;
     double beta;
+    double dl;                // weight of the double layer: 1, or 0 for the pure single layer (SLB_STOKES_SL)
     double tgl[kMaxNsQ];      // panel GL nodes on [-1,1]
     double lam[kMaxNsQ];      // barycentric weights
     double gx[kMaxQ], gw[kMaxQ];        // q-point GL on [-1,1]
@@ -80,38 +83,48 @@ __device__ void lagrange_eval(const QuadParams& P, double t, double* l, double* 
     }
 }
 
-// trig cardinal C_j(th) and C_j'(th), th_j = 2 pi j / N (real interpolant with the Nyquist cosine)
-__device__ void trig_eval(int N, double th, double* C, double* dC) {
+// trig cardinal C_j(th) and C_j'(th), th_j = 2 pi j / N (real interpolant with the Nyquist cosine):
+//   C_j = (1/N)[1 + 2 sum_{l=1}^{N/2-1} cos(l (th - th_j)) + cos(N (th - th_j) / 2)]
+// with cos(l (th - th_j)) = cos(l th) cos(l th_j) + sin(l th) sin(l th_j): one sincos per point,
+// cos / sin(l th) by rotation, cos / sin(l th_j) = TC / TS[(l j) mod N] (TC[m] = cos(2 pi m / N)),
+// and cos(N (th - th_j)/2) = (-1)^j cos(N th / 2).  No division: exact at th = th_j.
+__device__ void trig_eval(int N, double th, double* C, double* dC, const double* TC, const double* TS) {
+    double c1, s1;
+    sincos(th, &s1, &c1);
+    double cl[kMaxNtQ / 2 + 1], sl[kMaxNtQ / 2 + 1];
+    cl[0] = 1.0; sl[0] = 0.0;
+    for (int l = 1; l <= N / 2; ++l) {
+        cl[l] = cl[l - 1] * c1 - sl[l - 1] * s1;
+        sl[l] = sl[l - 1] * c1 + cl[l - 1] * s1;
+    }
+    const double cN = cl[N / 2], sN = sl[N / 2];
     for (int j = 0; j < N; ++j) {
-        const double p = th - 2.0 * kPi * j / N;
-        double sv = 1.0, dv = 0.0;
-        double c1, s1;
-        sincos(p, &s1, &c1);
-        double ck = c1, sk = s1;      // cos(l p), sin(l p) by rotation
+        double sv = 0.0, dv = 0.0;
+        int idx = 0;
         for (int l = 1; l < N / 2; ++l) {
-            sv += 2.0 * ck;
-            dv -= 2.0 * l * sk;
-            const double cn = ck * c1 - sk * s1, sn = sk * c1 + ck * s1;
-            ck = cn; sk = sn;
+            idx += j;
+            if (idx >= N) idx -= N;
+            const double tc = TC[idx], ts = TS[idx];
+            sv = fma(cl[l], tc, fma(sl[l], ts, sv));
+            dv = fma((double)l, fma(cl[l], ts, -sl[l] * tc), dv);
         }
-        // l = N/2 term (ck, sk now hold cos/sin((N/2) p))
-        sv += ck;
-        dv -= 0.5 * N * sk;
-        C[j] = sv / N;
-        dC[j] = dv / N;
+        const double sgn = (j & 1) ? -1.0 : 1.0;
+        C[j] = (1.0 + 2.0 * sv + sgn * cN) / N;
+        dC[j] = (2.0 * dv - 0.5 * N * sgn * sN) / N;
     }
 }
 
 // surface point and tangents from the panel's nodes Y[i][j][3]
-__device__ void geom_eval(const QuadParams& P, const double* Y, double t, double th, double* y, double* yt,
-                          double* yh, double* lbuf, double* dlbuf, double* Cb, double* dCb) {
+__device__ void geom_eval(const QuadParams& P, int nt, const double* Y, double t, double th, double* y, double* yt,
+                          double* yh, double* lbuf, double* dlbuf, double* Cb, double* dCb, const double* TC,
+                          const double* TS) {
     lagrange_eval(P, t, lbuf, dlbuf);
-    trig_eval(P.nt, th, Cb, dCb);
+    trig_eval(nt, th, Cb, dCb, TC, TS);
     for (int c = 0; c < 3; ++c) { y[c] = 0.0; yt[c] = 0.0; yh[c] = 0.0; }
     for (int i = 0; i < P.ns; ++i) {
         double a[3] = {0, 0, 0}, ad[3] = {0, 0, 0};
-        for (int j = 0; j < P.nt; ++j) {
-            const double* Yij = Y + (i * P.nt + j) * 3;
+        for (int j = 0; j < nt; ++j) {
+            const double* Yij = Y + (i * nt + j) * 3;
             for (int c = 0; c < 3; ++c) { a[c] = fma(Cb[j], Yij[c], a[c]); ad[c] = fma(dCb[j], Yij[c], ad[c]); }
         }
         for (int c = 0; c < 3; ++c) {
@@ -126,19 +139,24 @@ __global__ void __launch_bounds__(kQThreads)
 nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ trg_node,
                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
                 const double* __restrict__ y_coarse, const double* __restrict__ eta_panel,
-                const __grid_constant__ QuadParams P, double* __restrict__ blocks, int* __restrict__ status) {
+                const __grid_constant__ QuadParams P, double* __restrict__ blocks, int* __restrict__ status,
+                const int32_t* __restrict__ pnt, const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff) {
     extern __shared__ double sm[];
-    const int ns = P.ns, nt = P.nt, Nn = ns * nt;
+    // ragged (NEXT N4): panel k has pnt[k] angular nodes and starts at coarse node cn0[k]; block p at
+    // boff[p]; the shared layout is sized for P.nt = the largest order.  NULL: uniform P.nt.
+    const int ns = P.ns, ntm = P.nt, Nnm = ns * ntm;
     const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
     const int NG = TD * TD;
     const int tid = threadIdx.x;
     // shared layout
     double* Y = sm;                                   // [Nn][3]
-    double* Bacc = Y + Nn * 3;                        // [NG][ns][nt]
-    double* Gs = Bacc + NG * Nn;                      // [128][NG]
+    double* Bacc = Y + Nnm * 3;                       // [NG][ns][nt]
+    double* Gs = Bacc + NG * Nnm;                     // [128][NG]
     double* Ls = Gs + kQThreads * NG;                 // [128][ns]
     double* Cs = Ls + kQThreads * ns;                 // [128][nt]
-    Cell* cells = reinterpret_cast<Cell*>(Cs + kQThreads * nt);
+    double* TC = Cs + kQThreads * ntm;                // [ntm] cos(2 pi m / nt) of the current panel
+    double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
+    Cell* cells = reinterpret_cast<Cell*>(TS + ntm);
     __shared__ double s_par[8];                       // t*, th*, d, St, Sh, node-singular flag
     __shared__ int s_ncell, s_ntot, s_fail;
     // per-thread scratch for the interpolation (registers / local)
@@ -150,17 +168,20 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     const int64_t node = trg_node ? trg_node[t] : -1;
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
-        const double eta = (kind == FAR_STOKES_SLDL) ? eta_panel[k] : 0.0;
-        for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[k * Nn * 3 + e];
+        const int nt = pnt ? pnt[k] : ntm, Nn = ns * nt;
+        const int64_t c0 = cn0 ? cn0[k] : k * (int64_t)Nn;
+        const double eta = (kind == FAR_STOKES_SLDL) ? (eta_panel ? eta_panel[k] : 1.0) : 0.0;
+        for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[c0 * 3 + e];
+        for (int e = tid; e < nt; e += kQThreads) sincos(2.0 * kPi * e / nt, &TS[e], &TC[e]);
         for (int e = tid; e < NG * Nn; e += kQThreads) Bacc[e] = 0.0;
         __syncthreads();
         // ---------------- closest point and the cell list (thread 0)
         if (tid == 0) {
             s_fail = 0;
-            const bool singular = (node >= k * Nn && node < (k + 1) * Nn);
+            const bool singular = (node >= c0 && node < c0 + Nn);
             double ts, hs;
             if (singular) {
-                const int loc = (int)(node - k * Nn);
+                const int loc = (int)(node - c0);
                 ts = P.tgl[loc / nt];
                 hs = 2.0 * kPi * (loc % nt) / nt;
             } else {
@@ -176,7 +197,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 // Gauss-Newton on |x - y(t,th)|^2, t clamped to [-1, 1]
                 for (int it = 0; it < 12; ++it) {
                     double y[3], yt[3], yh[3];
-                    geom_eval(P, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb);
+                    geom_eval(P, nt, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
                     const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
                     const double a11 = yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2];
                     const double a22 = yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2];
@@ -195,7 +216,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 }
             }
             double y[3], yt[3], yh[3];
-            geom_eval(P, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb);
+            geom_eval(P, nt, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
             const double d = singular ? 0.0
                                       : sqrt((x0 - y[0]) * (x0 - y[0]) + (x1 - y[1]) * (x1 - y[1]) +
                                              (x2 - y[2]) * (x2 - y[2]));
@@ -307,7 +328,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
                 }
                 double y[3], yt[3], yh[3];
-                geom_eval(P, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb);
+                geom_eval(P, nt, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
                 // outward normal (R8): n = y_th x y_t / |.|, J = |y_th x y_t|
                 const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
                                       yh[0] * yt[1] - yh[1] * yt[0]};
@@ -323,7 +344,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                         G[0] = rn * ir * ir * ir / (4.0 * kPi) * wJ;
                     } else {
                         const double ir3 = ir * ir * ir;
-                        const double sl = eta / (8.0 * kPi), dl = 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
+                        const double sl = eta / (8.0 * kPi), dl = P.dl * 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
                         for (int a = 0; a < 3; ++a)
                             for (int b = 0; b < 3; ++b)
                                 G[a * 3 + b] = (sl * ((a == b ? ir : 0.0) + r[a] * r[b] * ir3) + dl * r[a] * r[b]) * wJ;
@@ -338,17 +359,38 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 for (int j = 0; j < nt; ++j) Cs[tid * nt + j] = 0.0;
             }
             __syncthreads();
-            const int nb = min(kQThreads, ntot - base);
-            for (int o = tid; o < NG * Nn; o += kQThreads) {
-                const int q2 = o / Nn, ij = o % Nn, i = ij / nt, j = ij % nt;
-                double acc = Bacc[o];
-                for (int n = 0; n < nb; ++n) acc = fma(Gs[n * NG + q2] * Ls[n * ns + i], Cs[n * nt + j], acc);
-                Bacc[o] = acc;
+            // contraction with the basis as a GEMM on the FP64 tensor cores (DMMA m8n8k4):
+            //   Bacc[(q2,i)][j] += sum_n W[(q2,i)][n] C[n][j],   W[(q2,i)][n] = G[n][q2] l_i(t_n)
+            // (nodes n past the batch end carry zeros); each warp owns whole 8x8 output tiles.
+            {
+                const int warp = tid >> 5, lane = tid & 31, fg = lane >> 2, ftq = lane & 3;
+                const int Mr = NG * ns, mtl = (Mr + 7) / 8, ntl = (nt + 7) / 8;
+                for (int tile = warp; tile < mtl * ntl; tile += kQThreads / 32) {
+                    const int m0 = (tile / ntl) * 8, n0 = (tile % ntl) * 8;
+                    const int row = m0 + fg;                       // A row of this lane
+                    const int q2 = row / ns, ia = row % ns;
+                    const bool rok = row < Mr;
+                    const int col = n0 + fg;                       // B column of this lane
+                    const bool cok = col < nt;
+                    const int oc = n0 + 2 * ftq;                   // output columns oc, oc+1 of row m0+fg
+                    double d0 = (rok && oc < nt) ? Bacc[row * nt + oc] : 0.0;
+                    double d1 = (rok && oc + 1 < nt) ? Bacc[row * nt + oc + 1] : 0.0;
+#pragma unroll 4
+                    for (int k0 = 0; k0 < kQThreads; k0 += 4) {
+                        const int n = k0 + ftq;
+                        const double a = rok ? Gs[n * NG + q2] * Ls[n * ns + ia] : 0.0;
+                        const double b = cok ? Cs[n * nt + col] : 0.0;
+                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                     : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+                    }
+                    if (rok && oc < nt) Bacc[row * nt + oc] = d0;
+                    if (rok && oc + 1 < nt) Bacc[row * nt + oc + 1] = d1;
+                }
             }
             __syncthreads();
         }
         // ---------------- write the block: [tdim][node (i,j)][sdim]
-        double* Bp = blocks + p * (int64_t)TD * Nn * TD;
+        double* Bp = blocks + (boff ? boff[p] : p * (int64_t)TD * Nn * TD);
         for (int o = tid; o < NG * Nn; o += kQThreads) {
             const int q2 = o / Nn, ij = o % Nn;
             const int a = q2 / TD, b = q2 % TD;
@@ -362,20 +404,14 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
 
 using namespace slb;
 
-extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
-                                        const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
-                                        const double* y_coarse, const double* eta_panel, int order, double beta,
-                                        double* blocks, cudaStream_t s) {
-    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL, SLB_ERR_INVALID_ARG, "bad kernel");
-    SLB_REQUIRE(n_trg >= 0 && ns >= 2 && nt >= 4 && nt % 2 == 0, SLB_ERR_INVALID_ARG, "bad sizes");
-    SLB_REQUIRE(ns <= kMaxNsQ && nt <= kMaxNtQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
-    SLB_REQUIRE(order >= 4 && order <= kMaxQ && beta > 0.0, SLB_ERR_INVALID_ARG, "need 4 <= order <= 24, beta > 0");
-    if (n_trg == 0) return SLB_OK;
-    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks, SLB_ERR_INVALID_ARG, "null pointer");
-    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes needs eta_panel");
-    SLB_REQUIRE(n_trg <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets");
+static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                               const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
+                               const double* y_coarse, const double* eta_panel, int order, double beta,
+                               double* blocks, cudaStream_t s, const int32_t* pnt, const int64_t* cn0,
+                               const int64_t* boff) {
     static QuadParams P;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
+    P.dl = (kernel == SLB_STOKES_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
     gl_nodes(ns, P.tgl, w);
     for (int i = 0; i < ns; ++i) {
@@ -387,9 +423,9 @@ extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const 
     gl_nodes(P.qd, P.dx, P.dw);
     for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
     const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
-    const int Nn = ns * nt;
-    const size_t smem = sizeof(double) * ((size_t)Nn * 3 + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns + nt)) +
-                        sizeof(Cell) * kMaxCells;
+    const int Nn = ns * nt;   // (largest) panel
+    const size_t smem = sizeof(double) * ((size_t)Nn * 3 + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns + nt) +
+                                          2 * (size_t)nt) + sizeof(Cell) * kMaxCells;
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
     SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int* st = nullptr;
@@ -397,7 +433,7 @@ extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const 
     SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
     const FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE : FAR_STOKES_SLDL;
     nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem, s>>>((int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx,
-                                                             y_coarse, eta_panel, P, blocks, st);
+                                                             y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff);
     ++g_launch_count;
     slb_status r = check_launch("nearquad_kernel");
     int h = 0;
@@ -411,5 +447,81 @@ extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const 
         set_error("nearquad: adaptive cell budget exceeded (target extremely close to a panel?)");
         r = SLB_ERR_UNSUPPORTED;
     }
+    return r;
+}
+
+static slb_status nearquad_check(slb_kernel kernel, int64_t n_trg, int ns, int order, double beta) {
+    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL || kernel == SLB_STOKES_SL,
+                SLB_ERR_INVALID_ARG, "bad kernel");
+    SLB_REQUIRE(n_trg >= 0 && ns >= 2, SLB_ERR_INVALID_ARG, "bad sizes");
+    SLB_REQUIRE(ns <= kMaxNsQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
+    SLB_REQUIRE(order >= 4 && order <= kMaxQ && beta > 0.0, SLB_ERR_INVALID_ARG, "need 4 <= order <= 24, beta > 0");
+    SLB_REQUIRE(n_trg <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets");
+    return SLB_OK;
+}
+
+extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                                        const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
+                                        const double* y_coarse, const double* eta_panel, int order, double beta,
+                                        double* blocks, cudaStream_t s) {
+    slb_status c = nearquad_check(kernel, n_trg, ns, order, beta);
+    if (c != SLB_OK) return c;
+    SLB_REQUIRE(nt >= 4 && nt % 2 == 0, SLB_ERR_INVALID_ARG, "bad sizes");
+    SLB_REQUIRE(nt <= kMaxNtQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
+    return nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, nt, y_coarse, eta_panel, order, beta,
+                        blocks, s, nullptr, nullptr, nullptr);
+}
+
+extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg, const double* x_trg,
+                                               const int64_t* trg_node, const int64_t* row_ptr,
+                                               const int32_t* panel_idx, int64_t n_panels, int ns,
+                                               const int32_t* panel_nt, const double* y_coarse,
+                                               const double* eta_panel, int order, double beta, double* blocks,
+                                               cudaStream_t s) {
+    slb_status c = nearquad_check(kernel, n_trg, ns, order, beta);
+    if (c != SLB_OK) return c;
+    if (n_trg == 0) return SLB_OK;
+    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks && panel_nt && n_panels > 0, SLB_ERR_INVALID_ARG,
+                "null pointer");
+    SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
+    const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
+    std::vector<int64_t> c0(n_panels + 1, 0);
+    int ntmax = 0;
+    for (int64_t k = 0; k < n_panels; ++k) {
+        SLB_REQUIRE(panel_nt[k] >= 4 && panel_nt[k] % 2 == 0, SLB_ERR_INVALID_ARG, "bad panel_nt");
+        SLB_REQUIRE(panel_nt[k] <= kMaxNtQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
+        c0[k + 1] = c0[k] + (int64_t)ns * panel_nt[k];
+        ntmax = std::max(ntmax, (int)panel_nt[k]);
+    }
+    int64_t nnz = 0;
+    SLB_CUDA(cudaStreamSynchronize(s));
+    SLB_CUDA(cudaMemcpy(&nnz, row_ptr + n_trg, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> pk(std::max<int64_t>(nnz, 1));
+    if (nnz) SLB_CUDA(cudaMemcpy(pk.data(), panel_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> bo(nnz + 1, 0);
+    for (int64_t p = 0; p < nnz; ++p) {
+        SLB_REQUIRE(pk[p] >= 0 && pk[p] < n_panels, SLB_ERR_INVALID_ARG, "panel_idx entry outside [0, n_panels)");
+        bo[p + 1] = bo[p] + (int64_t)TD * (c0[pk[p] + 1] - c0[pk[p]]) * TD;
+    }
+    int32_t* pnt_d = nullptr;
+    int64_t *c0_d = nullptr, *bo_d = nullptr;
+    auto cleanup = [&]() { cudaFree(pnt_d); cudaFree(c0_d); cudaFree(bo_d); };
+    if (cudaMalloc(&pnt_d, sizeof(int32_t) * n_panels) != cudaSuccess ||
+        cudaMalloc(&c0_d, sizeof(int64_t) * (n_panels + 1)) != cudaSuccess ||
+        cudaMalloc(&bo_d, sizeof(int64_t) * (nnz + 1)) != cudaSuccess) {
+        cleanup();
+        set_error("slb_nearcorr_quad_ragged: out of device memory");
+        return SLB_ERR_OOM;
+    }
+    cudaMemcpy(pnt_d, panel_nt, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
+    cudaMemcpy(c0_d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(bo_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice);
+    slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, ntmax, y_coarse, eta_panel,
+                                order, beta, blocks, s, pnt_d, c0_d, bo_d);
+    cudaStreamSynchronize(s);
+    cleanup();
     return r;
 }

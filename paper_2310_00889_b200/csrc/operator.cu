@@ -19,19 +19,26 @@
 
 using namespace slb;
 
-static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cudaStream_t s) {
+// In-place all-gather of per-panel data: rank r owns elements [E(ranges[r]), E(ranges[r+1])) with
+// E(p) = p * per_panel (uniform) or off[p] * unit (ragged panels, off = node offsets).
+static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cudaStream_t s,
+                            const std::vector<int64_t>* off = nullptr, int64_t unit = 1) {
     slb_comm* c = op->comm;
     if (!c || c->nranks == 1) return SLB_OK;
     NcclApi& A = nccl();
-    if (op->equal_shards) {
-        size_t cnt = (size_t)((op->ranges[1] - op->ranges[0]) * per_panel);
-        SLB_NCCL(A.AllGather(buf + op->ranges[c->rank] * per_panel, buf, cnt, ncclDouble, c->comm, s));
+    auto E = [&](int64_t p) { return off ? (*off)[p] * unit : p * per_panel; };
+    bool equal = true;
+    for (int r = 1; r < c->nranks; ++r)
+        if (E(op->ranges[r + 1]) - E(op->ranges[r]) != E(op->ranges[1]) - E(op->ranges[0])) equal = false;
+    if (equal) {
+        size_t cnt = (size_t)(E(op->ranges[1]) - E(op->ranges[0]));
+        SLB_NCCL(A.AllGather(buf + E(op->ranges[c->rank]), buf, cnt, ncclDouble, c->comm, s));
     } else {
         SLB_NCCL(A.GroupStart());
         for (int r = 0; r < c->nranks; ++r) {
-            size_t cnt = (size_t)((op->ranges[r + 1] - op->ranges[r]) * per_panel);
+            size_t cnt = (size_t)(E(op->ranges[r + 1]) - E(op->ranges[r]));
             if (cnt == 0) continue;
-            double* p = buf + op->ranges[r] * per_panel;
+            double* p = buf + E(op->ranges[r]);
             SLB_NCCL(A.Broadcast(p, p, cnt, ncclDouble, r, c->comm, s));
         }
         SLB_NCCL(A.GroupEnd());
@@ -44,6 +51,10 @@ static void free_op(slb_operator* op) {
     cudaFree(op->geo); cudaFree(op->sc); cudaFree(op->dyn); cudaFree(op->coarse);
     cudaFree(op->partials); cudaFree(op->Lsig); cudaFree(op->nb0); cudaFree(op->bodyc);
     cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev); cudaFree(op->rec);
+    cudaFree(op->cn0_d); cudaFree(op->fn0_d); cudaFree(op->lc0_d); cudaFree(op->lf0_d); cudaFree(op->boff_d);
+    cudaFree(op->pbucket_d);
+    for (auto& b : op->buckets) { cudaFree(b.plist_d); cudaFree(b.ip_buf); }
+    cudaFree(op->ip_buf);
     for (auto& e : op->ev) if (e) cudaEventDestroy(e);
     if (op->graph) cudaGraphExecDestroy(op->graph);
     for (auto& w : op->ws) if (w) cudaStreamDestroy(w);
@@ -95,9 +106,10 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     SLB_REQUIRE(d && out, SLB_ERR_INVALID_ARG, "null descriptor/out");
     *out = nullptr;
     SLB_REQUIRE(d->kernel == SLB_LAPLACE_DL || d->kernel == SLB_STOKES_SLDL, SLB_ERR_INVALID_ARG, "bad kernel");
-    SLB_REQUIRE(d->ns >= 1 && d->nt >= 2 && d->ms >= 1 && d->mt >= 2 && d->nt % 2 == 0, SLB_ERR_INVALID_ARG,
-                "bad grid");
-    SLB_REQUIRE(d->ns <= SLB_MAX_NS && d->nt <= SLB_MAX_NT && d->ms <= SLB_MAX_MS && d->mt <= SLB_MAX_MT,
+    const bool rag = d->panel_nt || d->panel_mt;      // ragged: nt, mt ignored (per-panel tables)
+    SLB_REQUIRE(d->ns >= 1 && d->ms >= 1 && (rag || (d->nt >= 2 && d->mt >= 2 && d->nt % 2 == 0)),
+                SLB_ERR_INVALID_ARG, "bad grid");
+    SLB_REQUIRE(d->ns <= SLB_MAX_NS && d->ms <= SLB_MAX_MS && (rag || (d->nt <= SLB_MAX_NT && d->mt <= SLB_MAX_MT)),
                 SLB_ERR_UNSUPPORTED, "grid beyond compiled limits");
     SLB_REQUIRE(d->n_panels_global >= 1 && d->panel_begin >= 0 && d->panel_end >= d->panel_begin &&
                     d->panel_end <= d->n_panels_global,
@@ -117,17 +129,97 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     op->sdim = op->tdim = (d->kernel == SLB_LAPLACE_DL) ? 1 : 3;
     if (d->kernel == SLB_LAPLACE_DL) op->kind = FAR_LAPLACE;
     else op->kind = (d->eta_fine || d->eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL;
-    if (!make_interp(d->ns, d->nt, d->ms, d->mt, &op->ip)) {
-        delete op;
-        set_error("slb_operator_create: interpolation matrices too large");
-        return SLB_ERR_UNSUPPORTED;
+    op->ragged = d->panel_nt || d->panel_mt;
+    if (op->ragged) {
+        // (NEXT N4) per-panel angular orders: node offsets and one interpolation bucket per (nt, mt)
+        if (!(d->panel_nt && d->panel_mt)) {
+            free_op(op);
+            set_error("slb_operator_create: panel_nt and panel_mt must both be given (or both NULL)");
+            return SLB_ERR_INVALID_ARG;
+        }
+        const int64_t P = d->n_panels_global;
+        op->cn0.assign(P + 1, 0);
+        op->fn0.assign(P + 1, 0);
+        std::vector<int32_t> pb(P);
+        for (int64_t k = 0; k < P; ++k) {
+            const int nt = d->panel_nt[k], mt = d->panel_mt[k];
+            if (!(nt >= 2 && nt % 2 == 0 && mt >= 2 && nt <= SLB_MAX_NT && mt <= SLB_MAX_MT)) {
+                free_op(op);
+                set_error("slb_operator_create: panel orders must be even and within the compiled limits");
+                return SLB_ERR_INVALID_ARG;
+            }
+            op->cn0[k + 1] = op->cn0[k] + (int64_t)d->ns * nt;
+            op->fn0[k + 1] = op->fn0[k] + (int64_t)d->ms * mt;
+            op->max_cols = std::max(op->max_cols, d->ns * nt * op->sdim);
+            int b = 0;
+            while (b < (int)op->buckets.size() && !(op->buckets[b].nt == nt && op->buckets[b].mt == mt)) ++b;
+            if (b == (int)op->buckets.size()) {
+                op->buckets.emplace_back();
+                slb_operator::Bucket& nb = op->buckets.back();
+                nb.nt = nt;
+                nb.mt = mt;
+                if (!make_interp(d->ns, nt, d->ms, mt, &nb.ip, &nb.ip_buf)) {
+                    free_op(op);
+                    set_error("slb_operator_create: interpolation matrices: allocation failed");
+                    return SLB_ERR_OOM;
+                }
+            }
+            pb[k] = b;
+            if (k >= d->panel_begin && k < d->panel_end) op->buckets[b].n_loc++;
+        }
+        op->ip = op->buckets[0].ip;
+        op->Nn = 0;                              // no uniform panel size
+        op->Mn = 0;
+        op->M = op->fn0[P];
+        op->P_loc = d->panel_end - d->panel_begin;
+        op->N_loc = op->cn0[d->panel_end] - op->cn0[d->panel_begin];
+        op->cols = 0;
+        // device tables (setup; synchronous)
+        const int64_t Pl = op->P_loc;
+        std::vector<int64_t> lc(Pl + 1), lf(Pl + 1);
+        for (int64_t q = 0; q <= Pl; ++q) {
+            lc[q] = op->cn0[d->panel_begin + q] - op->cn0[d->panel_begin];
+            lf[q] = op->fn0[d->panel_begin + q] - op->fn0[d->panel_begin];
+        }
+        bool okm = cudaMalloc(&op->cn0_d, sizeof(int64_t) * (P + 1)) == cudaSuccess &&
+                   cudaMalloc(&op->fn0_d, sizeof(int64_t) * (P + 1)) == cudaSuccess &&
+                   cudaMalloc(&op->lc0_d, sizeof(int64_t) * (Pl + 1)) == cudaSuccess &&
+                   cudaMalloc(&op->lf0_d, sizeof(int64_t) * (Pl + 1)) == cudaSuccess &&
+                   cudaMalloc(&op->pbucket_d, sizeof(int32_t) * P) == cudaSuccess;
+        if (okm) {
+            cudaMemcpy(op->cn0_d, op->cn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice);
+            cudaMemcpy(op->fn0_d, op->fn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice);
+            cudaMemcpy(op->lc0_d, lc.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
+            cudaMemcpy(op->lf0_d, lf.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
+            cudaMemcpy(op->pbucket_d, pb.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice);
+            for (auto& b : op->buckets) {
+                std::vector<int32_t> pl;
+                for (int64_t q = 0; q < Pl; ++q)
+                    if (d->panel_nt[d->panel_begin + q] == b.nt && d->panel_mt[d->panel_begin + q] == b.mt)
+                        pl.push_back((int32_t)q);
+                if (pl.empty()) continue;
+                okm = okm && cudaMalloc(&b.plist_d, sizeof(int32_t) * pl.size()) == cudaSuccess;
+                if (okm) cudaMemcpy(b.plist_d, pl.data(), sizeof(int32_t) * pl.size(), cudaMemcpyHostToDevice);
+            }
+        }
+        if (!okm) {
+            free_op(op);
+            set_error("slb_operator_create: out of device memory (ragged tables)");
+            return SLB_ERR_OOM;
+        }
+    } else {
+        if (!make_interp(d->ns, d->nt, d->ms, d->mt, &op->ip, &op->ip_buf)) {
+            free_op(op);
+            set_error("slb_operator_create: interpolation matrices: allocation failed");
+            return SLB_ERR_OOM;
+        }
+        op->Nn = (int64_t)d->ns * d->nt;
+        op->Mn = (int64_t)d->ms * d->mt;
+        op->M = d->n_panels_global * op->Mn;
+        op->P_loc = d->panel_end - d->panel_begin;
+        op->N_loc = op->P_loc * op->Nn;
+        op->cols = op->Nn * op->sdim;
     }
-    op->Nn = (int64_t)d->ns * d->nt;
-    op->Mn = (int64_t)d->ms * d->mt;
-    op->M = d->n_panels_global * op->Mn;
-    op->P_loc = d->panel_end - d->panel_begin;
-    op->N_loc = op->P_loc * op->Nn;
-    op->cols = op->Nn * op->sdim;
     op->plan = far_plan(op->M);
     {
         const char* e = getenv("SLB_FAR_PATH");
@@ -191,24 +283,45 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
             if (op->ranges[q + 1] - op->ranges[q] != op->ranges[1] - op->ranges[0]) op->equal_shards = false;
     }
     const int64_t T = d->n_trg_local;
-    const int64_t Mloc = op->P_loc * op->Mn;
+    const int64_t Mloc = op->ragged ? op->fn0[d->panel_end] - op->fn0[d->panel_begin] : op->P_loc * op->Mn;
+    const int64_t n_coarse_global = op->ragged ? op->cn0[d->n_panels_global] * op->sdim : d->n_panels_global * op->cols;
     OPCUDA(cudaMalloc(&op->geo, sizeof(double) * op->M * 6));
     OPCUDA(cudaMalloc(&op->sc, sizeof(double) * std::max<int64_t>(Mloc, 1) * 3));
     OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
-    OPCUDA(cudaMalloc(&op->coarse, sizeof(double) * d->n_panels_global * op->cols));
+    OPCUDA(cudaMalloc(&op->coarse, sizeof(double) * n_coarse_global));
     OPCUDA(cudaMalloc(&op->partials, sizeof(double) * std::max<int64_t>(op->plan.n_chunks * T * op->tdim, 1)));
     OPCUDA(cudaMalloc(&op->sig_dev, sizeof(double) * std::max<int64_t>(op->N_loc * op->sdim, 1)));
     OPCUDA(cudaMalloc(&op->u_dev, sizeof(double) * std::max<int64_t>(T * op->tdim, 1)));
     OPCUDA(cudaMemset(op->dyn, 0, sizeof(double) * op->M * 4));
-    OPCUDA(cudaMemset(op->coarse, 0, sizeof(double) * d->n_panels_global * op->cols));
+    OPCUDA(cudaMemset(op->coarse, 0, sizeof(double) * n_coarse_global));
     if (T > 0) OPST(csr_check(T, d->row_ptr, d->panel_idx, d->n_panels_global));
-    const int64_t f0 = d->panel_begin * op->Mn;
+    const int64_t f0 = op->ragged ? op->fn0[d->panel_begin] : d->panel_begin * op->Mn;
+    if (op->ragged && T > 0) {
+        // block offsets in CSR order: block p = [tdim][ns nt_k sdim], k = panel_idx[p]
+        int64_t nnz = 0;
+        OPCUDA(cudaMemcpy(&nnz, d->row_ptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> pk(std::max<int64_t>(nnz, 1));
+        if (nnz) OPCUDA(cudaMemcpy(pk.data(), d->panel_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> bo(nnz + 1, 0);
+        for (int64_t p = 0; p < nnz; ++p)
+            bo[p + 1] = bo[p] + (int64_t)op->tdim * (op->cn0[pk[p] + 1] - op->cn0[pk[p]]) * op->sdim;
+        OPCUDA(cudaMalloc(&op->boff_d, sizeof(int64_t) * (nnz + 1)));
+        OPCUDA(cudaMemcpy(op->boff_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice));
+    }
     OPST(pack_geo(op->kind, op->M, d->y_fine, d->n_fine, d->eta_fine, d->eta, op->geo, s));
     OPST(pack_scale(op->kind, Mloc, d->n_fine + 3 * f0, d->w_fine + f0, d->eta_fine ? d->eta_fine + f0 : nullptr,
                     d->eta, op->sc, s));
-    if (!d->blocks_folded && T > 0 && d->blocks)
-        OPST(fold_launch(op->kind, T, d->x_trg, d->row_ptr, d->panel_idx, op->ip, d->y_fine, d->n_fine,
-                         d->w_fine, d->eta_fine, d->eta, d->blocks, s));
+    if (!d->blocks_folded && T > 0 && d->blocks) {
+        if (op->ragged) {
+            for (int b = 0; b < (int)op->buckets.size(); ++b)
+                OPST(fold_launch(op->kind, T, d->x_trg, d->row_ptr, d->panel_idx, op->buckets[b].ip, d->y_fine,
+                                 d->n_fine, d->w_fine, d->eta_fine, d->eta, d->blocks, s, op->pbucket_d, b,
+                                 op->fn0_d, op->boff_d));
+        } else {
+            OPST(fold_launch(op->kind, T, d->x_trg, d->row_ptr, d->panel_idx, op->ip, d->y_fine, d->n_fine,
+                             d->w_fine, d->eta_fine, d->eta, d->blocks, s));
+        }
+    }
     // projector: body node offsets (local), moments, inverse inertia
     if (d->n_bodies_local > 0) {
         if (!(d->body_of_panel_local && d->y_coarse && d->w_coarse)) {
@@ -225,7 +338,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
                 set_error("slb_operator_create: body_of_panel_local must be nondecreasing in [0, n_bodies_local)");
                 return fail(SLB_ERR_INVALID_ARG);
             }
-            nb0[b + 1] += op->Nn;
+            nb0[b + 1] += op->ragged ? op->cn0[d->panel_begin + p + 1] - op->cn0[d->panel_begin + p] : op->Nn;
         }
         for (int64_t b = 0; b < nb; ++b) nb0[b + 1] += nb0[b];
         for (int64_t b = 0; b < nb; ++b) op->max_nodes_body = std::max(op->max_nodes_body, nb0[b + 1] - nb0[b]);
@@ -310,7 +423,8 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
     slb_status st;
     SLB_CUDA(cudaEventRecord(op->ev[0], s));
-    double* sig_p = op->coarse + d.panel_begin * op->cols;   // local sigma' inside the global coarse buffer
+    // local sigma' inside the global coarse buffer
+    double* sig_p = op->coarse + (op->ragged ? op->cn0[d.panel_begin] * op->sdim : d.panel_begin * op->cols);
     const double* Lsig = nullptr;
     if (d.n_bodies_local > 0) {
         st = proj_launch(d.n_bodies_local, op->nb0, d.y_coarse, d.w_coarse, op->bodyc, sigma_local, op->coef, sig_p,
@@ -320,13 +434,23 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     } else if (op->N_loc > 0) {
         SLB_CUDA(cudaMemcpyAsync(sig_p, sigma_local, sizeof(double) * op->N_loc * op->sdim, cudaMemcpyDeviceToDevice, s));
     }
-    st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, sig_p, nullptr, op->sc,
-                         op->dyn + d.panel_begin * op->Mn * 4, s);
-    if (st != SLB_OK) return st;
+    if (op->ragged) {
+        double* dyn_loc = op->dyn + op->fn0[d.panel_begin] * 4;
+        for (auto& b : op->buckets) {
+            if (!b.n_loc) continue;
+            st = upsample_launch(op->kind, b.n_loc, b.ip, op->sdim, sig_p, nullptr, op->sc, dyn_loc, s, b.plist_d,
+                                 op->lc0_d, op->lf0_d);
+            if (st != SLB_OK) return st;
+        }
+    } else {
+        st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, sig_p, nullptr, op->sc,
+                             op->dyn + d.panel_begin * op->Mn * 4, s);
+        if (st != SLB_OK) return st;
+    }
     SLB_CUDA(cudaEventRecord(op->ev[1], s));
-    st = allgather(op, op->dyn, op->Mn * 4, s);
+    st = op->ragged ? allgather(op, op->dyn, 0, s, &op->fn0, 4) : allgather(op, op->dyn, op->Mn * 4, s);
     if (st != SLB_OK) return st;
-    st = allgather(op, op->coarse, op->cols, s);
+    st = op->ragged ? allgather(op, op->coarse, 0, s, &op->cn0, op->sdim) : allgather(op, op->coarse, op->cols, s);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[2], s));
     if (op->use_const) {
@@ -347,8 +471,14 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
         if (st != SLB_OK) return st;
     }
     SLB_CUDA(cudaEventRecord(op->ev[3], s));
+    RagNear rag;
+    if (op->ragged) {
+        rag.cn0 = op->cn0_d;
+        rag.boff = op->boff_d;
+        rag.max_cols = op->max_cols;
+    }
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
-                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, op->near_G, s);
+                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, op->near_G, s, rag);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[4], s));
     op->timed = true;
@@ -378,6 +508,10 @@ slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]) {
 int slb_operator_launches_per_matvec(const slb_operator* op) {
     if (!op) return -1;
     int n = 3;                                   // upsample, far, finalize
+    if (op->ragged) {                            // one upsample per bucket with local panels
+        n -= 1;
+        for (auto& b : op->buckets) n += b.n_loc > 0;
+    }
     if (op->use_const) n += 1 + (int)op->const_launches - 1;   // pack_rec + one launch per source tile
     if (op->d.n_bodies_local > 0) n += 2;        // projector coef + apply
     return n;

@@ -71,6 +71,7 @@ struct slb_operator {
     int tdim = 1, sdim = 1;
     slb::FarPlan plan;
     slb::InterpParams ip;
+    double* ip_buf = nullptr;           // device interpolation matrices (large grids)
     int64_t P_loc = 0, N_loc = 0, Nn = 0, Mn = 0, M = 0, cols = 0;
     std::vector<int64_t> ranges;        // panel offsets of all ranks [R+1]
     bool equal_shards = true;
@@ -97,5 +98,23 @@ struct slb_operator {
     cudaGraphExec_t graph = nullptr;
     int64_t const_launches = 0;
     int near_G = 1;                     // targets per warp in the near stream kernel
+    // ragged angular orders (NEXT N4): per-(nt, mt) buckets; all empty / NULL for uniform panels
+    bool ragged = false;
+    std::vector<int64_t> cn0, fn0;      // host [P_global+1] first coarse / fine node of each panel
+    int64_t* cn0_d = nullptr;           // device copy of cn0
+    int64_t* fn0_d = nullptr;           // device copy of fn0
+    int64_t* lc0_d = nullptr;           // [P_loc+1] local coarse offsets (cn0 - cn0[begin])
+    int64_t* lf0_d = nullptr;           // [P_loc+1] local fine offsets (fn0 - fn0[begin])
+    int64_t* boff_d = nullptr;          // [nnz+1] block offsets (doubles)
+    int32_t* pbucket_d = nullptr;       // [P_global] bucket of each panel
+    struct Bucket {
+        int nt, mt;
+        slb::InterpParams ip;
+        int64_t n_loc = 0;              // local panels in this bucket
+        int32_t* plist_d = nullptr;     // their local panel ids
+        double* ip_buf = nullptr;       // device interpolation matrices when too large for ip.v
+    };
+    std::vector<Bucket> buckets;
+    int max_cols = 0;                   // widest block (nodes * sdim)
 };
 

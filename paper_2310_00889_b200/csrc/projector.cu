@@ -106,6 +106,43 @@ proj_apply_kernel(const int64_t* __restrict__ nb0, const double* __restrict__ y,
     sigma_p[3 * q + 2] = sigma[3 * q + 2] - l2;
 }
 
+// completion-flow density nu = alpha + beta x (y - c) with int nu = F, int nu x (y - c) = T
+// (P:L1903-1912).  c = w-centroid, so int (y - c) = 0:  alpha = F / A,  beta = -I^-1 T  (I as above).
+__global__ void __launch_bounds__(256)
+completion_kernel(const int64_t* __restrict__ nb0, const double* __restrict__ y, const double* __restrict__ bodyc,
+                  const double* __restrict__ ft, double* __restrict__ nu) {
+    const int64_t b = blockIdx.y;
+    const int64_t q = nb0[b] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nb0[b + 1]) return;
+    const double* bc = bodyc + b * 16;
+    const double* f = ft + b * 6;
+    const double* Ii = bc + 4;
+    const double A = bc[0];
+    double be[3];
+    for (int r = 0; r < 3; ++r) be[r] = -(Ii[3 * r] * f[3] + Ii[3 * r + 1] * f[4] + Ii[3 * r + 2] * f[5]);
+    const double d0 = y[3 * q] - bc[1], d1 = y[3 * q + 1] - bc[2], d2 = y[3 * q + 2] - bc[3];
+    nu[3 * q] = f[0] / A + (be[1] * d2 - be[2] * d1);
+    nu[3 * q + 1] = f[1] / A + (be[2] * d0 - be[0] * d2);
+    nu[3 * q + 2] = f[2] / A + (be[0] * d1 - be[1] * d0);
+}
+
+slb_status completion_launch(int64_t n_bodies, const int64_t* nb0, const double* y, const double* bodyc,
+                             const double* ft, double* nu, int64_t max_nodes_per_body, cudaStream_t s) {
+    if (n_bodies <= 0) return SLB_OK;
+    dim3 grid((unsigned)((max_nodes_per_body + 255) / 256), (unsigned)n_bodies);
+    completion_kernel<<<grid, 256, 0, s>>>(nb0, y, bodyc, ft, nu);
+    ++g_launch_count;
+    return check_launch("completion_kernel");
+}
+
+slb_status proj_coef_launch(int64_t n_bodies, const int64_t* nb0, const double* y, const double* w,
+                            const double* bodyc, const double* sigma, double* coef, cudaStream_t s) {
+    if (n_bodies <= 0) return SLB_OK;
+    proj_coef_kernel<<<(unsigned)n_bodies, 256, 0, s>>>(nb0, y, w, bodyc, sigma, coef);
+    ++g_launch_count;
+    return check_launch("proj_coef_kernel");
+}
+
 slb_status body_moments_launch(int64_t n_bodies, const int64_t* nb0, const double* y, const double* w,
                                double* mom, cudaStream_t s) {
     if (n_bodies <= 0) return SLB_OK;

@@ -25,116 +25,140 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 __device__ __forceinline__ int rup(int v, int m) { return (v + m - 1) / m * m; }
+// shared-memory leading dimensions (doubles) that keep the DMMA fragment loads <= 2-way bank
+// conflicted: rows indexed by the fragment's g (8 rows) want ld = 4 or 12 (mod 16); rows indexed by
+// tq (4 rows, 8 consecutive g) want ld = 8 (mod 16)
+__host__ __device__ __forceinline__ int ld_g(int x) { return (x % 16 == 0 || x % 16 == 8) ? x + 4 : x; }
+__host__ __device__ __forceinline__ int ld_t(int x) { return (x % 16 == 0) ? x + 8 : x; }
 
-// shared layout (doubles):
-//   Ps  [msp][nsp]           (zero padded; msp = rup(ms,8), nsp = rup(ns,4))
-//   F   [mtp][ntp]           (mtp = rup(mt,8), ntp = rup(nt,4))
-//   per warp: sig [rowsp][ntp]  rows (i,c) padded to rup(ns*nc, 8)
-//             T1  [nsp][mtp*nc] laid out as T1[i][(b,c)] (rows i padded to nsp, zero)
+// shared layout (doubles), one panel per CTA at a time:
+//   Ps  [msp][ldp]           (zero padded; msp = rup(ms,8), nsp = rup(ns,4), ldp >= nsp)
+//   F   [mtp][ldf]           (mtp = rup(mt,8), ntp = rup(nt,4), ldf >= ntp)
+//   raw [ns][nt][nc]         the panel's coarse density as stored (A operand of step 1 read in place)
+//   T1  [nsp][ld1]           T1[i][(b,c)] (rows i padded to nsp, zero)
+//   O   [ms][mt][nc]         step-2 result, written to HBM as whole 32-byte records
+// The CTA's warps split the 8x8 output tiles of both steps (a panel is 39 tiles at 10x12 -> 20x24,
+// 224 at 12x64 -> 24x128), so large panels are not serialised on one warp.
+// Ragged panels (NEXT N4): the launch covers the n_panels panels plist[0..n_panels) (NULL: 0..n-1)
+// of one (nt, mt) bucket; c_off / f_off give each panel's first coarse / fine node (NULL: uniform).
 __global__ void __launch_bounds__(kUpWarps * 32)
 upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__ InterpParams ip,
                      const double* __restrict__ sc_in, double* __restrict__ sf_out,
-                     const double* __restrict__ scale, double* __restrict__ dyn) {
+                     const double* __restrict__ scale, double* __restrict__ dyn,
+                     const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
+                     const int64_t* __restrict__ f_off) {
     extern __shared__ double sm[];
     const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
     const int nsp = rup(ns, 4), ntp = rup(nt, 4), msp = rup(ms, 8), mtp = rup(mt, 8);
     const int rows = ns * nc, rowsp = rup(rows, 8);
     const int ncol2 = mt * nc, ncol2p = rup(ncol2, 8);
-    double* Ps = sm;                          // [msp][nsp]
-    double* F = Ps + msp * nsp;               // [mtp][ntp]
-    double* wbase = F + mtp * ntp;
-    const int per_warp = rowsp * ntp + nsp * ncol2p;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* sig = wbase + warp * per_warp;    // [rowsp][ntp]
-    double* T1 = sig + rowsp * ntp;           // [nsp][ncol2p]
-    for (int q = threadIdx.x; q < msp * nsp; q += blockDim.x) {
-        const int a = q / nsp, i = q % nsp;
-        Ps[q] = (a < ms && i < ns) ? ip.v[a * ns + i] : 0.0;
-    }
-    for (int q = threadIdx.x; q < mtp * ntp; q += blockDim.x) {
-        const int b = q / ntp, j = q % ntp;
-        F[q] = (b < mt && j < nt) ? ip.v[ms * ns + b * nt + j] : 0.0;
-    }
-    __syncthreads();
-    const int g = lane >> 2, tq = lane & 3;   // fragment coordinates
+    const int ldp = ld_g(nsp), ldf = ld_g(ntp), ld1 = ld_t(ncol2p);
     const int nin = ns * nt * nc;
-    for (int64_t p = (int64_t)blockIdx.x * kUpWarps + warp; p < n_panels; p += (int64_t)gridDim.x * kUpWarps) {
-        // stage the panel's coarse density as sig[(i,c)][j] (zero padded)
-        const double* src = sc_in + p * nin;
-        for (int q = lane; q < rowsp * ntp; q += 32) sig[q] = 0.0;
-        __syncwarp();
-        for (int q = lane; q < nin; q += 32) {
-            const int c = q % nc, j = (q / nc) % nt, i = q / (nc * nt);
-            sig[(i * nc + c) * ntp + j] = src[q];
+    const int nout = ms * mt;
+    double* Ps = sm;                          // [msp][ldp]
+    double* F = Ps + msp * ldp;               // [mtp][ldf]
+    double* raw = F + mtp * ldf;              // [ns][nt][nc] (rup to 2)
+    double* T1 = raw + ((nin + 1) & ~1);      // [nsp][ld1]
+    double* O = T1 + nsp * ld1;               // [ms][mt][nc]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const double* V = ip.vg ? ip.vg : ip.v;
+    for (int q = threadIdx.x; q < msp * ldp; q += blockDim.x) {
+        const int a = q / ldp, i = q % ldp;
+        Ps[q] = (a < ms && i < ns) ? V[a * ns + i] : 0.0;
+    }
+    for (int q = threadIdx.x; q < mtp * ldf; q += blockDim.x) {
+        const int b = q / ldf, j = q % ldf;
+        F[q] = (b < mt && j < nt) ? V[ms * ns + b * nt + j] : 0.0;
+    }
+    const int g = lane >> 2, tq = lane & 3;   // fragment coordinates
+    const int nt1 = (rowsp / 8) * (mtp / 8);  // step-1 tiles
+    const int nt2 = (msp / 8) * (ncol2p / 8); // step-2 tiles
+    for (int64_t pl = blockIdx.x; pl < n_panels; pl += gridDim.x) {
+        const int64_t p = plist ? (int64_t)plist[pl] : pl;
+        const int64_t m0 = f_off ? f_off[p] : p * (int64_t)nout;
+        // stage the panel's coarse density unchanged (contiguous, coalesced)
+        const double* src = sc_in + (c_off ? c_off[p] * nc : p * nin);
+        __syncthreads();                      // previous panel's O fully written out; Ps/F staged
+        for (int q = threadIdx.x; q < nin; q += blockDim.x) raw[q] = __ldg(src + q);
+        for (int q = threadIdx.x; q < nsp * ld1; q += blockDim.x) T1[q] = 0.0;
+        __syncthreads();
+        // step 1: T1[(i,c)][b] = sum_j sigma[i][j][c] F[b][j]   (A fragment read in place from raw)
+        for (int tile = warp; tile < nt1; tile += nwarps) {
+            const int r0 = (tile / (mtp / 8)) * 8, n0 = (tile % (mtp / 8)) * 8;
+            const int r = r0 + g;
+            const int rb = (r < rows) ? (r / nc) * nt * nc + (r % nc) : -1;   // raw index of (i, j = 0, c)
+            double d0 = 0.0, d1 = 0.0;
+            for (int k0 = 0; k0 < ntp; k0 += 4) {
+                const int j = k0 + tq;
+                const double av = (rb >= 0 && j < nt) ? raw[rb + j * nc] : 0.0;
+                dmma_8x8x4(d0, d1, av, F[(n0 + g) * ldf + k0 + tq]);
+            }
+            if (r < rows) {
+                const int i = r / nc, c = r % nc;
+                const int b0 = n0 + 2 * tq;
+                if (b0 < mt) T1[i * ld1 + b0 * nc + c] = d0;
+                if (b0 + 1 < mt) T1[i * ld1 + (b0 + 1) * nc + c] = d1;
+            }
         }
-        for (int q = lane; q < nsp * ncol2p; q += 32) T1[q] = 0.0;
-        __syncwarp();
-        // step 1: T1[(i,c)][b] = sum_j sig[(i,c)][j] F[b][j]
-        for (int r0 = 0; r0 < rowsp; r0 += 8)
-            for (int n0 = 0; n0 < mtp; n0 += 8) {
-                double d0 = 0.0, d1 = 0.0;
-                for (int k0 = 0; k0 < ntp; k0 += 4)
-                    dmma_8x8x4(d0, d1, sig[(r0 + g) * ntp + k0 + tq], F[(n0 + g) * ntp + k0 + tq]);
-                const int r = r0 + g;
-                if (r < rows) {
-                    const int i = r / nc, c = r % nc;
-                    const int b0 = n0 + 2 * tq;
-                    if (b0 < mt) T1[i * ncol2p + b0 * nc + c] = d0;
-                    if (b0 + 1 < mt) T1[i * ncol2p + (b0 + 1) * nc + c] = d1;
+        __syncthreads();
+        // step 2: O[a][(b,c)] = sum_i Ps[a][i] T1[i][(b,c)]
+        for (int tile = warp; tile < nt2; tile += nwarps) {
+            const int a0 = (tile / (ncol2p / 8)) * 8, n0 = (tile % (ncol2p / 8)) * 8;
+            double d0 = 0.0, d1 = 0.0;
+            for (int k0 = 0; k0 < nsp; k0 += 4)
+                dmma_8x8x4(d0, d1, Ps[(a0 + g) * ldp + k0 + tq], T1[(k0 + tq) * ld1 + n0 + g]);
+            const int a = a0 + g;
+            if (a >= ms) continue;
+            const int col = n0 + 2 * tq;
+            if (col < ncol2) O[a * ncol2 + col] = d0;
+            if (col + 1 < ncol2) O[a * ncol2 + col + 1] = d1;
+        }
+        __syncthreads();
+        // epilogue: whole 32-byte source records {g, 0} per fine node (coalesced), or the plain values
+        if (dyn) {
+            double2* D2 = reinterpret_cast<double2*>(dyn);
+            for (int e = threadIdx.x; e < nout; e += blockDim.x) {
+                const int64_t m = m0 + e;
+                double v0, v1, v2;
+                if (kind == FAR_LAPLACE) {
+                    const double v = O[e];
+                    v0 = scale[3 * m] * v; v1 = scale[3 * m + 1] * v; v2 = scale[3 * m + 2] * v;
+                } else {
+                    const double sc = scale[m];
+                    v0 = sc * O[3 * e]; v1 = sc * O[3 * e + 1]; v2 = sc * O[3 * e + 2];
                 }
+                D2[2 * m] = make_double2(v0, v1);
+                D2[2 * m + 1] = make_double2(v2, 0.0);
             }
-        __syncwarp();
-        // step 2: O[a][(b,c)] = sum_i Ps[a][i] T1[i][(b,c)]  + epilogue
-        for (int a0 = 0; a0 < msp; a0 += 8)
-            for (int n0 = 0; n0 < ncol2p; n0 += 8) {
-                double d0 = 0.0, d1 = 0.0;
-                for (int k0 = 0; k0 < nsp; k0 += 4)
-                    dmma_8x8x4(d0, d1, Ps[(a0 + g) * nsp + k0 + tq], T1[(k0 + tq) * ncol2p + n0 + g]);
-                const int a = a0 + g;
-                if (a >= ms) continue;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int col = n0 + 2 * tq + h;
-                    if (col >= ncol2) continue;
-                    const int b = col / nc, c = col % nc;
-                    const int64_t m = p * (int64_t)(ms * mt) + a * mt + b;
-                    const double v = h ? d1 : d0;
-                    if (dyn) {
-                        if (kind == FAR_LAPLACE) {
-                            dyn[m * 4] = scale[3 * m] * v;
-                            dyn[m * 4 + 1] = scale[3 * m + 1] * v;
-                            dyn[m * 4 + 2] = scale[3 * m + 2] * v;
-                        } else {
-                            dyn[m * 4 + c] = scale[m] * v;
-                        }
-                    } else {
-                        sf_out[m * nc + c] = v;
-                    }
-                }
-            }
-        __syncwarp();
+        } else {
+            for (int e = threadIdx.x; e < nout * nc; e += blockDim.x) sf_out[m0 * nc + e] = O[e];
+        }
     }
 }
 
 slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int nc,
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
-                           double* dyn, cudaStream_t s) {
+                           double* dyn, cudaStream_t s, const int32_t* plist, const int64_t* c_off,
+                           const int64_t* f_off) {
     if (n_panels <= 0) return SLB_OK;
     auto rup_h = [](int v, int m) { return (v + m - 1) / m * m; };
     const int nsp = rup_h(ip.ns, 4), ntp = rup_h(ip.nt, 4), msp = rup_h(ip.ms, 8), mtp = rup_h(ip.mt, 8);
-    const int rowsp = rup_h(ip.ns * nc, 8), ncol2p = rup_h(ip.mt * nc, 8);
-    const size_t smem = sizeof(double) * ((size_t)msp * nsp + (size_t)mtp * ntp +
-                                          (size_t)kUpWarps * (rowsp * ntp + nsp * ncol2p));
+    const int ncol2p = rup_h(ip.mt * nc, 8);
+    const int ldp = ld_g(nsp), ldf = ld_g(ntp), ld1 = ld_t(ncol2p);
+    const int nin = ip.ns * ip.nt * nc;
+    const size_t smem = sizeof(double) * ((size_t)msp * ldp + (size_t)mtp * ldf + (size_t)((nin + 1) & ~1) +
+                                          (size_t)nsp * ld1 + (size_t)ip.ms * ip.mt * nc);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "upsample: grid too large for shared memory");
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
         SLB_CUDA(cudaFuncSetAttribute(upsample_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         smem_set = smem;
     }
-    const int64_t want = (n_panels + kUpWarps - 1) / kUpWarps;
-    const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)num_sms() * 8);
+    // one panel per CTA and pass; enough CTAs for every SM to hold several
+    const unsigned grid = (unsigned)std::min<int64_t>(n_panels, (int64_t)num_sms() * 16);
     upsample_dmma_kernel<<<grid, kUpWarps * 32, smem, s>>>((int)kind, nc, n_panels, ip, sigma_coarse, sigma_fine, sc,
-                                                           dyn);
+                                                           dyn, plist, c_off, f_off);
     ++g_launch_count;
     return check_launch("upsample_dmma_kernel");
 }

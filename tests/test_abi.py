@@ -49,7 +49,7 @@ def test_sm100a_cubin_present():
 
 
 def test_host_entry_points(lib):
-    assert lib.slb_abi_version() == 1
+    assert lib.slb_abi_version() == 2
     assert lib.slb_eta_cfie(0.05) == pytest.approx(1 / (2 * 0.05 * math.log(20)), rel=1e-15)
     assert math.isnan(lib.slb_eta_cfie(0.0)) and math.isnan(lib.slb_eta_cfie(1.5))
     # argument validation happens before any CUDA call

@@ -48,3 +48,20 @@ def test_near_build_edge_cases():
     x = cu(np.array([[100.0, 0, 0], [100.0, 0, 0]]))
     rp, pi = slb_near_build(x, y, cu(np.ones(3)), cu(np.array([-1, 2]), torch.int64))
     assert rp.cpu().tolist() == [0, 0, 1] and pi.cpu().tolist() == [2]
+
+
+def test_near_build_ragged_by_padding():
+    """ragged panels (N4, c3v): pad each panel's nodes to the widest panel with copies of its first
+    node (the min over nodes is unchanged) -- bit-exact against the generator's CSR"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_00889_b200 import slb_near_build
+    pr = make_config("c3v", panels=16)
+    no = pr.node_off()
+    cnt = np.diff(no)
+    j = np.arange(cnt.max())[None, :]
+    idx = no[:-1, None] + np.where(j < cnt[:, None], j, 0)
+    own = np.repeat(np.arange(pr.P), cnt).astype(np.int64)
+    rp, pi = slb_near_build(cu(pr.x_trg), cu(pr.y_c[idx]), cu(2.0 * pr.panel_len), cu(own, torch.int64))
+    assert np.array_equal(rp.cpu().numpy(), pr.row_ptr)
+    assert np.array_equal(pi.cpu().numpy(), pr.panel_idx)

@@ -97,3 +97,74 @@ def test_ring_sedimentation_speed(rho, panels, nt):
     err = abs(U - U_exact) / U_exact
     print(f"rho={rho:g} P={panels} Nt={nt} N={pr.N} gmres it={it} U={U:.15e} exact={U_exact:.15e} rel.err={err:.2e}")
     assert err < TOL[rho], (U, U_exact, err)
+
+
+# ------------------------------------------------------------------ the library's mobility solve
+def _mobility_ops(pr, quad):
+    from harness import DeviceProblem
+    p = __import__("copy").copy(pr)
+    p.projector = True
+    return DeviceProblem(p, quad=quad), DeviceProblem(pr, quad=quad, single_layer=True)
+
+
+@pytest.mark.parametrize("rho,panels,nt", [(1e-1, 16, 12), (1e-2, 24, 12)])
+def test_mobility_solve_ring_sedimentation(rho, panels, nt):
+    """slb_mobility_solve (completion flow + S apply + GMRES + V = -L sigma inside libslb) gives the
+    paper's sedimentation speed (Table t:conv-sbt)"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from synth import make_torus_problem
+    pr = make_torus_problem(rho=rho, panels=panels, Nt=nt, kernel=2)
+    mob, sl = _mobility_ops(pr, dict(order=14, beta=0.6))
+    rig, sig, it, rr = mob.op.mobility_solve(sl.op, [[0, 0, -1.0, 0, 0, 0]], tol=1e-14)
+    mob.close(); sl.close()
+    U = -rig[0, 2]
+    ex = golden()[rho]
+    assert np.abs(rig[0, [0, 1, 3, 4, 5]]).max() < 1e-10 * abs(U)      # pure translation along the axis
+    assert abs(U - ex) / ex < TOL[rho], (U, ex, it, rr)
+
+
+def test_mobility_solve_two_bodies_matches_assembled():
+    """two close rings, random forces and torques: the library's solve equals the same solve
+    assembled step by step outside it (6x6 completion systems, K_1 - K_0 for S, GMRES, and V read
+    with the oracle's Gram-Schmidt projector)"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import oracle as O
+    from harness import DeviceProblem
+    from synth import make_config
+    quad = dict(order=12, beta=0.6)
+    pr = make_config("c3", panels=10)                  # two tori, gap r/20, per-body eta
+    rng = np.random.default_rng(3)
+    ft = rng.standard_normal((2, 6))
+    body = np.repeat(pr.body_of_panel, np.diff(pr.node_off()))
+    cent = np.array([np.average(pr.y_c[body == b], axis=0, weights=pr.w_c[body == b]) for b in range(2)])
+    mob, sl = _mobility_ops(pr, quad)
+    rig, sig, it, rr = mob.op.mobility_solve(sl.op, ft, tol=1e-13)
+    mob.close(); sl.close()
+    # assembled
+    nu = np.zeros((pr.N, 3))
+    for b in range(2):
+        m = body == b
+        nu[m] = completion_density(pr.y_c[m], pr.w_c[m], cent[b], ft[b, :3], ft[b, 3:])
+    nu_d = torch.from_numpy(nu).cuda()
+    import copy
+    Knu = []
+    for e in (1.0, 0.0):
+        p = copy.copy(pr)
+        p.eta_f = np.full_like(pr.eta_f, e)
+        p.eta_body = np.full_like(pr.eta_body, e)
+        dp = DeviceProblem(p, quad=quad)
+        Knu.append(dp.matvec(nu_d).clone())
+        dp.close()
+    p = copy.copy(pr)
+    p.projector = True
+    dp = DeviceProblem(p, quad=quad)
+    x, it2, rr2 = dp.op.gmres((Knu[1] - Knu[0]).contiguous(), restart=100, max_iters=1000, tol=1e-13)
+    dp.close()
+    V = -O.projector(pr.y_c, pr.w_c, body.astype(np.int32), 2, x.cpu().numpy())
+    for b in range(2):
+        m = np.nonzero(body == b)[0]
+        d = pr.y_c[m] - cent[b]
+        Vb = rig[b, :3] + np.cross(rig[b, 3:], d)                 # library's rigid motion at the nodes
+        np.testing.assert_allclose(Vb, V[m], rtol=0, atol=1e-9 * np.abs(V).max())

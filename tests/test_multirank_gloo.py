@@ -39,15 +39,21 @@ def _worker(rank, world, port, name, kw, q):
         orc = O.Oracle(pr)
         # sigma' on local panels (projector is per body; bodies are whole on a rank)
         sp_full, _, Ls_full = orc.prepare(pr.sigma)
-        sp_loc = sp_full[pb * pr.Nn:pe * pr.Nn]
-        sf_loc = O.upsample(sp_loc.reshape(-1), pe - pb, pr.Ns, pr.Nt, pr.Ms, pr.Mt, d).reshape(-1, d)
+        no, fo = pr.node_off(), pr.fine_off()          # panel -> node offsets (ragged-safe)
+        sp_loc = sp_full[no[pb]:no[pe]]
+        if pr.ragged:
+            sf_loc = O.upsample_ragged(sp_loc.reshape(-1), pr.Ns, pr.nt_of_panel()[pb:pe], pr.Ms,
+                                       pr.mt_of_panel()[pb:pe], d).reshape(-1, d)
+        else:
+            sf_loc = O.upsample(sp_loc.reshape(-1), pe - pb, pr.Ns, pr.Nt, pr.Ms, pr.Mt, d).reshape(-1, d)
+        assert sf_loc.shape[0] == fo[pe] - fo[pb]
         # all-gather (variable counts: pad to the max shard, as a grouped broadcast would place them)
-        maxp = max(e - b for b, e in ranges)
-        buf = torch.zeros(maxp * pr.Mn * d, dtype=torch.float64)
+        maxn = max(int(fo[e] - fo[b]) for b, e in ranges)
+        buf = torch.zeros(maxn * d, dtype=torch.float64)
         buf[:sf_loc.size] = torch.from_numpy(sf_loc.reshape(-1))
         parts = [torch.zeros_like(buf) for _ in range(world)]
         dist.all_gather(parts, buf)
-        sf = np.concatenate([p.numpy()[:(e - b) * pr.Mn * d] for p, (b, e) in zip(parts, ranges)]).reshape(-1, d)
+        sf = np.concatenate([p.numpy()[:int(fo[e] - fo[b]) * d] for p, (b, e) in zip(parts, ranges)]).reshape(-1, d)
         # this rank's rows with the gathered fine density
         u_loc = orc.apply_rows(pr.sigma, rows, prepared=(sp_full, sf, Ls_full))
         out = [None] * world
@@ -58,7 +64,8 @@ def _worker(rank, world, port, name, kw, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,kw", [("c1", {}), ("c4", dict(n_loops=3, panels=6)), ("c2", dict(panels=9))])
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c4", dict(n_loops=3, panels=6)), ("c2", dict(panels=9)),
+                                     ("c3v", dict(panels=6))])
 def test_two_rank_partition_matches_single(name, kw):
     import oracle as O
     from synth import make_config
