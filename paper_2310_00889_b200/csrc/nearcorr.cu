@@ -167,7 +167,8 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
                           const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
                           int64_t n_on, double c_id, const double* __restrict__ sig_local,
                           const double* __restrict__ Lsig, double* __restrict__ u, int G,
-                          const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff, int sdim) {
+                          const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff, int sdim, int ucols2) {
+    // uniform panels (cn0 = boff = NULL): every block is TD x ucols2 double2
     extern __shared__ __align__(128) double2 ring[];      // [warps][STG][S]
     __shared__ __align__(8) uint64_t bars[kNearWarps * kNearStages];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -188,10 +189,11 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
     int64_t pp = pa, qq = 0;
     auto produce = [&](int st) {
         if (pp >= pb) return;
-        const int64_t len2 = (boff[pp + 1] - boff[pp]) / 2;
+        const int64_t len2 = boff ? (boff[pp + 1] - boff[pp]) / 2 : (int64_t)TD * ucols2;
+        const int64_t b0 = boff ? boff[pp] / 2 : pp * (int64_t)TD * ucols2;
         const int64_t n2 = (len2 - qq) < S ? (len2 - qq) : S;
         mbar_expect_tx(&mybar[st], (uint32_t)(n2 * 16));
-        bulk_g2s(myring + (size_t)st * S, B + boff[pp] / 2 + qq, (uint32_t)(n2 * 16), &mybar[st]);
+        bulk_g2s(myring + (size_t)st * S, B + b0 + qq, (uint32_t)(n2 * 16), &mybar[st]);
         qq += n2;
         if (qq >= len2) { ++pp; qq = 0; }
     };
@@ -206,8 +208,8 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
         const int64_t p1 = row_ptr[t + 1];
         for (int64_t p = row_ptr[t]; p < p1; ++p) {
             const int64_t k = panel_idx[p];
-            const int ck = (int)((cn0[k + 1] - cn0[k]) * sdim / 2);
-            const double2* Sk = S2 + cn0[k] * sdim / 2;
+            const int ck = cn0 ? (int)((cn0[k + 1] - cn0[k]) * sdim / 2) : ucols2;
+            const double2* Sk = cn0 ? S2 + cn0[k] * sdim / 2 : S2 + k * (int64_t)ucols2;
             const int len2 = TD * ck;
             for (int q0 = 0; q0 < len2; q0 += S, ++i) {
                 const int st = (int)(i % kNearStages);
@@ -258,15 +260,18 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
     }
 }
 
+// Chunked streaming for ragged blocks, and for uniform blocks too wide for two CTAs of the plain
+// ring per SM (c3: 17 KB blocks): slots of S <= kChunk2 double2 keep two 4-warp CTAs per SM.
+constexpr int kChunk2 = 576;   // double2 per slot: 4 warps x 3 stages x 9.2 KB = 110 KB per CTA
+
 static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_t* row_ptr, const int32_t* panel_idx,
                                      const double* blocks, const double* sigma_c, const double* partials,
                                      int64_t n_chunks, int64_t n_on, double c_id, const double* sig_local,
-                                     const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
+                                     const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag,
+                                     int ucols = 0) {
     if (T <= 0) return SLB_OK;
-    // slot: the widest block if 4 warps x 3 stages of it fit in ~150 KB, else a chunk of that size
-    const int widest2 = tdim * rag.max_cols / 2;
-    const int Smax = (int)(150 * 1024 / (kNearWarps * kNearStages * 16));
-    const int S = std::min(widest2, Smax);
+    const int widest2 = tdim * (rag.boff ? rag.max_cols : ucols) / 2;
+    const int S = std::min(widest2, kChunk2);
     const size_t smem = (size_t)kNearWarps * kNearStages * S * 16;
     G = std::max(1, G);
     const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
@@ -276,7 +281,7 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
         near_stream_ragged_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(                              \
             T, S, row_ptr, panel_idx, blocks, sigma_c, partials, n_chunks, n_on, c_id, sig_local, Lsig, u, G,  \
-            rag.cn0, rag.boff, tdim);                                                                         \
+            rag.cn0, rag.boff, tdim, ucols / 2);                                                              \
     } while (0)
     if (tdim == 1) {
         if (mode == 0) RAG_LAUNCH(1, 0); else RAG_LAUNCH(1, 1);
@@ -298,9 +303,9 @@ slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, c
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
                            const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
                            const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
-    if (rag.boff)
+    if (rag.boff || tdim * cols / 2 > kChunk2 + kChunk2 / 8)
         return near_ragged_launch(1, T, tdim, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
-                                  n_on, c_id, sig_local, Lsig, u, G, s, rag);
+                                  n_on, c_id, sig_local, Lsig, u, G, s, rag, cols);
     return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
                               n_on, c_id, sig_local, Lsig, u, G, s);
 }
