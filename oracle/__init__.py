@@ -41,7 +41,8 @@ class OrProblem(ctypes.Structure):
                 ("panel_idx", ctypes.c_void_p), ("blk_seed", ctypes.c_uint64),
                 ("s_blk", ctypes.c_double), ("blocks", ctypes.c_void_p), ("n_bodies", ctypes.c_int),
                 ("body_of_node", ctypes.c_void_p), ("y_c", ctypes.c_void_p), ("w_c", ctypes.c_void_p),
-                ("panel_nt", ctypes.c_void_p), ("panel_mt", ctypes.c_void_p)]
+                ("panel_nt", ctypes.c_void_p), ("panel_mt", ctypes.c_void_p),
+                ("panel_ns", ctypes.c_void_p), ("panel_ms", ctypes.c_void_p)]
 
 
 def lib():
@@ -54,7 +55,7 @@ def lib():
         L.or_lagrange_matrix.argtypes = [ctypes.c_int, P, ctypes.c_int, P, P]
         L.or_trig_matrix.argtypes = [ctypes.c_int, ctypes.c_int, P]
         L.or_upsample.argtypes = [ctypes.c_long] + [ctypes.c_int] * 5 + [P, P]
-        L.or_upsample_ragged.argtypes = [ctypes.c_long, ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int, P, P]
+        L.or_upsample_ragged.argtypes = [ctypes.c_long, P, P, P, P, ctypes.c_int, P, P]
         L.or_kernel_matrix.argtypes = [ctypes.c_int, P, P, ctypes.c_double, P]
         L.or_farfield.argtypes = [ctypes.c_int, ctypes.c_long, P, ctypes.c_long, P, P, P, P, P, P]
         L.or_splitmix64.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
@@ -119,13 +120,16 @@ def upsample(sigma_c, n_panels, ns, nt, ms, mt, nc):
     return out.reshape(n_panels * ms * mt, nc) if nc > 1 else out
 
 
-def upsample_ragged(sigma_c, ns, nt_panels, ms, mt_panels, nc):
-    """per-panel angular orders (NEXT N4): panel k is ns x nt[k] -> ms x mt[k]"""
+def upsample_ragged(sigma_c, ns_panels, nt_panels, ms_panels, mt_panels, nc):
+    """per-panel orders (NEXT N4): panel k is ns[k] x nt[k] -> ms[k] x mt[k] (ints broadcast)"""
     nt = _c(nt_panels, np.int32)
-    mt = _c(mt_panels, np.int32)
+    P = nt.size
+    ns = _c(np.broadcast_to(np.asarray(ns_panels), (P,)), np.int32)
+    ms = _c(np.broadcast_to(np.asarray(ms_panels), (P,)), np.int32)
+    mt = _c(np.broadcast_to(np.asarray(mt_panels), (P,)), np.int32)
     sigma_c = _c(sigma_c)
-    out = np.empty(int((ms * mt.astype(np.int64)).sum()) * nc)
-    lib().or_upsample_ragged(nt.size, ns, _p(nt), ms, _p(mt), nc, _p(sigma_c), _p(out))
+    out = np.empty(int((ms.astype(np.int64) * mt).sum()) * nc)
+    lib().or_upsample_ragged(P, _p(ns), _p(nt), _p(ms), _p(mt), nc, _p(sigma_c), _p(out))
     return out
 
 
@@ -192,7 +196,9 @@ class Oracle:
                           body=_c(np.repeat(pr.body_of_panel, np.diff(pr.node_off())), np.int32),
                           y_c=_c(pr.y_c), w_c=_c(pr.w_c),
                           pnt=_c(pr.nt_of_panel(), np.int32) if pr.ragged else None,
-                          pmt=_c(pr.mt_of_panel(), np.int32) if pr.ragged else None)
+                          pmt=_c(pr.mt_of_panel(), np.int32) if pr.ragged else None,
+                          pns=_c(pr.ns_of_panel(), np.int32) if pr.ragged else None,
+                          pms=_c(pr.ms_of_panel(), np.int32) if pr.ragged else None)
         k = self._keep
         self.s = OrProblem(kind=pr.kernel, ns=pr.Ns, nt=pr.Nt, ms=pr.Ms, mt=pr.Mt,
                            n_panels=pr.P, n_trg=pr.T, n_on=pr.n_on, c_identity=pr.c_identity,
@@ -201,7 +207,8 @@ class Oracle:
                            panel_idx=_p(k["panel_idx"]), blk_seed=pr.blk_seed, s_blk=pr.s_blk,
                            blocks=_p(k["blocks"]), n_bodies=pr.n_bodies if pr.projector else 0,
                            body_of_node=_p(k["body"]), y_c=_p(k["y_c"]), w_c=_p(k["w_c"]),
-                           panel_nt=_p(k["pnt"]), panel_mt=_p(k["pmt"]))
+                           panel_nt=_p(k["pnt"]), panel_mt=_p(k["pmt"]),
+                           panel_ns=_p(k["pns"]), panel_ms=_p(k["pms"]))
 
     def prepare(self, sigma):
         pr = self.pr

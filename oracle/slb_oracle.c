@@ -161,21 +161,21 @@ void or_upsample(long n_panels, int ns, int nt, int ms, int mt, int nc,
     free(sg); free(wg); free(sf); free(wf); free(Ps); free(F);
 }
 
-/* Ragged grids (NEXT N4; §3.1: element k has N_s x N_th^(k) nodes):
- * panel k's coarse block starts at node sum_{k'<k} ns nt[k'], its fine block at
- * sum_{k'<k} ms mt[k']; each panel is interpolated with its own (nt[k], mt[k]) matrices. */
-void or_upsample_ragged(long n_panels, int ns, const int* nt, int ms, const int* mt, int nc,
+/* Ragged grids (NEXT N4; §3.1: element k has N_s^(k) x N_th^(k) nodes):
+ * panel k's coarse block starts at node sum_{k'<k} ns[k'] nt[k'], its fine block at
+ * sum_{k'<k} ms[k'] mt[k']; each panel is interpolated with its own (ns, nt, ms, mt) matrices. */
+void or_upsample_ragged(long n_panels, const int* ns, const int* nt, const int* ms, const int* mt, int nc,
                         const double* sigma_c, double* sigma_f) {
     long* c0 = malloc(sizeof(long) * (n_panels + 1));
     long* f0 = malloc(sizeof(long) * (n_panels + 1));
     c0[0] = f0[0] = 0;
     for (long p = 0; p < n_panels; ++p) {
-        c0[p + 1] = c0[p] + (long)ns * nt[p];
-        f0[p + 1] = f0[p] + (long)ms * mt[p];
+        c0[p + 1] = c0[p] + (long)ns[p] * nt[p];
+        f0[p + 1] = f0[p] + (long)ms[p] * mt[p];
     }
     #pragma omp parallel for schedule(dynamic, 1)
     for (long p = 0; p < n_panels; ++p)
-        or_upsample(1, ns, nt[p], ms, mt[p], nc, sigma_c + c0[p] * nc, sigma_f + f0[p] * nc);
+        or_upsample(1, ns[p], nt[p], ms[p], mt[p], nc, sigma_c + c0[p] * nc, sigma_f + f0[p] * nc);
     free(c0); free(f0);
 }
 
@@ -367,9 +367,11 @@ typedef struct {
     const int* body_of_node;   /* [N] */
     const double* y_c;         /* [N][3] */
     const double* w_c;         /* [N] */
-    /* ragged angular orders per panel (NEXT N4), or NULL: every panel has (nt, mt) */
+    /* ragged orders per panel (NEXT N4), or NULL: every panel has (ns, nt, ms, mt) */
     const int* panel_nt;       /* [n_panels] */
     const int* panel_mt;       /* [n_panels] */
+    const int* panel_ns;       /* [n_panels] */
+    const int* panel_ms;       /* [n_panels] */
 } or_problem;
 
 /* node offsets of panel k (coarse c0, fine f0), k = 0..n_panels */
@@ -378,8 +380,10 @@ static void or_offsets(const or_problem* pb, long* c0, long* f0) {
     for (long k = 0; k < pb->n_panels; ++k) {
         int nt = pb->panel_nt ? pb->panel_nt[k] : pb->nt;
         int mt = pb->panel_mt ? pb->panel_mt[k] : pb->mt;
-        c0[k + 1] = c0[k] + (long)pb->ns * nt;
-        f0[k + 1] = f0[k] + (long)pb->ms * mt;
+        int ns = pb->panel_ns ? pb->panel_ns[k] : pb->ns;
+        int ms = pb->panel_ms ? pb->panel_ms[k] : pb->ms;
+        c0[k + 1] = c0[k] + (long)ns * nt;
+        f0[k + 1] = f0[k] + (long)ms * mt;
     }
 }
 
@@ -397,9 +401,18 @@ void or_prepare(const or_problem* pb, const double* sigma, double* sigma_p,
     } else {
         for (long q = 0; q < N * d; ++q) { sigma_p[q] = sigma[q]; if (Lsigma) Lsigma[q] = 0.0; }
     }
-    if (pb->panel_nt)
-        or_upsample_ragged(pb->n_panels, pb->ns, pb->panel_nt, pb->ms, pb->panel_mt, d, sigma_p, sigma_f);
-    else
+    if (pb->panel_nt || pb->panel_ns) {
+        int* a[4];
+        for (int q = 0; q < 4; ++q) a[q] = malloc(sizeof(int) * pb->n_panels);
+        for (long k = 0; k < pb->n_panels; ++k) {
+            a[0][k] = pb->panel_ns ? pb->panel_ns[k] : pb->ns;
+            a[1][k] = pb->panel_nt ? pb->panel_nt[k] : pb->nt;
+            a[2][k] = pb->panel_ms ? pb->panel_ms[k] : pb->ms;
+            a[3][k] = pb->panel_mt ? pb->panel_mt[k] : pb->mt;
+        }
+        or_upsample_ragged(pb->n_panels, a[0], a[1], a[2], a[3], d, sigma_p, sigma_f);
+        for (int q = 0; q < 4; ++q) free(a[q]);
+    } else
         or_upsample(pb->n_panels, pb->ns, pb->nt, pb->ms, pb->mt, d, sigma_p, sigma_f);
     free(c0); free(f0);
 }

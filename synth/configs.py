@@ -65,31 +65,40 @@ class Problem:
     panel_len: Optional[np.ndarray] = None
     body_center: Optional[np.ndarray] = None
     extra: dict = field(default_factory=dict)
-    # ragged angular orders (NEXT N4, P:L770-781): N_th^(k) per panel, fine M_th^(k) = q_th N_th^(k)
-    # with q_th = Mt // Nt (Nt, Mt then hold the base pair).  None: every panel has Nt.
+    # ragged orders (NEXT N4, P:L770-781): N_th^(k) and/or N_s^(k) per panel; fine orders
+    # M_th^(k) = q_th N_th^(k), M_s^(k) = q_s N_s^(k) with q_th = Mt // Nt, q_s = Ms // Ns (Ns, Nt, Ms, Mt
+    # then hold the base orders).  None: every panel has the base order.
     panel_nt: Optional[np.ndarray] = None
+    panel_ns: Optional[np.ndarray] = None
 
     @property
     def ragged(self):
-        return self.panel_nt is not None
+        return self.panel_nt is not None or self.panel_ns is not None
 
     def nt_of_panel(self):
-        return self.panel_nt.astype(np.int64) if self.ragged else np.full(self.P, self.Nt, np.int64)
+        return self.panel_nt.astype(np.int64) if self.panel_nt is not None else np.full(self.P, self.Nt, np.int64)
 
     def mt_of_panel(self):
         return self.nt_of_panel() * (self.Mt // self.Nt) if self.ragged else np.full(self.P, self.Mt, np.int64)
 
+    def ns_of_panel(self):
+        return self.panel_ns.astype(np.int64) if self.panel_ns is not None else np.full(self.P, self.Ns, np.int64)
+
+    def ms_of_panel(self):
+        return self.ns_of_panel() * (self.Ms // self.Ns) if self.ragged else np.full(self.P, self.Ms, np.int64)
+
     def node_off(self):
         """[P+1] first coarse node of each panel"""
-        return np.concatenate([[0], np.cumsum(self.Ns * self.nt_of_panel())]).astype(np.int64)
+        return np.concatenate([[0], np.cumsum(self.ns_of_panel() * self.nt_of_panel())]).astype(np.int64)
 
     def fine_off(self):
         """[P+1] first fine node of each panel"""
-        return np.concatenate([[0], np.cumsum(self.Ms * self.mt_of_panel())]).astype(np.int64)
+        return np.concatenate([[0], np.cumsum(self.ms_of_panel() * self.mt_of_panel())]).astype(np.int64)
 
     def blk_off(self):
         """[nnz+1] first entry of each near block [t_dim][N_n^(k) s_dim] in the flat block array"""
-        bl = self.tdim * self.sdim * self.Ns * self.nt_of_panel()[self.panel_idx]
+        nn = self.ns_of_panel() * self.nt_of_panel()
+        bl = self.tdim * self.sdim * nn[self.panel_idx]
         return np.concatenate([[0], np.cumsum(bl)]).astype(np.int64)
 
     def n_blocks_entries(self):
@@ -143,25 +152,31 @@ class Problem:
 
 
 def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 2),
-              extra_targets=None, c1_rule=False, projector=False, rng=None, nt_panels=None):
-    """nt_panels: optional list (per body) of per-panel angular orders (ragged, NEXT N4); Nt is
-    then the base order and q[1] the fine factor of every panel."""
+              extra_targets=None, c1_rule=False, projector=False, rng=None, nt_panels=None, ns_panels=None):
+    """nt_panels / ns_panels: optional lists (per body) of per-panel angular / GL orders (ragged,
+    NEXT N4); Nt, Ns are then the base orders and q the fine factors of every panel."""
     Ms, Mt = q[0] * Ns, q[1] * Nt
-    if nt_panels is None:
+    ragged = nt_panels is not None or ns_panels is not None
+    if ragged:
+        nt_panels = nt_panels if nt_panels is not None else [np.full(P, Nt) for P in P_per_body]
+        ns_panels = ns_panels if ns_panels is not None else [np.full(P, Ns) for P in P_per_body]
+        coarse = [discretize_ragged(b, P, np.asarray(ns), nt) for b, P, ns, nt in zip(bodies, P_per_body, ns_panels, nt_panels)]
+        fine = [discretize_ragged(b, P, q[0] * np.asarray(ns), q[1] * np.asarray(nt))
+                for b, P, ns, nt in zip(bodies, P_per_body, ns_panels, nt_panels)]
+    else:
         coarse = [discretize(b, P, Ns, Nt) for b, P in zip(bodies, P_per_body)]
         fine = [discretize(b, P, Ms, Mt) for b, P in zip(bodies, P_per_body)]
-    else:
-        coarse = [discretize_ragged(b, P, Ns, nt) for b, P, nt in zip(bodies, P_per_body, nt_panels)]
-        fine = [discretize_ragged(b, P, Ms, q[1] * np.asarray(nt)) for b, P, nt in zip(bodies, P_per_body, nt_panels)]
     cat = lambda L, a: np.ascontiguousarray(np.concatenate([getattr(g, a) for g in L], axis=0))
     y_c, n_c, w_c = cat(coarse, "y"), cat(coarse, "n"), cat(coarse, "w")
     y_f, n_f, w_f = cat(fine, "y"), cat(fine, "n"), cat(fine, "w")
     body_of_panel = np.concatenate([np.full(P, b, np.int32) for b, P in enumerate(P_per_body)])
     Ptot = int(body_of_panel.shape[0])
-    panel_nt = None if nt_panels is None else np.concatenate([np.asarray(v, np.int32) for v in nt_panels])
+    panel_nt = None if not ragged else np.concatenate([np.asarray(v, np.int32) for v in nt_panels])
+    panel_ns = None if not ragged else np.concatenate([np.asarray(v, np.int32) for v in ns_panels])
     nt_k = np.full(Ptot, Nt, np.int64) if panel_nt is None else panel_nt.astype(np.int64)
-    node_off = np.concatenate([[0], np.cumsum(Ns * nt_k)])
-    fine_per_panel = Ms * q[1] * nt_k
+    ns_k = np.full(Ptot, Ns, np.int64) if panel_ns is None else panel_ns.astype(np.int64)
+    node_off = np.concatenate([[0], np.cumsum(ns_k * nt_k)])
+    fine_per_panel = q[0] * ns_k * q[1] * nt_k
     if kernel == STOKES_SLDL:
         eta_body = np.array([eta_cfie_input(b.rho_min) for b in bodies])
     else:
@@ -174,29 +189,32 @@ def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 
     sdim = 1 if kernel == LAPLACE_DL else 3
     sigma = rng.standard_normal((y_c.shape[0], sdim))
     L = np.concatenate([panel_arclength(b, P) for b, P in zip(bodies, P_per_body)])
-    # first node of every GL ring: its centerline point and radius (ragged-safe)
-    ring_first = (node_off[:-1, None] + np.arange(Ns)[None, :] * nt_k[:, None]).reshape(-1)
-    ring_xc = cat(coarse, "xc")[ring_first].reshape(Ptot, Ns, 3)
+    # first node of every GL ring: its centerline point and radius (ragged-safe: panels with fewer
+    # rings repeat their first ring, which leaves the min over rings unchanged)
+    nsmax = int(ns_k.max())
+    ii = np.arange(nsmax)[None, :]
+    ring_first = (node_off[:-1, None] + np.where(ii < ns_k[:, None], ii, 0) * nt_k[:, None]).reshape(-1)
+    ring_xc = cat(coarse, "xc")[ring_first].reshape(Ptot, nsmax, 3)
     s_all = np.concatenate([g.s for g in coarse])
-    S_ring = s_all[ring_first].reshape(Ptot, Ns)
-    rho_ring = np.empty((Ptot, Ns))
+    S_ring = s_all[ring_first].reshape(Ptot, nsmax)
+    rho_ring = np.empty((Ptot, nsmax))
     for bi, b in enumerate(bodies):
         m = body_of_panel == bi
-        rho_ring[m] = np.broadcast_to(b.rho(S_ring[m]), (int(m.sum()), Ns))
+        rho_ring[m] = np.broadcast_to(b.rho(S_ring[m]), (int(m.sum()), nsmax))
     own = np.full(x_trg.shape[0], -1, np.int64)
-    own[:n_on] = np.repeat(np.arange(Ptot), Ns * nt_k)
+    own[:n_on] = np.repeat(np.arange(Ptot), ns_k * nt_k)
     forced = None
     if c1_rule:
         # config 1 node targets: panels {k-1, k, k+1} mod P of their own body (R15)
         P0 = P_per_body[0]
         k = np.repeat(np.arange(P0), Ns * Nt)
         forced = np.stack([(k - 1) % P0, k, (k + 1) % P0], axis=1)
-    if panel_nt is None:
+    if not ragged:
         y_panels = y_c.reshape(Ptot, Ns * Nt, 3)
     else:   # pad every panel to the largest node count with copies of its first node (min unchanged)
-        nmax = int((Ns * nt_k).max())
+        nmax = int((ns_k * nt_k).max())
         j = np.arange(nmax)[None, :]
-        idx = node_off[:-1, None] + np.where(j < Ns * nt_k[:, None], j, 0)
+        idx = node_off[:-1, None] + np.where(j < (ns_k * nt_k)[:, None], j, 0)
         y_panels = y_c[idx]
     row_ptr, panel_idx = build_near_csr(x_trg, y_panels, ring_xc, rho_ring, L, own, forced_rows=forced)
     # coincident-pair guard (R14): no target may sit on a fine source
@@ -210,7 +228,8 @@ def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 
                    w_f=w_f, eta_f=eta_f, eta_body=eta_body, x_trg=x_trg, n_on=n_on,
                    c_identity=0.5, sigma=sigma, row_ptr=row_ptr, panel_idx=panel_idx,
                    blk_seed=blk_seed, s_blk=s_blk, projector=projector, panel_len=L,
-                   body_center=centers, panel_nt=panel_nt)
+                   body_center=centers, panel_nt=panel_nt,
+                   panel_ns=panel_ns if (panel_ns is not None and np.any(panel_ns != Ns)) else None)
 
 
 def _assert_separated(x, y, tol=1e-9):
@@ -253,14 +272,15 @@ CONFIGS = ("c1", "c2", "c3", "c3v", "c4", "c5", "c5alt")
 
 
 def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_DL, eta=None, extra_targets=None,
-                       seed_offset=0, nt_panels=None):
+                       seed_offset=0, nt_panels=None, ns_panels=None):
     """Single torus (axis z, centre 0) with the 2 L_k near rule -- pin problems for the special
     quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes; eta=0 -> pure DL."""
     seed = BASE_SEED + 100 + seed_offset
     rng = np.random.default_rng(seed)
     b = torus_body(R, rho)
     pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng,
-                   nt_panels=None if nt_panels is None else [np.asarray(nt_panels)])
+                   nt_panels=None if nt_panels is None else [np.asarray(nt_panels)],
+                   ns_panels=None if ns_panels is None else [np.asarray(ns_panels)])
     if kernel == STOKES_SLDL and eta is not None:
         pr.eta_body[:] = eta
         pr.eta_f[:] = eta
@@ -290,22 +310,24 @@ def make_config(name: str, **kw) -> Problem:
         b1 = torus_body(1.0, rho, (2.0 + 2 * rho + gap, 0.0, 0.0))
         return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 20, rng=rng)
     if name == "c3v":
-        # c3 with per-panel angular orders (NEXT N4; the paper's close-touching mesh is adaptive in
-        # N_th up to 88): N_th by the distance from the panel's centerline midpoint to the
-        # other ring's centerline -- 64 within 0.15, 40 within 0.4, 24 within 0.8, else 12 (base 12, q = 2)
+        # c3 with per-panel orders (NEXT N4; the paper's close-touching mesh is adaptive in N_th up
+        # to 88): N_th by the distance from the panel's centerline midpoint to the other
+        # ring's centerline -- 64 within 0.15, 40 within 0.4, 24 within 0.8, else 12; N_s = 16 within
+        # 0.4, else 12 (base 12 x 12, q = 2)
         P = kw.get("panels", 64)
         rho, gap = 0.05, 0.0025
         c1x = 2.0 + 2 * rho + gap
         b0 = torus_body(1.0, rho, (0.0, 0.0, 0.0))
         b1 = torus_body(1.0, rho, (c1x, 0.0, 0.0))
         mid = (np.arange(P) + 0.5) / P
-        nts = []
+        nts, nss = [], []
         for b, other in ((b0, b1), (b1, b0)):
             xm = b.xc(mid)
             so = np.arange(720) / 720
             d = np.min(np.linalg.norm(xm[:, None, :] - other.xc(so)[None, :, :], axis=-1), axis=1)
             nts.append(np.select([d < 0.15, d < 0.4, d < 0.8], [64, 40, 24], 12).astype(np.int32))
-        return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 12, rng=rng, nt_panels=nts)
+            nss.append(np.where(d < 0.4, 16, 12).astype(np.int32))      # N_s^(k): 16 at the gap
+        return _assemble(name, STOKES_SLDL, seed, [b0, b1], [P, P], 12, 12, rng=rng, nt_panels=nts, ns_panels=nss)
     if name == "c4":
         n = kw.get("n_loops", 64)
         P = kw.get("panels", 32)

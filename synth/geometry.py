@@ -161,27 +161,27 @@ def discretize(body: Body, P: int, Ns: int, Nt: int) -> Grid:
                 J=J, s=S.copy(), th=TH.copy(), xc=xc, P=P, Ns=Ns, Nt=Nt)
 
 
-def discretize_ragged(body: Body, P: int, Ns: int, nt_panels) -> Grid:
-    """Per-panel angular order N_th^(k) (§3.1: element k has N_s^(k) x
-    N_th^(k) nodes).  Layout [panel][i][j], panel k contributing Ns * nt_panels[k] nodes; the
-    node recipe per panel is discretize()'s.  Grid.Nt is 0 (ragged)."""
+def discretize_ragged(body: Body, P: int, Ns, nt_panels) -> Grid:
+    """Per-panel orders (§3.1: element k has N_s^(k) x N_th^(k) nodes).
+    Ns: int or [P] array; nt_panels: [P].  Layout [panel][i][j], panel k contributing
+    N_s^(k) N_th^(k) nodes; the node recipe per panel is discretize()'s.  Grid.Ns/Nt are 0 (ragged)."""
     nt_panels = np.asarray(nt_panels, dtype=np.int64)
+    ns_panels = np.broadcast_to(np.asarray(Ns, dtype=np.int64), (P,))
     assert nt_panels.shape == (P,) and np.all(nt_panels % 2 == 0) and np.all(nt_panels >= 2)
-    parts = []
-    for nt in np.unique(nt_panels):
-        g = discretize(body, P, Ns, int(nt))
-        parts.append((int(nt), g))
-    by_nt = dict(parts)
+    assert np.all(ns_panels >= 1)
+    cache = {}
     fields = ("y", "n", "w", "J", "s", "th", "xc")
     out = {f: [] for f in fields}
     for k in range(P):
-        nt = int(nt_panels[k])
-        g = by_nt[nt]
-        a, b = k * Ns * nt, (k + 1) * Ns * nt
+        ns, nt = int(ns_panels[k]), int(nt_panels[k])
+        if (ns, nt) not in cache:
+            cache[(ns, nt)] = discretize(body, P, ns, nt)
+        g = cache[(ns, nt)]
+        a, b = k * ns * nt, (k + 1) * ns * nt
         for f in fields:
             out[f].append(getattr(g, f)[a:b])
     cat = {f: np.ascontiguousarray(np.concatenate(out[f], axis=0)) for f in fields}
-    return Grid(P=P, Ns=Ns, Nt=0, **cat)
+    return Grid(P=P, Ns=0, Nt=0, **cat)
 
 
 def panel_arclength(body: Body, P: int) -> np.ndarray:

@@ -42,8 +42,8 @@ def _worker(rank, world, port, name, kw, q):
         no, fo = pr.node_off(), pr.fine_off()          # panel -> node offsets (ragged-safe)
         sp_loc = sp_full[no[pb]:no[pe]]
         if pr.ragged:
-            sf_loc = O.upsample_ragged(sp_loc.reshape(-1), pr.Ns, pr.nt_of_panel()[pb:pe], pr.Ms,
-                                       pr.mt_of_panel()[pb:pe], d).reshape(-1, d)
+            sf_loc = O.upsample_ragged(sp_loc.reshape(-1), pr.ns_of_panel()[pb:pe], pr.nt_of_panel()[pb:pe],
+                                       pr.ms_of_panel()[pb:pe], pr.mt_of_panel()[pb:pe], d).reshape(-1, d)
         else:
             sf_loc = O.upsample(sp_loc.reshape(-1), pe - pb, pr.Ns, pr.Nt, pr.Ms, pr.Mt, d).reshape(-1, d)
         assert sf_loc.shape[0] == fo[pe] - fo[pb]

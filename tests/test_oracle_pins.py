@@ -368,26 +368,27 @@ def test_eta_printed_values():
 # PAPER.md §3.1: element k carries its own N_th^(k).  The oracle's ragged bookkeeping
 # (per-panel interpolation, node / fine / block offsets) is pinned by exactness, by the physics of
 # a ragged refined torus, and by an independent dense assembly from the generator's offsets.
-def test_n4_ragged_upsample_exactness():
-    ns, ms = 10, 20
+@pytest.mark.parametrize("ragged_ns", [False, True])
+def test_n4_ragged_upsample_exactness(ragged_ns):
     nts = np.array([12, 4, 20, 8, 12, 16])
-    mts = 2 * nts
+    nss = np.array([10, 6, 12, 10, 16, 8]) if ragged_ns else np.full(6, 10)
+    mts, mss = 2 * nts, 2 * nss
     rng = np.random.default_rng(11)
-    coef = rng.standard_normal((nts.size, ns))
-    sc, _ = O.gauss_legendre(ns)
-    sf, _ = O.gauss_legendre(ms)
     cs, fs = [], []
-    for p, (nt, mt) in enumerate(zip(nts, mts)):
+    for p, (ns, nt, ms, mt) in enumerate(zip(nss, nts, mss, mts)):
+        coef = rng.standard_normal(ns)                 # degree ns-1 polynomial in t
         a = rng.standard_normal(nt // 2)
         b = rng.standard_normal(nt // 2)
         ny = rng.standard_normal()
-        f = lambda t, th: np.polynomial.polynomial.polyval(t, coef[p]) * (
+        sc, _ = O.gauss_legendre(int(ns))
+        sf, _ = O.gauss_legendre(int(ms))
+        f = lambda t, th: np.polynomial.polynomial.polyval(t, coef) * (
             sum(a[l] * np.cos(l * th) + b[l] * np.sin(l * th) for l in range(nt // 2)) + ny * np.cos(nt * th / 2))
         cs.append(f(sc[:, None], 2 * np.pi * np.arange(nt)[None, :] / nt).reshape(-1))
         fs.append(f(sf[:, None], 2 * np.pi * np.arange(mt)[None, :] / mt).reshape(-1))
     c, f = np.concatenate(cs), np.concatenate(fs)
     for nc in (1, 3):
-        out = O.upsample_ragged(np.repeat(c[:, None], nc, 1) * (1 + np.arange(nc)), ns, nts, ms, mts, nc)
+        out = O.upsample_ragged(np.repeat(c[:, None], nc, 1) * (1 + np.arange(nc)), nss, nts, mss, mts, nc)
         np.testing.assert_allclose(out.reshape(-1, nc), np.repeat(f[:, None], nc, 1) * (1 + np.arange(nc)),
                                    rtol=0, atol=1e-13 * np.abs(f).max())
 
@@ -426,7 +427,7 @@ def test_n4_ragged_operator_vs_dense_assembly():
     far over the non-near panels + B sigma."""
     from synth.rng import block_entries_array
     pr = make_config("c3v", panels=8)
-    assert pr.ragged and len(set(pr.panel_nt.tolist())) > 1
+    assert pr.ragged and len(set(pr.panel_nt.tolist())) > 1 and len(set(pr.panel_ns.tolist())) > 1
     no, fo, bo = pr.node_off(), pr.fine_off(), pr.blk_off()
     d = pr.sdim
     orc = O.Oracle(pr)
@@ -434,8 +435,9 @@ def test_n4_ragged_operator_vs_dense_assembly():
     sp, sf, _ = orc.prepare(pr.sigma)
     _, uf, un = orc.apply_rows(pr.sigma, rows, parts=True, prepared=(sp, sf, None))
     # fine density: per-panel uniform upsample with that panel's orders
-    sf_ref = np.concatenate([O.upsample(pr.sigma[no[k]:no[k + 1]].reshape(-1), 1, pr.Ns, int(pr.panel_nt[k]),
-                                        pr.Ms, 2 * int(pr.panel_nt[k]), d) for k in range(pr.P)]).reshape(-1, d)
+    nsk, ntk = pr.ns_of_panel(), pr.nt_of_panel()
+    sf_ref = np.concatenate([O.upsample(pr.sigma[no[k]:no[k + 1]].reshape(-1), 1, int(nsk[k]), int(ntk[k]),
+                                        2 * int(nsk[k]), 2 * int(ntk[k]), d) for k in range(pr.P)]).reshape(-1, d)
     np.testing.assert_array_equal(sf.reshape(-1, d), sf_ref)
     for q, t in enumerate(rows):
         bsig = np.zeros(d)
