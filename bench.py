@@ -285,7 +285,7 @@ def main():
             "config": config_info(pr, world, "inputs larger than L2 (fine sources "
                                   f"{pr.M * 80 / 1e6:.0f} MB, near blocks {pr.n_blocks_entries() * 8 / 1e9:.1f} GB)"),
             "pairs_per_s": pr.pairs() * value,
-            "roofline": {"bound": "alu", "kernel": "far_const_kernel (FP64 DFMA pipe; far_kernel below M = 2^19)", "achieved": far_tf,
+            "roofline": {"bound": "alu", "kernel": "far_const_kernel (FP64 DFMA pipe; far_kernel below M = 2^16)", "achieved": far_tf,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": far_tf / FP64_PEAK_TFLOPS,
                          "traffic": traffic,
                          "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1965 MHz (no FP64 entry in "

@@ -83,7 +83,8 @@ class DeviceProblem:
             pi_d = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
             slb_nearcorr_quad(3 if single_layer else pr.kernel, self.x_trg, rp_d, pi_d, pr.Ns, pr.Nt, f64(pr.y_c),
                               self.blocks, trg_node=trg_node, eta_panel=None if single_layer else eta_panel, order=quad.get("order", 12),
-                              beta=quad.get("beta", 0.6), panel_nt=pr.panel_nt if pr.ragged else None)
+                              beta=quad.get("beta", 0.6), panel_nt=pr.nt_of_panel() if pr.ragged else None,
+                              panel_ns=pr.ns_of_panel() if pr.ragged else None)
         self.y_f, self.n_f, self.w_f = f64(pr.y_f), f64(pr.n_f), f64(pr.w_f)
         # pure double layer (all eta = 0) runs the DL kernel: eta_fine must then be NULL
         self.eta_f = f64(pr.eta_f) if (pr.kernel == 2 and np.any(pr.eta_f != 0)) else None
@@ -107,7 +108,9 @@ class DeviceProblem:
                            eta_fine=self.eta_f, eta=0.0,
                            folded=not fold, n_bodies=nb, body_of_panel=bop, y_coarse=y_c, w_coarse=w_c,
                            comm=comm, panel_nt=pr.nt_of_panel() if pr.ragged else None,
-                           panel_mt=pr.mt_of_panel() if pr.ragged else None)
+                           panel_mt=pr.mt_of_panel() if pr.ragged else None,
+                           panel_ns=pr.ns_of_panel() if pr.ragged else None,
+                           panel_ms=pr.ms_of_panel() if pr.ragged else None)
 
     def matvec(self, sigma=None, out=None):
         return self.op.matvec(self.sigma if sigma is None else sigma, out)

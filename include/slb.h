@@ -81,11 +81,12 @@ void slb_coincident_reset(void);
 /* Number of kernels this library has launched since it was loaded (launch accounting). */
 unsigned long long slb_launch_count(void);
 
-/* (a, NEXT N4) Ragged upsample: panel p is ns x nt[p] -> ms x mt[p] (HOST arrays [n_panels]),
+/* (a, NEXT N4) Ragged upsample: panel p is ns[p] x nt[p] -> ms[p] x mt[p] (HOST arrays [n_panels]),
  * nodes of consecutive panels back to back in both arrays.  Otherwise as
  * slb_upsample.  Synchronises s (uploads the panel tables). */
-slb_status slb_upsample_ragged(int64_t n_panels, int ns, const int32_t* nt, int ms, const int32_t* mt, int ncomp,
-                               const double* sigma_coarse, double* sigma_fine, cudaStream_t s);
+slb_status slb_upsample_ragged(int64_t n_panels, const int32_t* ns, const int32_t* nt, const int32_t* ms,
+                               const int32_t* mt, int ncomp, const double* sigma_coarse, double* sigma_fine,
+                               cudaStream_t s);
 
 /* (a) Upsample a density from the coarse Nystrom grid to the fine smooth-quadrature grid,
  *   sigma_fine[p][a][b][c] = sum_i sum_j P_s[a][i] F_th[b][j] sigma_coarse[p][i][j][c],
@@ -150,13 +151,13 @@ slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_t
                              const double* y_coarse, const double* eta_panel, int order, double beta,
                              double* blocks, cudaStream_t s);
 
-/* (NEXT N1 + N4) Same for ragged angular orders: panel k has ns x panel_nt[k] nodes (HOST array
- * [n_panels], even, <= 64), y_coarse is the per-panel node blocks back to back,
- * block p = [tdim][ns*panel_nt[k]*sdim] packed back to back in CSR order.  Synchronises s. */
+/* (NEXT N1 + N4) Same for ragged orders: panel k has panel_ns[k] x panel_nt[k] nodes (HOST arrays
+ * [n_panels]; N_s <= 32, N_th even <= 64), y_coarse is the per-panel node blocks back to back
+ * (P:L770-781), block p = [tdim][N_n^(k) sdim] packed back to back in CSR order.  Synchronises s. */
 slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
-                                    const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels, int ns,
-                                    const int32_t* panel_nt, const double* y_coarse, const double* eta_panel,
-                                    int order, double beta, double* blocks, cudaStream_t s);
+                                    const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels,
+                                    const int32_t* panel_ns, const int32_t* panel_nt, const double* y_coarse,
+                                    const double* eta_panel, int order, double beta, double* blocks, cudaStream_t s);
 
 /* Synthetic special-quadrature blocks (input generation, R10):
  *   blocks[q] = ((2 u_q - 1) sqrt(3)) s_blk,  u_q = (splitmix64(seed, first + q) >> 11) 2^-53,
@@ -210,14 +211,17 @@ typedef struct {
     const int32_t* body_of_panel_local; /* [panel_end-panel_begin] local body id, nondecreasing */
     const double* y_coarse;             /* [local nodes][3] */
     const double* w_coarse;             /* [local nodes] */
-    /* (NEXT N4) ragged angular orders, §3.1 P:L770-781 ("element k ... Fourier order
-     * N_th^(k)"): HOST arrays [n_panels_global], or both NULL for uniform panels.  Panel k then has
-     * ns x panel_nt[k] coarse and ms x panel_mt[k] fine nodes (each even, within the compiled
-     * limits; nt and mt are ignored).  Every node array is the per-panel blocks back to back in
-     * panel order; near block p is [tdim][ns*panel_nt[k]*sdim] with k = panel_idx[p], the blocks
-     * packed back to back in CSR order.  Read during slb_operator_create only. */
+    /* (NEXT N4) ragged orders, §3.1 P:L770-781 ("element k ... polynomial order N_s^(k),
+     * Fourier order N_th^(k)"): HOST arrays [n_panels_global]; each pair (panel_nt, panel_mt) and
+     * (panel_ns, panel_ms) is given together or both NULL (then the scalar nt, mt / ns, ms apply).
+     * Panel k has panel_ns[k] x panel_nt[k] coarse and panel_ms[k] x panel_mt[k] fine nodes
+     * (N_th, M_th even; all within the compiled limits).  Every node array is the per-panel
+     * blocks back to back in panel order; near block p is [tdim][N_n^(k) sdim] with k =
+     * panel_idx[p], the blocks packed back to back in CSR order.  Read during create only. */
     const int32_t* panel_nt;
     const int32_t* panel_mt;
+    const int32_t* panel_ns;
+    const int32_t* panel_ms;
 } slb_operator_desc;
 
 /* Borrows every descriptor pointer (they must outlive the operator); owns only its scratch

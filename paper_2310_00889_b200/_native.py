@@ -24,7 +24,7 @@ class OperatorDesc(ctypes.Structure):
                 ("x_trg", P), ("y_fine", P), ("n_fine", P), ("w_fine", P), ("eta_fine", P),
                 ("eta", D), ("row_ptr", P), ("panel_idx", P), ("blocks", P), ("blocks_folded", I32),
                 ("n_bodies_local", I64), ("body_of_panel_local", P), ("y_coarse", P), ("w_coarse", P),
-                ("panel_nt", P), ("panel_mt", P)]
+                ("panel_nt", P), ("panel_mt", P), ("panel_ns", P), ("panel_ms", P)]
 
 
 _SIGS = {
@@ -35,14 +35,14 @@ _SIGS = {
     "slb_coincident_reset": (None, []),
     "slb_launch_count": (ctypes.c_ulonglong, []),
     "slb_upsample": (I32, [I64, I32, I32, I32, I32, I32, P, P, P]),
-    "slb_upsample_ragged": (I32, [I64, I32, P, I32, P, I32, P, P, P]),
+    "slb_upsample_ragged": (I32, [I64, P, P, P, P, I32, P, P, P]),
     "slb_farfield_laplace_dl": (I32, [I64, P, I64, P, P, P, P, P, P]),
     "slb_farfield_stokes_sldl": (I32, [I64, P, I64, P, P, P, P, D, P, P, P]),
     "slb_nearcorr_apply": (I32, [I64, I32, I32, I32, P, P, P, P, P, P]),
     "slb_nearcorr_fold": (I32, [I32, I64, P, P, P, I32, I32, I32, I32, P, P, P, P, D, P, P]),
     "slb_fill_blocks": (I32, [ctypes.c_uint64, ctypes.c_uint64, I64, D, P, P]),
     "slb_nearcorr_quad": (I32, [I32, I64, P, P, P, P, I32, I32, P, P, I32, D, P, P]),
-    "slb_nearcorr_quad_ragged": (I32, [I32, I64, P, P, P, P, I64, I32, P, P, P, I32, D, P, P]),
+    "slb_nearcorr_quad_ragged": (I32, [I32, I64, P, P, P, P, I64, P, P, P, P, I32, D, P, P]),
     "slb_near_build": (I32, [I64, P, I64, I32, P, P, P, P, P, I64, ctypes.POINTER(I64), P]),
     "slb_comm_unique_id": (I32, [P]),
     "slb_comm_create": (I32, [P, I32, I32, ctypes.POINTER(P)]),

@@ -69,17 +69,21 @@ def _host_i32(a, name):
     return arr
 
 
-def slb_upsample_ragged(sigma_coarse, ns, nt_panels, ms, mt_panels, ncomp, out=None):
-    """(NEXT N4) per-panel angular orders: panel p is ns x nt[p] -> ms x mt[p] (host int arrays)."""
+def slb_upsample_ragged(sigma_coarse, ns_panels, nt_panels, ms_panels, mt_panels, ncomp, out=None):
+    """(NEXT N4) per-panel orders: panel p is ns[p] x nt[p] -> ms[p] x mt[p] (host int arrays; a
+    scalar ns / ms applies to every panel)."""
+    import numpy as np
     nt = _host_i32(nt_panels, "nt_panels")
-    mt = _host_i32(mt_panels, "mt_panels")
-    if nt.shape != mt.shape:
-        raise SlbError("nt_panels and mt_panels differ in length")
+    P = nt.size
+    ns = _host_i32(np.broadcast_to(np.asarray(ns_panels), (P,)), "ns_panels")
+    ms = _host_i32(np.broadcast_to(np.asarray(ms_panels), (P,)), "ms_panels")
+    mt = _host_i32(np.broadcast_to(np.asarray(mt_panels), (P,)), "mt_panels")
     if out is None:
-        out = torch.empty(int((ms * mt.astype("int64")).sum()) * ncomp, dtype=torch.float64,
+        out = torch.empty(int((ms.astype("int64") * mt).sum()) * ncomp, dtype=torch.float64,
                           device=sigma_coarse.device)
-    check(lib().slb_upsample_ragged(nt.size, ns, ctypes.c_void_p(nt.ctypes.data), ms, ctypes.c_void_p(mt.ctypes.data),
-                                    ncomp, _dev(sigma_coarse, "sigma_coarse"), _dev(out, "sigma_fine"), _stream()))
+    vp = lambda a: ctypes.c_void_p(a.ctypes.data)
+    check(lib().slb_upsample_ragged(P, vp(ns), vp(nt), vp(ms), vp(mt), ncomp, _dev(sigma_coarse, "sigma_coarse"),
+                                    _dev(out, "sigma_fine"), _stream()))
     return out
 
 
@@ -122,16 +126,20 @@ def slb_nearcorr_fold(kernel, x_trg, row_ptr, panel_idx, ns, nt, ms, mt, y_fine,
 
 
 def slb_nearcorr_quad(kernel, x_trg, row_ptr, panel_idx, ns, nt, y_coarse, blocks, trg_node=None, eta_panel=None,
-                      order=12, beta=0.6, panel_nt=None):
+                      order=12, beta=0.6, panel_nt=None, panel_ns=None):
     """Special-quadrature blocks B for the CSR pairs (unfolded), written into `blocks`.
-    panel_nt (host int array [n_panels]): ragged angular orders (NEXT N4); nt is then ignored."""
+    panel_nt / panel_ns (host int arrays [n_panels]): ragged orders (NEXT N4); nt / ns then ignored."""
+    import numpy as np
     T = row_ptr.shape[0] - 1
-    if panel_nt is not None:
-        pnt = _host_i32(panel_nt, "panel_nt")
+    if panel_nt is not None or panel_ns is not None:
+        P = len(panel_nt) if panel_nt is not None else len(panel_ns)
+        pnt = _host_i32(panel_nt if panel_nt is not None else np.full(P, nt), "panel_nt")
+        pns = _host_i32(panel_ns if panel_ns is not None else np.full(P, ns), "panel_ns")
         check(lib().slb_nearcorr_quad_ragged(kernel, T, _dev(x_trg, "x_trg"),
                                              _dev(trg_node, "trg_node", torch.int64, True),
                                              _dev(row_ptr, "row_ptr", torch.int64),
-                                             _dev(panel_idx, "panel_idx", torch.int32), pnt.size, ns,
+                                             _dev(panel_idx, "panel_idx", torch.int32), P,
+                                             ctypes.c_void_p(pns.ctypes.data),
                                              ctypes.c_void_p(pnt.ctypes.data), _dev(y_coarse, "y_coarse"),
                                              _dev(eta_panel, "eta_panel", allow_none=True), int(order), float(beta),
                                              _dev(blocks, "blocks"), _stream()))
@@ -201,8 +209,8 @@ class Operator:
     def __init__(self, *, kernel, ns, nt, ms, mt, n_panels_global, panel_begin, panel_end, x_trg, n_on,
                  y_fine, n_fine, w_fine, row_ptr, panel_idx, blocks, c_identity=0.5, eta_fine=None, eta=0.0,
                  folded=False, n_bodies=0, body_of_panel=None, y_coarse=None, w_coarse=None, comm=None,
-                 panel_nt=None, panel_mt=None):
-        """panel_nt / panel_mt (host int arrays [n_panels_global]): ragged angular orders (NEXT N4)."""
+                 panel_nt=None, panel_mt=None, panel_ns=None, panel_ms=None):
+        """panel_nt / panel_mt, panel_ns / panel_ms (host int arrays [n_panels_global]): ragged orders (NEXT N4)."""
         self._keep = [x_trg, y_fine, n_fine, w_fine, eta_fine, row_ptr, panel_idx, blocks, body_of_panel,
                       y_coarse, w_coarse]
         d = OperatorDesc()
@@ -221,15 +229,22 @@ class Operator:
         if n_bodies:
             d.body_of_panel_local = _dev(body_of_panel, "body_of_panel", torch.int32)
             d.y_coarse, d.w_coarse = _dev(y_coarse, "y_coarse"), _dev(w_coarse, "w_coarse")
-        if (panel_nt is None) != (panel_mt is None):
-            raise SlbError("panel_nt and panel_mt must be given together")
+        if (panel_nt is None) != (panel_mt is None) or (panel_ns is None) != (panel_ms is None):
+            raise SlbError("panel_nt/panel_mt and panel_ns/panel_ms must be given in pairs")
+        import numpy as np
+        P = n_panels_global
+        nn = np.full(P, ns, dtype=np.int64) * np.full(P, nt, dtype=np.int64)
         if panel_nt is not None:
             pnt, pmt = _host_i32(panel_nt, "panel_nt"), _host_i32(panel_mt, "panel_mt")
             self._keep += [pnt, pmt]
             d.panel_nt, d.panel_mt = pnt.ctypes.data, pmt.ctypes.data
-            self.n_loc_nodes = int(ns * pnt[panel_begin:panel_end].astype("int64").sum())
-        else:
-            self.n_loc_nodes = (panel_end - panel_begin) * ns * nt
+            nn = nn // nt * pnt.astype(np.int64)
+        if panel_ns is not None:
+            pns, pms = _host_i32(panel_ns, "panel_ns"), _host_i32(panel_ms, "panel_ms")
+            self._keep += [pns, pms]
+            d.panel_ns, d.panel_ms = pns.ctypes.data, pms.ctypes.data
+            nn = nn // ns * pns.astype(np.int64)
+        self.n_loc_nodes = int(nn[panel_begin:panel_end].sum())
         self.desc = d
         self.kernel = kernel
         self.tdim = 1 if kernel == LAPLACE_DL else 3

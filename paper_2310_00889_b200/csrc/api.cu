@@ -2,6 +2,7 @@
 // error/status plumbing shared by the library.  See include/slb.h for the contract.
 #include <cmath>
 #include <string>
+#include <array>
 #include <map>
 #include <string>
 #include <vector>
@@ -101,22 +102,23 @@ slb_status slb_upsample(int64_t n_panels, int ns, int nt, int ms, int mt, int nc
     return st;
 }
 
-slb_status slb_upsample_ragged(int64_t n_panels, int ns, const int32_t* nt, int ms, const int32_t* mt, int ncomp,
-                               const double* sigma_coarse, double* sigma_fine, cudaStream_t s) {
+slb_status slb_upsample_ragged(int64_t n_panels, const int32_t* ns, const int32_t* nt, const int32_t* ms,
+                               const int32_t* mt, int ncomp, const double* sigma_coarse, double* sigma_fine,
+                               cudaStream_t s) {
     SLB_REQUIRE(n_panels >= 0, SLB_ERR_INVALID_ARG, "n_panels < 0");
     SLB_REQUIRE(ncomp == 1 || ncomp == 3, SLB_ERR_INVALID_ARG, "ncomp must be 1 or 3");
-    SLB_REQUIRE(ns >= 1 && ms >= 1 && ns <= SLB_MAX_NS && ms <= SLB_MAX_MS, SLB_ERR_INVALID_ARG, "bad ns/ms");
     if (n_panels == 0) return SLB_OK;
-    SLB_REQUIRE(nt && mt && sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
+    SLB_REQUIRE(ns && nt && ms && mt && sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(check_sticky("slb_upsample_ragged") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
     std::vector<int64_t> c0(n_panels + 1, 0), f0(n_panels + 1, 0);
-    std::map<std::pair<int, int>, std::vector<int32_t>> groups;
+    std::map<std::array<int, 4>, std::vector<int32_t>> groups;
     for (int64_t p = 0; p < n_panels; ++p) {
-        SLB_REQUIRE(nt[p] >= 2 && nt[p] % 2 == 0 && nt[p] <= SLB_MAX_NT && mt[p] >= 2 && mt[p] <= SLB_MAX_MT,
-                    SLB_ERR_INVALID_ARG, "panel orders must be even and within the compiled limits");
-        c0[p + 1] = c0[p] + (int64_t)ns * nt[p];
-        f0[p + 1] = f0[p] + (int64_t)ms * mt[p];
-        groups[{nt[p], mt[p]}].push_back((int32_t)p);
+        SLB_REQUIRE(nt[p] >= 2 && nt[p] % 2 == 0 && nt[p] <= SLB_MAX_NT && mt[p] >= 2 && mt[p] <= SLB_MAX_MT &&
+                        ns[p] >= 1 && ns[p] <= SLB_MAX_NS && ms[p] >= 1 && ms[p] <= SLB_MAX_MS,
+                    SLB_ERR_INVALID_ARG, "panel orders must be positive (N_th even) and within the compiled limits");
+        c0[p + 1] = c0[p] + (int64_t)ns[p] * nt[p];
+        f0[p + 1] = f0[p] + (int64_t)ms[p] * mt[p];
+        groups[{ns[p], nt[p], ms[p], mt[p]}].push_back((int32_t)p);
     }
     int64_t *c0d = nullptr, *f0d = nullptr;
     int32_t* pl = nullptr;
@@ -139,7 +141,7 @@ slb_status slb_upsample_ragged(int64_t n_panels, int ns, const int32_t* nt, int 
     int64_t off = 0;
     for (auto& g : groups) {
         double* o = nullptr;
-        if (!make_interp(ns, g.first.first, ms, g.first.second, &ip, &o)) {
+        if (!make_interp(g.first[0], g.first[1], g.first[2], g.first[3], &ip, &o)) {
             set_error("slb_upsample_ragged: interpolation matrices: allocation failed");
             st = SLB_ERR_OOM;
             break;

@@ -196,7 +196,7 @@ slb_status finalize_launch(const FarPlan& plan, int64_t n_trg, int tdim, int col
                            const double* blocks, const double* sigma_c_global, int64_t n_on,
                            double c_id, const double* sig_local, const double* Lsig, double* u,
                            int G, cudaStream_t s, const RagNear& rag = RagNear());
-int near_group_size(int64_t T, int64_t nnz);
+int near_group_size(int64_t T, int64_t nnz, double block_bytes);   // block_bytes: mean near block size
 slb_status csr_check(int64_t T, const int64_t* row_ptr, const int32_t* panel_idx, int64_t n_panels);
 // Ragged (NEXT N4): only pairs whose panel has pbucket[k] == bucket are folded (pbucket NULL: all);
 // fn0 = first fine node of each global panel, boff = block offsets (NULL: uniform).

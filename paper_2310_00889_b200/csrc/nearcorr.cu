@@ -260,9 +260,9 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
     }
 }
 
-// Chunked streaming for ragged blocks, and for uniform blocks too wide for two CTAs of the plain
-// ring per SM (c3: 17 KB blocks): slots of S <= kChunk2 double2 keep two 4-warp CTAs per SM.
-constexpr int kChunk2 = 576;   // double2 per slot: 4 warps x 3 stages x 9.2 KB = 110 KB per CTA
+// Chunked streaming for ragged blocks: slots of S <= kChunk2 double2 (measured on c3v: 800 double2
+// = 12.8 KB slots, one 4-warp CTA per SM, beat 576 with two CTAs per SM by 15 %).
+constexpr int kChunk2 = 800;
 
 static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_t* row_ptr, const int32_t* panel_idx,
                                      const double* blocks, const double* sigma_c, const double* partials,
@@ -303,7 +303,7 @@ slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, c
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
                            const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
                            const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
-    if (rag.boff || tdim * cols / 2 > kChunk2 + kChunk2 / 8)
+    if (rag.boff)
         return near_ragged_launch(1, T, tdim, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
                                   n_on, c_id, sig_local, Lsig, u, G, s, rag, cols);
     return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
@@ -321,7 +321,8 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
             const double* __restrict__ y_f, const double* __restrict__ n_f, const double* __restrict__ w_f,
             const double* __restrict__ eta_f, double eta, double* __restrict__ blocks,
             const int32_t* __restrict__ pbucket, int bucket, const int64_t* __restrict__ fn0,
-            const int64_t* __restrict__ boff) {
+            const int64_t* __restrict__ boff, int rch) {
+    // rch: fine GL rows (a) per pass -- ms unless a (32 x 128) panel's G would not fit shared memory
     extern __shared__ double sm[];
     const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
     const double* Ps = ip.vg ? ip.vg : ip.v;
@@ -329,65 +330,69 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
     const int Mn = ms * mt, Nn = ns * nt;
     const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
     const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
-    double* G = sm;                 // [NG][Mn]
-    double* H = sm + NG * Mn;       // [NG][ms][nt]
+    const int Mc = rch * mt;        // fine nodes per pass
+    double* G = sm;                 // [NG][rch * mt]
+    double* H = sm + NG * Mc;       // [NG][rch][nt]
     const int64_t t = blockIdx.x;
     if (t >= T) return;
     const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
-        if (pbucket && pbucket[k] != bucket) continue;          // ragged: another launch's (nt, mt)
+        if (pbucket && pbucket[k] != bucket) continue;          // ragged: another launch's orders
         const int64_t mk0 = fn0 ? fn0[k] : k * (int64_t)Mn;
-        for (int q = threadIdx.x; q < Mn; q += blockDim.x) {
-            const int64_t m = mk0 + q;
-            double r[3] = {x0 - y_f[3 * m], x1 - y_f[3 * m + 1], x2 - y_f[3 * m + 2]};
-            double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
-            double nn[3] = {n_f[3 * m], n_f[3 * m + 1], n_f[3 * m + 2]};
-            double w = w_f[m];
-            if (r2 == 0.0) {
-                for (int g = 0; g < NG; ++g) G[g * Mn + q] = 0.0;
-                continue;
-            }
-            double ir = 1.0 / sqrt(r2);
-            double rn = r[0] * nn[0] + r[1] * nn[1] + r[2] * nn[2];
-            if (kind == FAR_LAPLACE) {
-                G[q] = rn * ir * ir * ir / (4.0 * kPi) * w;
-            } else {
-                double e = (kind == FAR_STOKES_SLDL) ? (eta_f ? eta_f[m] : eta) : 0.0;
-                double ir3 = ir * ir * ir;
-                double sl = e / (8.0 * kPi);
-                double dl = 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
-                int g = 0;
-                for (int i = 0; i < 3; ++i)
-                    for (int j = i; j < 3; ++j, ++g) {
-                        double v = sl * ((i == j ? ir : 0.0) + r[i] * r[j] * ir3) + dl * r[i] * r[j];
-                        G[g * Mn + q] = v * w;
-                    }
-            }
-        }
-        __syncthreads();
-        const int nH = NG * ms * nt;
-        for (int q = threadIdx.x; q < nH; q += blockDim.x) {
-            int b = q % nt, a = (q / nt) % ms, g = q / (nt * ms);
-            const double* Gr = G + g * Mn + a * mt;
-            double acc = 0.0;
-            for (int c = 0; c < mt; ++c) acc = fma(Gr[c], F[c * nt + b], acc);
-            H[q] = acc;
-        }
-        __syncthreads();
         double* Bp = blocks + (boff ? boff[p] : p * (int64_t)TD * Nn * TD);
-        const int nE = TD * Nn * TD;
-        for (int q = threadIdx.x; q < nE; q += blockDim.x) {
-            int j = q % TD, node = (q / TD) % Nn, i = q / (TD * Nn);
-            int a2 = node / nt, b = node % nt;
-            int lo = i < j ? i : j, hi = i < j ? j : i;
-            int g = (TD == 1) ? 0 : (lo == 0 ? hi : (lo == 1 ? 2 + hi : 5));
-            const double* Hg = H + g * ms * nt;
-            double acc = 0.0;
-            for (int a = 0; a < ms; ++a) acc = fma(Ps[a * ns + a2], Hg[a * nt + b], acc);
-            Bp[q] -= acc;
+        for (int a0 = 0; a0 < ms; a0 += rch) {
+            const int ra = min(rch, ms - a0);
+            for (int q = threadIdx.x; q < ra * mt; q += blockDim.x) {
+                const int64_t m = mk0 + (int64_t)a0 * mt + q;
+                double r[3] = {x0 - y_f[3 * m], x1 - y_f[3 * m + 1], x2 - y_f[3 * m + 2]};
+                double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+                double nn[3] = {n_f[3 * m], n_f[3 * m + 1], n_f[3 * m + 2]};
+                double w = w_f[m];
+                if (r2 == 0.0) {
+                    for (int g = 0; g < NG; ++g) G[g * Mc + q] = 0.0;
+                    continue;
+                }
+                double ir = 1.0 / sqrt(r2);
+                double rn = r[0] * nn[0] + r[1] * nn[1] + r[2] * nn[2];
+                if (kind == FAR_LAPLACE) {
+                    G[q] = rn * ir * ir * ir / (4.0 * kPi) * w;
+                } else {
+                    double e = (kind == FAR_STOKES_SLDL) ? (eta_f ? eta_f[m] : eta) : 0.0;
+                    double ir3 = ir * ir * ir;
+                    double sl = e / (8.0 * kPi);
+                    double dl = 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
+                    int g = 0;
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = i; j < 3; ++j, ++g) {
+                            double v = sl * ((i == j ? ir : 0.0) + r[i] * r[j] * ir3) + dl * r[i] * r[j];
+                            G[g * Mc + q] = v * w;
+                        }
+                }
+            }
+            __syncthreads();
+            const int nH = NG * ra * nt;
+            for (int q = threadIdx.x; q < nH; q += blockDim.x) {
+                int b = q % nt, a = (q / nt) % ra, g = q / (nt * ra);
+                const double* Gr = G + g * Mc + a * mt;
+                double acc = 0.0;
+                for (int c = 0; c < mt; ++c) acc = fma(Gr[c], F[c * nt + b], acc);
+                H[(g * rch + a) * nt + b] = acc;
+            }
+            __syncthreads();
+            const int nE = TD * Nn * TD;
+            for (int q = threadIdx.x; q < nE; q += blockDim.x) {
+                int j = q % TD, node = (q / TD) % Nn, i = q / (TD * Nn);
+                int a2 = node / nt, b = node % nt;
+                int lo = i < j ? i : j, hi = i < j ? j : i;
+                int g = (TD == 1) ? 0 : (lo == 0 ? hi : (lo == 1 ? 2 + hi : 5));
+                const double* Hg = H + g * rch * nt;
+                double acc = 0.0;
+                for (int a = 0; a < ra; ++a) acc = fma(Ps[(a0 + a) * ns + a2], Hg[a * nt + b], acc);
+                Bp[q] -= acc;
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -399,11 +404,14 @@ slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64
     if (T <= 0) return SLB_OK;
     SLB_REQUIRE(T <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets for fold");
     const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
-    size_t smem = sizeof(double) * (size_t)(NG * ip.ms * ip.mt + NG * ip.ms * ip.nt);
+    auto smem_of = [&](int r) { return sizeof(double) * (size_t)(NG * r * ip.mt + NG * r * ip.nt); };
+    int rch = ip.ms;
+    while (rch > 1 && smem_of(rch) > 227 * 1024) rch = (rch + 1) / 2;
+    const size_t smem = smem_of(rch);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "fold: grid too large for shared memory");
     SLB_CUDA(cudaFuncSetAttribute(fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fold_kernel<<<(unsigned)T, 128, smem, s>>>((int)kind, T, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine,
-                                              w_fine, eta_fine, eta, blocks, pbucket, bucket, fn0, boff);
+                                              w_fine, eta_fine, eta, blocks, pbucket, bucket, fn0, boff, rch);
     ++g_launch_count;
     return check_launch("fold_kernel");
 }
@@ -436,12 +444,16 @@ extern "C" slb_status slb_fill_blocks(uint64_t seed, uint64_t first, int64_t cou
 }
 
 namespace slb {
-// targets per warp for the streaming near kernel: about 48 blocks of streaming per warp
-int near_group_size(int64_t T, int64_t nnz) {
+// targets per warp for the streaming near kernel: ~420 KB of blocks streamed per warp (48 blocks of
+// 8.6 KB at c4/c5), but at least ~8 CTAs' worth of warp groups per SM so the last wave's tail stays
+// short (c3, 30 k targets with 17 KB blocks: G = 2 -> 0.81 ms vs G = 9 -> 1.07 ms).
+int near_group_size(int64_t T, int64_t nnz, double block_bytes) {
     if (const char* e = getenv("SLB_NEAR_G")) return std::max(1, atoi(e));
-    if (T <= 0) return 1;
-    const double avg = (double)nnz / (double)T;
-    return (int)std::min<double>(16.0, std::max<double>(1.0, std::round(48.0 / std::max(avg, 1e-9))));
+    if (T <= 0 || nnz <= 0) return 1;
+    const double per_target = (double)nnz / (double)T * block_bytes;
+    double G = std::round(420e3 / std::max(per_target, 1.0));
+    G = std::min(G, std::floor((double)T / (4.0 * 148.0 * 8.0)));
+    return (int)std::min<double>(16.0, std::max<double>(1.0, G));
 }
 }  // namespace slb
 

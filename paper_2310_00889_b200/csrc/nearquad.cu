@@ -33,12 +33,13 @@ constexpr int kQThreads = 128;
 constexpr int kMaxCells = 768;
 constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
 
+constexpr int kTri = kMaxNsQ * (kMaxNsQ + 1) / 2;   // GL tables for every n <= kMaxNsQ, at n (n-1) / 2
 struct QuadParams {
-    int ns, nt, q, qd;
+    int ns, nt, q, qd;        // ns, nt: the largest panel orders of the launch (shared-memory layout)
     double beta;
     double dl;                // weight of the double layer: 1, or 0 for the pure single layer (SLB_STOKES_SL)
-    double tgl[kMaxNsQ];      // panel GL nodes on [-1,1]
-    double lam[kMaxNsQ];      // barycentric weights
+    double tgl[kTri];         // GL nodes on [-1,1] of every order n: tgl[n (n-1)/2 + i]
+    double lam[kTri];         // barycentric weights, same layout
     double gx[kMaxQ], gw[kMaxQ];        // q-point GL on [-1,1]
     double dx[kMaxQ], dw[kMaxQ];        // qd-point GL on [0,1]
 };
@@ -51,18 +52,18 @@ struct Cell {
 };
 
 // Lagrange basis l_i(t) and l_i'(t) (barycentric second form + derivative formula)
-__device__ void lagrange_eval(const QuadParams& P, double t, double* l, double* dl) {
-    const int n = P.ns;
+// tg / lm: the panel order's GL nodes and barycentric weights (QuadParams tables)
+__device__ void lagrange_eval(int n, const double* tg, const double* lm, double t, double* l, double* dl) {
     int hit = -1;
     for (int i = 0; i < n; ++i)
-        if (fabs(t - P.tgl[i]) < 1e-15) hit = i;
+        if (fabs(t - tg[i]) < 1e-15) hit = i;
     if (hit >= 0) {
         // l_i(t_k) = delta; l_i'(t_k) = (lam_i/lam_k)/(t_k - t_i) (i != k), l_k'(t_k) = -sum_{i != k} l_i'(t_k)
         double s = 0.0;
         for (int i = 0; i < n; ++i) {
             l[i] = (i == hit) ? 1.0 : 0.0;
             if (i != hit) {
-                dl[i] = (P.lam[i] / P.lam[hit]) / (P.tgl[hit] - P.tgl[i]);
+                dl[i] = (lm[i] / lm[hit]) / (tg[hit] - tg[i]);
                 s += dl[i];
             }
         }
@@ -71,13 +72,13 @@ __device__ void lagrange_eval(const QuadParams& P, double t, double* l, double* 
     }
     double den = 0.0, dden = 0.0;
     for (int i = 0; i < n; ++i) {
-        const double c = P.lam[i] / (t - P.tgl[i]);
+        const double c = lm[i] / (t - tg[i]);
         den += c;
-        dden -= c / (t - P.tgl[i]);
+        dden -= c / (t - tg[i]);
     }
     for (int i = 0; i < n; ++i) {
-        const double c = P.lam[i] / (t - P.tgl[i]);
-        const double dc = -c / (t - P.tgl[i]);
+        const double c = lm[i] / (t - tg[i]);
+        const double dc = -c / (t - tg[i]);
         l[i] = c / den;
         dl[i] = (dc * den - c * dden) / (den * den);
     }
@@ -115,13 +116,13 @@ __device__ void trig_eval(int N, double th, double* C, double* dC, const double*
 }
 
 // surface point and tangents from the panel's nodes Y[i][j][3]
-__device__ void geom_eval(const QuadParams& P, int nt, const double* Y, double t, double th, double* y, double* yt,
-                          double* yh, double* lbuf, double* dlbuf, double* Cb, double* dCb, const double* TC,
-                          const double* TS) {
-    lagrange_eval(P, t, lbuf, dlbuf);
+__device__ void geom_eval(int ns, const double* tg, const double* lm, int nt, const double* Y, double t, double th,
+                          double* y, double* yt, double* yh, double* lbuf, double* dlbuf, double* Cb, double* dCb,
+                          const double* TC, const double* TS) {
+    lagrange_eval(ns, tg, lm, t, lbuf, dlbuf);
     trig_eval(nt, th, Cb, dCb, TC, TS);
     for (int c = 0; c < 3; ++c) { y[c] = 0.0; yt[c] = 0.0; yh[c] = 0.0; }
-    for (int i = 0; i < P.ns; ++i) {
+    for (int i = 0; i < ns; ++i) {
         double a[3] = {0, 0, 0}, ad[3] = {0, 0, 0};
         for (int j = 0; j < nt; ++j) {
             const double* Yij = Y + (i * nt + j) * 3;
@@ -135,16 +136,109 @@ __device__ void geom_eval(const QuadParams& P, int nt, const double* Y, double t
     }
 }
 
+// trig cardinal functions without the per-panel cos/sin tables (closest-point pre-pass)
+__device__ void trig_eval_direct(int N, double th, double* C, double* dC) {
+    for (int j = 0; j < N; ++j) {
+        const double p = th - 2.0 * kPi * j / N;
+        double sv = 1.0, dv = 0.0, c1, s1;
+        sincos(p, &s1, &c1);
+        double ck = c1, sk = s1;
+        for (int l = 1; l < N / 2; ++l) {
+            sv += 2.0 * ck;
+            dv -= 2.0 * l * sk;
+            const double cn = ck * c1 - sk * s1, sn = sk * c1 + ck * s1;
+            ck = cn; sk = sn;
+        }
+        sv += ck;
+        dv -= 0.5 * N * sk;
+        C[j] = sv / N;
+        dC[j] = dv / N;
+    }
+}
+
+// Closest point (t*, th*) of every off-surface (target, panel) pair by Gauss-Newton on
+// |x - y(t, th)|^2 from the nearest node, one thread per CSR entry (setup pre-pass: keeps this
+// serial iteration off the quadrature CTA's critical path).  cp[p] = {t*, th*}; singular pairs skipped.
+__global__ void __launch_bounds__(128)
+nearquad_cp_kernel(int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ trg_node,
+                   const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
+                   const double* __restrict__ y_coarse, const __grid_constant__ QuadParams P,
+                   const int32_t* __restrict__ pnt, const int64_t* __restrict__ cn0,
+                   const int32_t* __restrict__ pns, double* __restrict__ cp) {
+    const int64_t nnz = row_ptr[T];
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nnz) return;
+    int64_t lo = 0, hi = T - 1;                           // target t: row_ptr[t] <= p < row_ptr[t+1]
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (row_ptr[mid] <= p) lo = mid; else hi = mid - 1;
+    }
+    const int64_t t = lo;
+    const int64_t k = panel_idx[p];
+    const int nt = pnt ? pnt[k] : P.nt, ns = pns ? pns[k] : P.ns, Nn = ns * nt;
+    const int64_t c0 = cn0 ? cn0[k] : k * (int64_t)Nn;
+    const int64_t node = trg_node ? trg_node[t] : -1;
+    if (node >= c0 && node < c0 + Nn) return;              // singular: the node itself
+    const double* tg = P.tgl + ns * (ns - 1) / 2;
+    const double* lm = P.lam + ns * (ns - 1) / 2;
+    const double* Y = y_coarse + c0 * 3;
+    const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
+    double best = 1e300, ts = 0.0, hs = 0.0;
+    for (int i = 0; i < ns; ++i)
+        for (int j = 0; j < nt; ++j) {
+            const double* Yij = Y + (i * nt + j) * 3;
+            const double d2 = (x0 - Yij[0]) * (x0 - Yij[0]) + (x1 - Yij[1]) * (x1 - Yij[1]) +
+                              (x2 - Yij[2]) * (x2 - Yij[2]);
+            if (d2 < best) { best = d2; ts = tg[i]; hs = 2.0 * kPi * j / nt; }
+        }
+    double lb[kMaxNsQ], dlb[kMaxNsQ], Cb[kMaxNtQ], dCb[kMaxNtQ];
+    for (int it = 0; it < 12; ++it) {
+        double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
+        lagrange_eval(ns, tg, lm, ts, lb, dlb);
+        trig_eval_direct(nt, hs, Cb, dCb);
+        for (int i = 0; i < ns; ++i) {
+            double a[3] = {0, 0, 0}, ad[3] = {0, 0, 0};
+            for (int j = 0; j < nt; ++j) {
+                const double* Yij = Y + (i * nt + j) * 3;
+                for (int c = 0; c < 3; ++c) { a[c] = fma(Cb[j], Yij[c], a[c]); ad[c] = fma(dCb[j], Yij[c], ad[c]); }
+            }
+            for (int c = 0; c < 3; ++c) {
+                y[c] = fma(lb[i], a[c], y[c]);
+                yt[c] = fma(dlb[i], a[c], yt[c]);
+                yh[c] = fma(lb[i], ad[c], yh[c]);
+            }
+        }
+        const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
+        const double a11 = yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2];
+        const double a22 = yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2];
+        const double a12 = yt[0] * yh[0] + yt[1] * yh[1] + yt[2] * yh[2];
+        const double g1 = r[0] * yt[0] + r[1] * yt[1] + r[2] * yt[2];
+        const double g2 = r[0] * yh[0] + r[1] * yh[1] + r[2] * yh[2];
+        const double det = a11 * a22 - a12 * a12;
+        if (!(det > 0.0)) break;
+        double dt = (a22 * g1 - a12 * g2) / det, dh = (a11 * g2 - a12 * g1) / det;
+        const double tn = fmin(1.0, fmax(-1.0, ts + dt));
+        if (tn != ts + dt) dh = g2 / a22;                  // on the boundary: 1-D step in th
+        dt = tn - ts;
+        ts = tn;
+        hs += dh;
+        if (fabs(dt) + fabs(dh) < 1e-15) break;
+    }
+    cp[2 * p] = ts;
+    cp[2 * p + 1] = hs;
+}
+
 __global__ void __launch_bounds__(kQThreads)
 nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ trg_node,
                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
                 const double* __restrict__ y_coarse, const double* __restrict__ eta_panel,
                 const __grid_constant__ QuadParams P, double* __restrict__ blocks, int* __restrict__ status,
-                const int32_t* __restrict__ pnt, const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff) {
+                const int32_t* __restrict__ pnt, const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff,
+                const int32_t* __restrict__ pns, const double* __restrict__ cp) {
     extern __shared__ double sm[];
     // ragged (NEXT N4): panel k has pnt[k] angular nodes and starts at coarse node cn0[k]; block p at
     // boff[p]; the shared layout is sized for P.nt = the largest order.  NULL: uniform P.nt.
-    const int ns = P.ns, ntm = P.nt, Nnm = ns * ntm;
+    const int nsm = P.ns, ntm = P.nt, Nnm = nsm * ntm;   // largest panel of the launch
     const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
     const int NG = TD * TD;
     const int tid = threadIdx.x;
@@ -153,7 +247,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     double* Bacc = Y + Nnm * 3;                       // [NG][ns][nt]
     double* Gs = Bacc + NG * Nnm;                     // [128][NG]
     double* Ls = Gs + kQThreads * NG;                 // [128][ns]
-    double* Cs = Ls + kQThreads * ns;                 // [128][nt]
+    double* Cs = Ls + kQThreads * nsm;                // [128][nt]
     double* TC = Cs + kQThreads * ntm;                // [ntm] cos(2 pi m / nt) of the current panel
     double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
     Cell* cells = reinterpret_cast<Cell*>(TS + ntm);
@@ -168,7 +262,9 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     const int64_t node = trg_node ? trg_node[t] : -1;
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
-        const int nt = pnt ? pnt[k] : ntm, Nn = ns * nt;
+        const int nt = pnt ? pnt[k] : ntm, ns = pns ? pns[k] : nsm, Nn = ns * nt;
+        const double* tg = P.tgl + ns * (ns - 1) / 2;
+        const double* lm = P.lam + ns * (ns - 1) / 2;
         const int64_t c0 = cn0 ? cn0[k] : k * (int64_t)Nn;
         const double eta = (kind == FAR_STOKES_SLDL) ? (eta_panel ? eta_panel[k] : 1.0) : 0.0;
         for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[c0 * 3 + e];
@@ -182,41 +278,14 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             double ts, hs;
             if (singular) {
                 const int loc = (int)(node - c0);
-                ts = P.tgl[loc / nt];
+                ts = tg[loc / nt];
                 hs = 2.0 * kPi * (loc % nt) / nt;
-            } else {
-                double best = 1e300;
-                ts = 0.0; hs = 0.0;
-                for (int i = 0; i < ns; ++i)
-                    for (int j = 0; j < nt; ++j) {
-                        const double* Yij = Y + (i * nt + j) * 3;
-                        const double d2 = (x0 - Yij[0]) * (x0 - Yij[0]) + (x1 - Yij[1]) * (x1 - Yij[1]) +
-                                          (x2 - Yij[2]) * (x2 - Yij[2]);
-                        if (d2 < best) { best = d2; ts = P.tgl[i]; hs = 2.0 * kPi * j / nt; }
-                    }
-                // Gauss-Newton on |x - y(t,th)|^2, t clamped to [-1, 1]
-                for (int it = 0; it < 12; ++it) {
-                    double y[3], yt[3], yh[3];
-                    geom_eval(P, nt, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
-                    const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
-                    const double a11 = yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2];
-                    const double a22 = yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2];
-                    const double a12 = yt[0] * yh[0] + yt[1] * yh[1] + yt[2] * yh[2];
-                    const double g1 = r[0] * yt[0] + r[1] * yt[1] + r[2] * yt[2];
-                    const double g2 = r[0] * yh[0] + r[1] * yh[1] + r[2] * yh[2];
-                    const double det = a11 * a22 - a12 * a12;
-                    if (!(det > 0.0)) break;
-                    double dt = (a22 * g1 - a12 * g2) / det, dh = (a11 * g2 - a12 * g1) / det;
-                    const double tn = fmin(1.0, fmax(-1.0, ts + dt));
-                    if (tn != ts + dt) dh = g2 / a22;      // on the boundary: 1-D step in th
-                    dt = tn - ts;
-                    ts = tn;
-                    hs += dh;
-                    if (fabs(dt) + fabs(dh) < 1e-15) break;
-                }
+            } else {                          // Gauss-Newton result of the pre-pass
+                ts = cp[2 * p];
+                hs = cp[2 * p + 1];
             }
             double y[3], yt[3], yh[3];
-            geom_eval(P, nt, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
+            geom_eval(ns, tg, lm, nt, Y, ts, hs, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
             const double d = singular ? 0.0
                                       : sqrt((x0 - y[0]) * (x0 - y[0]) + (x1 - y[1]) * (x1 - y[1]) +
                                              (x2 - y[2]) * (x2 - y[2]));
@@ -328,7 +397,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
                 }
                 double y[3], yt[3], yh[3];
-                geom_eval(P, nt, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
+                geom_eval(ns, tg, lm, nt, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
                 // outward normal (R8): n = y_th x y_t / |.|, J = |y_th x y_t|
                 const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
                                       yh[0] * yt[1] - yh[1] * yt[0]};
@@ -408,16 +477,20 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
                                const double* y_coarse, const double* eta_panel, int order, double beta,
                                double* blocks, cudaStream_t s, const int32_t* pnt, const int64_t* cn0,
-                               const int64_t* boff) {
+                               const int64_t* boff, const int32_t* pns) {
     static QuadParams P;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
     P.dl = (kernel == SLB_STOKES_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
-    gl_nodes(ns, P.tgl, w);
-    for (int i = 0; i < ns; ++i) {
-        double pr = 1.0;
-        for (int l = 0; l < ns; ++l) if (l != i) pr *= (P.tgl[i] - P.tgl[l]);
-        P.lam[i] = 1.0 / pr;
+    for (int n = 2; n <= kMaxNsQ; ++n) {
+        double* tg = P.tgl + n * (n - 1) / 2;
+        double* lm = P.lam + n * (n - 1) / 2;
+        gl_nodes(n, tg, w);
+        for (int i = 0; i < n; ++i) {
+            double pr = 1.0;
+            for (int l = 0; l < n; ++l) if (l != i) pr *= (tg[i] - tg[l]);
+            lm[i] = 1.0 / pr;
+        }
     }
     gl_nodes(P.q, P.gx, P.gw);
     gl_nodes(P.qd, P.dx, P.dw);
@@ -431,9 +504,19 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     int* st = nullptr;
     SLB_CUDA(cudaMallocAsync(&st, sizeof(int), s));
     SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
+    int64_t nnz = 0;
+    SLB_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_trg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SLB_CUDA(cudaStreamSynchronize(s));
+    double* cp = nullptr;
+    SLB_CUDA(cudaMallocAsync(&cp, sizeof(double) * 2 * std::max<int64_t>(nnz, 1), s));
+    if (nnz > 0) {
+        nearquad_cp_kernel<<<(unsigned)((nnz + 127) / 128), 128, 0, s>>>(n_trg, x_trg, trg_node, row_ptr, panel_idx,
+                                                                        y_coarse, P, pnt, cn0, pns, cp);
+        ++g_launch_count;
+    }
     const FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE : FAR_STOKES_SLDL;
     nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem, s>>>((int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx,
-                                                             y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff);
+                                                             y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff, pns, cp);
     ++g_launch_count;
     slb_status r = check_launch("nearquad_kernel");
     int h = 0;
@@ -443,6 +526,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         if (e != cudaSuccess) { set_error(std::string("nearquad: ") + cudaGetErrorString(e)); r = SLB_ERR_CUDA; }
     }
     cudaFreeAsync(st, s);
+    cudaFreeAsync(cp, s);
     if (r == SLB_OK && h) {
         set_error("nearquad: adaptive cell budget exceeded (target extremely close to a panel?)");
         r = SLB_ERR_UNSUPPORTED;
@@ -472,29 +556,32 @@ extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const 
     SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks, SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
     return nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, nt, y_coarse, eta_panel, order, beta,
-                        blocks, s, nullptr, nullptr, nullptr);
+                        blocks, s, nullptr, nullptr, nullptr, nullptr);
 }
 
 extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg, const double* x_trg,
                                                const int64_t* trg_node, const int64_t* row_ptr,
-                                               const int32_t* panel_idx, int64_t n_panels, int ns,
+                                               const int32_t* panel_idx, int64_t n_panels, const int32_t* panel_ns,
                                                const int32_t* panel_nt, const double* y_coarse,
                                                const double* eta_panel, int order, double beta, double* blocks,
                                                cudaStream_t s) {
-    slb_status c = nearquad_check(kernel, n_trg, ns, order, beta);
+    slb_status c = nearquad_check(kernel, n_trg, 2, order, beta);
     if (c != SLB_OK) return c;
     if (n_trg == 0) return SLB_OK;
-    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks && panel_nt && n_panels > 0, SLB_ERR_INVALID_ARG,
-                "null pointer");
+    SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks && panel_nt && panel_ns && n_panels > 0,
+                SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
     const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
     std::vector<int64_t> c0(n_panels + 1, 0);
-    int ntmax = 0;
+    int ntmax = 0, nsmax = 0;
     for (int64_t k = 0; k < n_panels; ++k) {
-        SLB_REQUIRE(panel_nt[k] >= 4 && panel_nt[k] % 2 == 0, SLB_ERR_INVALID_ARG, "bad panel_nt");
-        SLB_REQUIRE(panel_nt[k] <= kMaxNtQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
-        c0[k + 1] = c0[k] + (int64_t)ns * panel_nt[k];
+        SLB_REQUIRE(panel_nt[k] >= 4 && panel_nt[k] % 2 == 0 && panel_ns[k] >= 2, SLB_ERR_INVALID_ARG,
+                    "bad panel orders");
+        SLB_REQUIRE(panel_nt[k] <= kMaxNtQ && panel_ns[k] <= kMaxNsQ, SLB_ERR_UNSUPPORTED,
+                    "panel grid too large for nearquad");
+        c0[k + 1] = c0[k] + (int64_t)panel_ns[k] * panel_nt[k];
         ntmax = std::max(ntmax, (int)panel_nt[k]);
+        nsmax = std::max(nsmax, (int)panel_ns[k]);
     }
     int64_t nnz = 0;
     SLB_CUDA(cudaStreamSynchronize(s));
@@ -506,10 +593,11 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
         SLB_REQUIRE(pk[p] >= 0 && pk[p] < n_panels, SLB_ERR_INVALID_ARG, "panel_idx entry outside [0, n_panels)");
         bo[p + 1] = bo[p] + (int64_t)TD * (c0[pk[p] + 1] - c0[pk[p]]) * TD;
     }
-    int32_t* pnt_d = nullptr;
+    int32_t *pnt_d = nullptr, *pns_d = nullptr;
     int64_t *c0_d = nullptr, *bo_d = nullptr;
-    auto cleanup = [&]() { cudaFree(pnt_d); cudaFree(c0_d); cudaFree(bo_d); };
+    auto cleanup = [&]() { cudaFree(pnt_d); cudaFree(pns_d); cudaFree(c0_d); cudaFree(bo_d); };
     if (cudaMalloc(&pnt_d, sizeof(int32_t) * n_panels) != cudaSuccess ||
+        cudaMalloc(&pns_d, sizeof(int32_t) * n_panels) != cudaSuccess ||
         cudaMalloc(&c0_d, sizeof(int64_t) * (n_panels + 1)) != cudaSuccess ||
         cudaMalloc(&bo_d, sizeof(int64_t) * (nnz + 1)) != cudaSuccess) {
         cleanup();
@@ -517,10 +605,11 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
         return SLB_ERR_OOM;
     }
     cudaMemcpy(pnt_d, panel_nt, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
+    cudaMemcpy(pns_d, panel_ns, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
     cudaMemcpy(c0_d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
     cudaMemcpy(bo_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice);
-    slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, ntmax, y_coarse, eta_panel,
-                                order, beta, blocks, s, pnt_d, c0_d, bo_d);
+    slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse, eta_panel,
+                                order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d);
     cudaStreamSynchronize(s);
     cleanup();
     return r;

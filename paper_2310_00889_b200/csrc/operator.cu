@@ -129,12 +129,12 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     op->sdim = op->tdim = (d->kernel == SLB_LAPLACE_DL) ? 1 : 3;
     if (d->kernel == SLB_LAPLACE_DL) op->kind = FAR_LAPLACE;
     else op->kind = (d->eta_fine || d->eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL;
-    op->ragged = d->panel_nt || d->panel_mt;
+    op->ragged = d->panel_nt || d->panel_mt || d->panel_ns || d->panel_ms;
     if (op->ragged) {
-        // (NEXT N4) per-panel angular orders: node offsets and one interpolation bucket per (nt, mt)
-        if (!(d->panel_nt && d->panel_mt)) {
+        // (NEXT N4) per-panel orders: node offsets and one interpolation bucket per (ns, nt, ms, mt)
+        if (!d->panel_nt != !d->panel_mt || !d->panel_ns != !d->panel_ms) {
             free_op(op);
-            set_error("slb_operator_create: panel_nt and panel_mt must both be given (or both NULL)");
+            set_error("slb_operator_create: panel_nt/panel_mt and panel_ns/panel_ms come in pairs");
             return SLB_ERR_INVALID_ARG;
         }
         const int64_t P = d->n_panels_global;
@@ -142,23 +142,29 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         op->fn0.assign(P + 1, 0);
         std::vector<int32_t> pb(P);
         for (int64_t k = 0; k < P; ++k) {
-            const int nt = d->panel_nt[k], mt = d->panel_mt[k];
-            if (!(nt >= 2 && nt % 2 == 0 && mt >= 2 && nt <= SLB_MAX_NT && mt <= SLB_MAX_MT)) {
+            const int nt = d->panel_nt ? d->panel_nt[k] : d->nt, mt = d->panel_mt ? d->panel_mt[k] : d->mt;
+            const int ns = d->panel_ns ? d->panel_ns[k] : d->ns, ms = d->panel_ms ? d->panel_ms[k] : d->ms;
+            if (!(nt >= 2 && nt % 2 == 0 && mt >= 2 && nt <= SLB_MAX_NT && mt <= SLB_MAX_MT && ns >= 1 && ms >= 1 &&
+                  ns <= SLB_MAX_NS && ms <= SLB_MAX_MS)) {
                 free_op(op);
-                set_error("slb_operator_create: panel orders must be even and within the compiled limits");
+                set_error("slb_operator_create: panel orders must be positive (N_th even) and within the compiled limits");
                 return SLB_ERR_INVALID_ARG;
             }
-            op->cn0[k + 1] = op->cn0[k] + (int64_t)d->ns * nt;
-            op->fn0[k + 1] = op->fn0[k] + (int64_t)d->ms * mt;
-            op->max_cols = std::max(op->max_cols, d->ns * nt * op->sdim);
+            op->cn0[k + 1] = op->cn0[k] + (int64_t)ns * nt;
+            op->fn0[k + 1] = op->fn0[k] + (int64_t)ms * mt;
+            op->max_cols = std::max(op->max_cols, ns * nt * op->sdim);
             int b = 0;
-            while (b < (int)op->buckets.size() && !(op->buckets[b].nt == nt && op->buckets[b].mt == mt)) ++b;
+            while (b < (int)op->buckets.size() && !(op->buckets[b].nt == nt && op->buckets[b].mt == mt &&
+                                                    op->buckets[b].ns == ns && op->buckets[b].ms == ms))
+                ++b;
             if (b == (int)op->buckets.size()) {
                 op->buckets.emplace_back();
                 slb_operator::Bucket& nb = op->buckets.back();
                 nb.nt = nt;
                 nb.mt = mt;
-                if (!make_interp(d->ns, nt, d->ms, mt, &nb.ip, &nb.ip_buf)) {
+                nb.ns = ns;
+                nb.ms = ms;
+                if (!make_interp(ns, nt, ms, mt, &nb.ip, &nb.ip_buf)) {
                     free_op(op);
                     set_error("slb_operator_create: interpolation matrices: allocation failed");
                     return SLB_ERR_OOM;
@@ -192,11 +198,11 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
             cudaMemcpy(op->lc0_d, lc.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
             cudaMemcpy(op->lf0_d, lf.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
             cudaMemcpy(op->pbucket_d, pb.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice);
-            for (auto& b : op->buckets) {
+            for (int bi = 0; bi < (int)op->buckets.size(); ++bi) {
+                auto& b = op->buckets[bi];
                 std::vector<int32_t> pl;
                 for (int64_t q = 0; q < Pl; ++q)
-                    if (d->panel_nt[d->panel_begin + q] == b.nt && d->panel_mt[d->panel_begin + q] == b.mt)
-                        pl.push_back((int32_t)q);
+                    if (pb[d->panel_begin + q] == bi) pl.push_back((int32_t)q);
                 if (pl.empty()) continue;
                 okm = okm && cudaMalloc(&b.plist_d, sizeof(int32_t) * pl.size()) == cudaSuccess;
                 if (okm) cudaMemcpy(b.plist_d, pl.data(), sizeof(int32_t) * pl.size(), cudaMemcpyHostToDevice);
@@ -223,7 +229,9 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     op->plan = far_plan(op->M);
     {
         const char* e = getenv("SLB_FAR_PATH");
-        op->use_const = e ? (std::string(e) == "const") : (op->M >= (int64_t(1) << 19));
+        // constant-bank path from M = 2^16 (measured: c3 far 7.15 vs 7.63 ms, c3v 9.05 vs 9.80 ms on the
+        // TMA path); the choice depends on M only, so every rank of a sharded operator takes the same path
+        op->use_const = e ? (std::string(e) == "const") : (op->M >= (int64_t(1) << 16));
         if (op->use_const) op->plan.n_chunks = far_const_bufs();
     }
     if (d->n_on_local > op->N_loc) {
@@ -305,6 +313,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         std::vector<int64_t> bo(nnz + 1, 0);
         for (int64_t p = 0; p < nnz; ++p)
             bo[p + 1] = bo[p] + (int64_t)op->tdim * (op->cn0[pk[p] + 1] - op->cn0[pk[p]]) * op->sdim;
+        op->blk_total = bo[nnz];
         OPCUDA(cudaMalloc(&op->boff_d, sizeof(int64_t) * (nnz + 1)));
         OPCUDA(cudaMemcpy(op->boff_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice));
     }
@@ -376,7 +385,9 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     if (T > 0) {
         int64_t nnz = 0;
         OPCUDA(cudaMemcpy(&nnz, d->row_ptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost));
-        op->near_G = near_group_size(T, nnz);
+        const double bb = op->ragged ? (nnz ? op->blk_total * 8.0 / (double)nnz : 0.0)
+                                     : (double)op->tdim * op->cols * 8.0;
+        op->near_G = near_group_size(T, nnz, bb);
     }
     if (op->use_const) {
         OPCUDA(cudaMalloc(&op->rec, sizeof(double) * op->M * 10));

@@ -108,7 +108,7 @@ struct slb_operator {
     int64_t* boff_d = nullptr;          // [nnz+1] block offsets (doubles)
     int32_t* pbucket_d = nullptr;       // [P_global] bucket of each panel
     struct Bucket {
-        int nt, mt;
+        int nt, mt, ns, ms;
         slb::InterpParams ip;
         int64_t n_loc = 0;              // local panels in this bucket
         int32_t* plist_d = nullptr;     // their local panel ids
@@ -116,5 +116,6 @@ struct slb_operator {
     };
     std::vector<Bucket> buckets;
     int max_cols = 0;                   // widest block (nodes * sdim)
+    int64_t blk_total = 0;              // doubles in all local blocks (ragged)
 };
 

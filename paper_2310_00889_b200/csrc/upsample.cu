@@ -46,7 +46,8 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
                      const double* __restrict__ sc_in, double* __restrict__ sf_out,
                      const double* __restrict__ scale, double* __restrict__ dyn,
                      const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
-                     const int64_t* __restrict__ f_off) {
+                     const int64_t* __restrict__ f_off, int orows) {
+    // orows: output rows (a) staged in O at a time (msp, or fewer multiples of 8 for very large grids)
     extern __shared__ double sm[];
     const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
     const int nsp = rup(ns, 4), ntp = rup(nt, 4), msp = rup(ms, 8), mtp = rup(mt, 8);
@@ -59,7 +60,7 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
     double* F = Ps + msp * ldp;               // [mtp][ldf]
     double* raw = F + mtp * ldf;              // [ns][nt][nc] (rup to 2)
     double* T1 = raw + ((nin + 1) & ~1);      // [nsp][ld1]
-    double* O = T1 + nsp * ld1;               // [ms][mt][nc]
+    double* O = T1 + nsp * ld1;               // [orows][mt][nc]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const double* V = ip.vg ? ip.vg : ip.v;
@@ -102,37 +103,43 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
             }
         }
         __syncthreads();
-        // step 2: O[a][(b,c)] = sum_i Ps[a][i] T1[i][(b,c)]
-        for (int tile = warp; tile < nt2; tile += nwarps) {
-            const int a0 = (tile / (ncol2p / 8)) * 8, n0 = (tile % (ncol2p / 8)) * 8;
-            double d0 = 0.0, d1 = 0.0;
-            for (int k0 = 0; k0 < nsp; k0 += 4)
-                dmma_8x8x4(d0, d1, Ps[(a0 + g) * ldp + k0 + tq], T1[(k0 + tq) * ld1 + n0 + g]);
-            const int a = a0 + g;
-            if (a >= ms) continue;
-            const int col = n0 + 2 * tq;
-            if (col < ncol2) O[a * ncol2 + col] = d0;
-            if (col + 1 < ncol2) O[a * ncol2 + col + 1] = d1;
-        }
-        __syncthreads();
-        // epilogue: whole 32-byte source records {g, 0} per fine node (coalesced), or the plain values
-        if (dyn) {
-            double2* D2 = reinterpret_cast<double2*>(dyn);
-            for (int e = threadIdx.x; e < nout; e += blockDim.x) {
-                const int64_t m = m0 + e;
-                double v0, v1, v2;
-                if (kind == FAR_LAPLACE) {
-                    const double v = O[e];
-                    v0 = scale[3 * m] * v; v1 = scale[3 * m + 1] * v; v2 = scale[3 * m + 2] * v;
-                } else {
-                    const double sc = scale[m];
-                    v0 = sc * O[3 * e]; v1 = sc * O[3 * e + 1]; v2 = sc * O[3 * e + 2];
-                }
-                D2[2 * m] = make_double2(v0, v1);
-                D2[2 * m + 1] = make_double2(v2, 0.0);
+        // step 2: O[a][(b,c)] = sum_i Ps[a][i] T1[i][(b,c)], orows output rows at a time
+        for (int ac = 0; ac < msp; ac += orows) {
+            const int ntc = (min(orows, msp - ac) / 8) * (ncol2p / 8);
+            for (int tile = warp; tile < ntc; tile += nwarps) {
+                const int a0 = ac + (tile / (ncol2p / 8)) * 8, n0 = (tile % (ncol2p / 8)) * 8;
+                double d0 = 0.0, d1 = 0.0;
+                for (int k0 = 0; k0 < nsp; k0 += 4)
+                    dmma_8x8x4(d0, d1, Ps[(a0 + g) * ldp + k0 + tq], T1[(k0 + tq) * ld1 + n0 + g]);
+                const int a = a0 + g;
+                if (a >= ms) continue;
+                const int col = n0 + 2 * tq;
+                if (col < ncol2) O[(a - ac) * ncol2 + col] = d0;
+                if (col + 1 < ncol2) O[(a - ac) * ncol2 + col + 1] = d1;
             }
-        } else {
-            for (int e = threadIdx.x; e < nout * nc; e += blockDim.x) sf_out[m0 * nc + e] = O[e];
+            __syncthreads();
+            // epilogue: whole 32-byte source records {g, 0} per fine node (coalesced), or the plain values
+            const int e0 = ac * mt, e1 = min(ac + orows, ms) * mt;
+            if (dyn) {
+                double2* D2 = reinterpret_cast<double2*>(dyn);
+                for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+                    const int64_t m = m0 + e;
+                    const int eo = e - e0;
+                    double v0, v1, v2;
+                    if (kind == FAR_LAPLACE) {
+                        const double v = O[eo];
+                        v0 = scale[3 * m] * v; v1 = scale[3 * m + 1] * v; v2 = scale[3 * m + 2] * v;
+                    } else {
+                        const double sc = scale[m];
+                        v0 = sc * O[3 * eo]; v1 = sc * O[3 * eo + 1]; v2 = sc * O[3 * eo + 2];
+                    }
+                    D2[2 * m] = make_double2(v0, v1);
+                    D2[2 * m + 1] = make_double2(v2, 0.0);
+                }
+            } else {
+                for (int e = e0 * nc + threadIdx.x; e < e1 * nc; e += blockDim.x) sf_out[m0 * nc + e] = O[e - e0 * nc];
+            }
+            __syncthreads();
         }
     }
 }
@@ -147,8 +154,13 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     const int ncol2p = rup_h(ip.mt * nc, 8);
     const int ldp = ld_g(nsp), ldf = ld_g(ntp), ld1 = ld_t(ncol2p);
     const int nin = ip.ns * ip.nt * nc;
-    const size_t smem = sizeof(double) * ((size_t)msp * ldp + (size_t)mtp * ldf + (size_t)((nin + 1) & ~1) +
-                                          (size_t)nsp * ld1 + (size_t)ip.ms * ip.mt * nc);
+    auto smem_of = [&](int orows) {
+        return sizeof(double) * ((size_t)msp * ldp + (size_t)mtp * ldf + (size_t)((nin + 1) & ~1) +
+                                 (size_t)nsp * ld1 + (size_t)orows * ip.mt * nc);
+    };
+    int orows = msp;
+    while (orows > 8 && smem_of(orows) > 227 * 1024) orows -= 8;
+    const size_t smem = smem_of(orows);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "upsample: grid too large for shared memory");
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
@@ -158,7 +170,7 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     // one panel per CTA and pass; enough CTAs for every SM to hold several
     const unsigned grid = (unsigned)std::min<int64_t>(n_panels, (int64_t)num_sms() * 16);
     upsample_dmma_kernel<<<grid, kUpWarps * 32, smem, s>>>((int)kind, nc, n_panels, ip, sigma_coarse, sigma_fine, sc,
-                                                           dyn, plist, c_off, f_off);
+                                                           dyn, plist, c_off, f_off, orows);
     ++g_launch_count;
     return check_launch("upsample_dmma_kernel");
 }

@@ -38,14 +38,15 @@ def S():
 
 
 @pytest.mark.parametrize("nc", [1, 3])
-def test_upsample_ragged_parity(S, nc):
+@pytest.mark.parametrize("ragged_ns", [False, True])
+def test_upsample_ragged_parity(S, nc, ragged_ns):
     rng = np.random.default_rng(5 + nc)
     nts = rng.choice([4, 8, 12, 20, 40, 64], size=37).astype(np.int32)
-    mts = 2 * nts
-    ns, ms = 10, 20
-    sc = rng.standard_normal(int(ns * nts.sum()) * nc)
-    g = S.slb_upsample_ragged(cu(sc), ns, nts, ms, mts, nc).cpu().numpy()
-    ref = O.upsample_ragged(sc, ns, nts, ms, mts, nc)
+    nss = rng.choice([4, 10, 12, 16], size=37).astype(np.int32) if ragged_ns else np.full(37, 10, np.int32)
+    mts, mss = 2 * nts, 2 * nss
+    sc = rng.standard_normal(int((nss.astype(np.int64) * nts).sum()) * nc)
+    g = S.slb_upsample_ragged(cu(sc), nss, nts, mss, mts, nc).cpu().numpy()
+    ref = O.upsample_ragged(sc, nss, nts, mss, mts, nc)
     assert rel(g, ref) <= TOL
 
 
@@ -65,7 +66,7 @@ def _vs_oracle(pr, rows=None, **kw):
 def test_matvec_ragged_parity_small(S, kw, path, monkeypatch):
     monkeypatch.setenv("SLB_FAR_PATH", path)
     pr = make_config("c3v", **kw)
-    assert pr.ragged and len(set(pr.panel_nt.tolist())) > 1
+    assert pr.ragged and len(set(pr.panel_nt.tolist())) > 1 and len(set(pr.ns_of_panel().tolist())) > 1
     err, u, u2 = _vs_oracle(pr)
     assert err <= TOL, err
     assert np.array_equal(u, u2)
