@@ -158,7 +158,8 @@ slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, 
                            double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
                            cudaEvent_t fork, cudaEvent_t* join, int64_t* launches);
 slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s);
-int far_const_bufs();
+int far_const_bufs(int64_t M);   // streams / partial arrays for M sources
+int far_const_tile(int64_t M);   // sources per constant-bank tile
 slb_status far_const_prepare();
 
 // ---- packing kernels (farfield.cu) ----

@@ -9,11 +9,11 @@
 // from 61 to 55 cycles per warp and the measured pair rate rises ~8% (tools/const_probe.cu).
 //
 // Structure: the packed source records rec[m] = {y(3), a(3), g(3), 0} (80 B) are split into
-// tiles of kConstTile = 200 sources.  Tile i is copied (D2D, stream-ordered) into constant buffer
-// i % 4 and processed by a launch on internal stream i % 4 over ALL local targets; stream s
-// accumulates its tiles s, s+4, s+8, ... into its own partial array, so the summation order per
-// target depends only on M and the four kernels in flight hide each other's tails.  The whole
-// sequence is captured once into a CUDA graph per operator and replayed per apply.
+// tiles of 200 sources (100 below 2^19 sources).  Tile i is copied (D2D, stream-ordered) into
+// constant buffer i % nb (nb = 4, or 8) and processed by a launch on internal stream i % nb over ALL
+// local targets; stream s accumulates its tiles s, s+nb, ... into its own partial array, so the
+// summation order per target depends only on M and the nb kernels in flight hide each other's
+// tails.  The whole sequence is captured once into a CUDA graph per operator and replayed per apply.
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <vector>
@@ -21,12 +21,18 @@
 
 namespace slb {
 
-constexpr int kConstTile = 200;          // sources per constant buffer (200 x 80 B = 16 KB)
-constexpr int kConstBufs = 4;            // buffers = streams = partial arrays
+constexpr int kConstRecs = 800;          // records the constant bank holds (800 x 80 B = 64 KB)
+constexpr int kMaxConstBufs = 8;         // buffers = streams = partial arrays: 4 x 200 or 8 x 100 records
 constexpr int kRec = 10;                 // doubles per packed record
 constexpr int kConstThreads = 128;
+constexpr int kSlot = kConstRecs / kMaxConstBufs * kRec;   // doubles per 1/8 of the bank
 
-__constant__ double c_rec[kConstBufs][kConstTile * kRec];
+__constant__ double c_rec[kConstRecs * kRec];
+
+// buffers for M sources (a function of M only: every rank of a sharded operator sums in the same
+// order).  8 x 100 below 2^19 sources: with few local targets (c3: 30 k) 4 launches of T/256 CTAs
+// do not fill 148 SMs x 4 CTAs, 8 do.
+static int const_bufs_for(int64_t M) { return M < (int64_t(1) << 19) ? 8 : 4; }
 
 template <int KIND, int J, int CM>
 __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const double* s, double (&acc)[J][3],
@@ -87,7 +93,7 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
     }
     bool anyz = false;
     unsigned zc0 = 0;
-    const double* base = c_rec[BUF];
+    const double* base = c_rec + BUF * kSlot;     // BUF: buffer offset in eighths of the bank
 #pragma unroll UNR
     for (int m = 0; m < n_src; ++m) const_pairs<KIND, J, CM>(x, base + kRec * m, acc, anyz, zc0);
     if (CM == 1 && zc0) {
@@ -174,49 +180,55 @@ static void launch_tile(int64_t T, const double* x, int n, int first, double* pa
 }
 
 template <int KIND>
-static void launch_tile_buf(int buf, int64_t T, const double* x, int n, int first, double* part,
+static void launch_tile_buf(int slot, int64_t T, const double* x, int n, int first, double* part,
                             unsigned long long* zc, cudaStream_t s) {
-    switch (buf) {
+    switch (slot) {
         case 0: launch_tile<KIND, 0>(T, x, n, first, part, zc, s); break;
         case 1: launch_tile<KIND, 1>(T, x, n, first, part, zc, s); break;
         case 2: launch_tile<KIND, 2>(T, x, n, first, part, zc, s); break;
-        default: launch_tile<KIND, 3>(T, x, n, first, part, zc, s); break;
+        case 3: launch_tile<KIND, 3>(T, x, n, first, part, zc, s); break;
+        case 4: launch_tile<KIND, 4>(T, x, n, first, part, zc, s); break;
+        case 5: launch_tile<KIND, 5>(T, x, n, first, part, zc, s); break;
+        case 6: launch_tile<KIND, 6>(T, x, n, first, part, zc, s); break;
+        default: launch_tile<KIND, 7>(T, x, n, first, part, zc, s); break;
     }
 }
 
-// Issue the constant-bank far field on the 4 internal streams (forked from/joined to s).
-// partials: [kConstBufs][T][D].  Returns the number of kernel launches issued.
+// Issue the constant-bank far field on nb = const_bufs_for(M) internal streams (forked from/joined to s).
+// partials: [nb][T][D].  Returns the number of kernel launches issued.
 slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
                            double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
                            cudaEvent_t fork, cudaEvent_t* join, int64_t* launches) {
     const int D = (kind == FAR_LAPLACE) ? 1 : 3;
+    const int nb = const_bufs_for(M);
+    const int tile = kConstRecs / nb;                // 200 or 100 records per buffer
+    const int stride = kMaxConstBufs / nb;           // buffer b occupies eighth b * stride
     *launches = 0;
     SLB_CUDA(cudaEventRecord(fork, s));
-    for (int b = 0; b < kConstBufs; ++b) SLB_CUDA(cudaStreamWaitEvent(ws[b], fork, 0));
-    const int64_t ntiles = (M + kConstTile - 1) / kConstTile;
-    for (int b = 0; b < kConstBufs; ++b) {
+    for (int b = 0; b < nb; ++b) SLB_CUDA(cudaStreamWaitEvent(ws[b], fork, 0));
+    const int64_t ntiles = (M + tile - 1) / tile;
+    for (int b = 0; b < nb; ++b) {
         double* part = partials + (int64_t)b * T * D;
         if (b >= ntiles && T > 0) SLB_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * T * D, ws[b]));
     }
     for (int64_t i = 0; i < ntiles; ++i) {
-        const int b = (int)(i % kConstBufs);
-        const int64_t m0 = i * kConstTile;
-        const int n = (int)std::min<int64_t>(kConstTile, M - m0);
+        const int b = (int)(i % nb);
+        const int64_t m0 = i * tile;
+        const int n = (int)std::min<int64_t>(tile, M - m0);
         SLB_CUDA(cudaMemcpyToSymbolAsync(c_rec, rec + m0 * kRec, sizeof(double) * n * kRec,
-                                         sizeof(double) * (size_t)b * kConstTile * kRec, cudaMemcpyDeviceToDevice,
-                                         ws[b]));
+                                         sizeof(double) * (size_t)b * stride * kSlot, cudaMemcpyDeviceToDevice, ws[b]));
         if (T > 0) {
             double* part = partials + (int64_t)b * T * D;
-            const int first = (i < kConstBufs) ? 1 : 0;
+            const int first = (i < nb) ? 1 : 0;
             switch (kind) {
-                case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b, T, x, n, first, part, zc, ws[b]); break;
-                case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b, T, x, n, first, part, zc, ws[b]); break;
-                default: launch_tile_buf<FAR_LAPLACE>(b, T, x, n, first, part, zc, ws[b]); break;
+                case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
+                case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
+                default: launch_tile_buf<FAR_LAPLACE>(b * stride, T, x, n, first, part, zc, ws[b]); break;
             }
             ++*launches;
         }
     }
-    for (int b = 0; b < kConstBufs; ++b) {
+    for (int b = 0; b < nb; ++b) {
         SLB_CUDA(cudaEventRecord(join[b], ws[b]));
         SLB_CUDA(cudaStreamWaitEvent(s, join[b], 0));
     }
@@ -230,7 +242,8 @@ slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, doub
     return check_launch("pack_rec_kernel");
 }
 
-int far_const_bufs() { return kConstBufs; }
+int far_const_bufs(int64_t M) { return const_bufs_for(M); }
+int far_const_tile(int64_t M) { return kConstRecs / const_bufs_for(M); }
 
 // Load this module's kernels and constant symbol eagerly (lazy module loading must not happen
 // inside a stream capture).
@@ -241,7 +254,11 @@ slb_status far_const_prepare() {
 #define PREP1(K, C) SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 0, C>)); \
     SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 1, C>));                 \
     SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 2, C>));                 \
-    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 3, C>));
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 3, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 4, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 5, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 6, C>));                 \
+    SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 7, C>));
 #define PREP(K) PREP1(K, 0) PREP1(K, 1)
     PREP(FAR_STOKES_SLDL)
     PREP(FAR_STOKES_DL)

@@ -232,7 +232,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         // constant-bank path from M = 2^16 (measured: c3 far 7.15 vs 7.63 ms, c3v 9.05 vs 9.80 ms on the
         // TMA path); the choice depends on M only, so every rank of a sharded operator takes the same path
         op->use_const = e ? (std::string(e) == "const") : (op->M >= (int64_t(1) << 16));
-        if (op->use_const) op->plan.n_chunks = far_const_bufs();
+        if (op->use_const) op->plan.n_chunks = far_const_bufs(op->M);
     }
     if (d->n_on_local > op->N_loc) {
         free_op(op);
@@ -414,7 +414,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
             op->graph = nullptr;
             cudaGetLastError();            // clear the capture error; fall back to direct issue
         }
-        op->const_launches = (T > 0) ? (op->M + 199) / 200 : 0;
+        op->const_launches = (T > 0) ? (op->M + far_const_tile(op->M) - 1) / far_const_tile(op->M) : 0;
     }
     OPCUDA(cudaDeviceSynchronize());
     OPST(check_launch("slb_operator_create"));

@@ -93,8 +93,8 @@ struct slb_operator {
     // constant-bank far field (large M): packed records, 4 worker streams, captured graph
     bool use_const = false;
     double* rec = nullptr;              // [M][10]
-    cudaStream_t ws[4] = {nullptr, nullptr, nullptr, nullptr};
-    cudaEvent_t fork = nullptr, join[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t ws[8] = {};
+    cudaEvent_t fork = nullptr, join[8] = {};
     cudaGraphExec_t graph = nullptr;
     int64_t const_launches = 0;
     int near_G = 1;                     // targets per warp in the near stream kernel
