@@ -9,8 +9,8 @@
 // from 61 to 55 cycles per warp and the measured pair rate rises ~8% (tools/const_probe.cu).
 //
 // Structure: the packed source records rec[m] = {y(3), a(3), g(3), 0} (80 B) are split into
-// tiles of 200 sources (100 below 2^19 sources).  Tile i is copied (D2D, stream-ordered) into
-// constant buffer i % nb (nb = 4, or 8) and processed by a launch on internal stream i % nb over ALL
+// tiles of 200 sources.  Tile i is copied (D2D, stream-ordered) into constant buffer i % nb
+// (nb = 4; the bank can also be split 8 x 100) and processed by a launch on internal stream i % nb over ALL
 // local targets; stream s accumulates its tiles s, s+nb, ... into its own partial array, so the
 // summation order per target depends only on M and the nb kernels in flight hide each other's
 // tails.  The whole sequence is captured once into a CUDA graph per operator and replayed per apply.
@@ -30,9 +30,9 @@ constexpr int kSlot = kConstRecs / kMaxConstBufs * kRec;   // doubles per 1/8 of
 __constant__ double c_rec[kConstRecs * kRec];
 
 // buffers for M sources (a function of M only: every rank of a sharded operator sums in the same
-// order).  8 x 100 below 2^19 sources: with few local targets (c3: 30 k) 4 launches of T/256 CTAs
-// do not fill 148 SMs x 4 CTAs, 8 do.
-static int const_bufs_for(int64_t M) { return M < (int64_t(1) << 19) ? 8 : 4; }
+// order).  8 x 100 records was measured too: slower on c3 / c3v (far 7.90 / 9.52 ms vs 7.33 / 9.05 ms
+// with 4 x 200) -- twice the launches and copies cost more than the better SM fill gains.
+static int const_bufs_for(int64_t M) { (void)M; return 4; }
 
 template <int KIND, int J, int CM>
 __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const double* s, double (&acc)[J][3],
