@@ -145,7 +145,8 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
  * (on-surface, singular) else -1 (may be NULL: all off-surface); eta_panel [n_panels] (Stokes
  * eta S + D; NULL for Laplace DL); order = GL points per cell direction (4..24), beta = accepted
  * distance / cell diameter.  blocks [nnz][tdim][ns*nt*sdim] written (unfolded B).  Synchronises s.
- * SLB_ERR_UNSUPPORTED if a target is too close for the cell budget. */
+ * SLB_ERR_UNSUPPORTED if a target is too close for the cell budget, or if a panel's working set
+ * exceeds shared memory (Stokes: N_s N_th <= 1024, e.g. 16 x 64). */
 slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
                              const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
                              const double* y_coarse, const double* eta_panel, int order, double beta,

@@ -46,8 +46,9 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
                      const double* __restrict__ sc_in, double* __restrict__ sf_out,
                      const double* __restrict__ scale, double* __restrict__ dyn,
                      const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
-                     const int64_t* __restrict__ f_off, int orows) {
-    // orows: output rows (a) staged in O at a time (msp, or fewer multiples of 8 for very large grids)
+                     const int64_t* __restrict__ f_off, int orows, int gmats) {
+    // orows: output rows (a) staged in O at a time (msp, or fewer multiples of 8 for very large grids);
+    // gmats: read P_s and F_th from the (L1-cached) global copy instead of shared memory (largest grids)
     extern __shared__ double sm[];
     const int ns = ip.ns, nt = ip.nt, ms = ip.ms, mt = ip.mt;
     const int nsp = rup(ns, 4), ntp = rup(nt, 4), msp = rup(ms, 8), mtp = rup(mt, 8);
@@ -56,22 +57,31 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
     const int ldp = ld_g(nsp), ldf = ld_g(ntp), ld1 = ld_t(ncol2p);
     const int nin = ns * nt * nc;
     const int nout = ms * mt;
-    double* Ps = sm;                          // [msp][ldp]
-    double* F = Ps + msp * ldp;               // [mtp][ldf]
-    double* raw = F + mtp * ldf;              // [ns][nt][nc] (rup to 2)
+    double* Ps = sm;                          // [msp][ldp]   (absent when gmats)
+    double* F = Ps + (gmats ? 0 : msp * ldp); // [mtp][ldf]   (absent when gmats)
+    double* raw = F + (gmats ? 0 : mtp * ldf);// [ns][nt][nc] (rup to 2)
     double* T1 = raw + ((nin + 1) & ~1);      // [nsp][ld1]
     double* O = T1 + nsp * ld1;               // [orows][mt][nc]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const double* V = ip.vg ? ip.vg : ip.v;
-    for (int q = threadIdx.x; q < msp * ldp; q += blockDim.x) {
-        const int a = q / ldp, i = q % ldp;
-        Ps[q] = (a < ms && i < ns) ? V[a * ns + i] : 0.0;
+    if (!gmats) {
+        for (int q = threadIdx.x; q < msp * ldp; q += blockDim.x) {
+            const int a = q / ldp, i = q % ldp;
+            Ps[q] = (a < ms && i < ns) ? V[a * ns + i] : 0.0;
+        }
+        for (int q = threadIdx.x; q < mtp * ldf; q += blockDim.x) {
+            const int b = q / ldf, j = q % ldf;
+            F[q] = (b < mt && j < nt) ? V[ms * ns + b * nt + j] : 0.0;
+        }
     }
-    for (int q = threadIdx.x; q < mtp * ldf; q += blockDim.x) {
-        const int b = q / ldf, j = q % ldf;
-        F[q] = (b < mt && j < nt) ? V[ms * ns + b * nt + j] : 0.0;
-    }
+    // fragment loaders: F[b][j] and Ps[a][i], zero outside the matrices
+    auto Fv = [&](int b, int j) -> double {
+        return gmats ? ((b < mt && j < nt) ? __ldg(V + ms * ns + b * nt + j) : 0.0) : F[b * ldf + j];
+    };
+    auto Pv = [&](int a, int i) -> double {
+        return gmats ? ((a < ms && i < ns) ? __ldg(V + a * ns + i) : 0.0) : Ps[a * ldp + i];
+    };
     const int g = lane >> 2, tq = lane & 3;   // fragment coordinates
     const int nt1 = (rowsp / 8) * (mtp / 8);  // step-1 tiles
     const int nt2 = (msp / 8) * (ncol2p / 8); // step-2 tiles
@@ -93,7 +103,7 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
             for (int k0 = 0; k0 < ntp; k0 += 4) {
                 const int j = k0 + tq;
                 const double av = (rb >= 0 && j < nt) ? raw[rb + j * nc] : 0.0;
-                dmma_8x8x4(d0, d1, av, F[(n0 + g) * ldf + k0 + tq]);
+                dmma_8x8x4(d0, d1, av, Fv(n0 + g, k0 + tq));
             }
             if (r < rows) {
                 const int i = r / nc, c = r % nc;
@@ -110,7 +120,7 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
                 const int a0 = ac + (tile / (ncol2p / 8)) * 8, n0 = (tile % (ncol2p / 8)) * 8;
                 double d0 = 0.0, d1 = 0.0;
                 for (int k0 = 0; k0 < nsp; k0 += 4)
-                    dmma_8x8x4(d0, d1, Ps[(a0 + g) * ldp + k0 + tq], T1[(k0 + tq) * ld1 + n0 + g]);
+                    dmma_8x8x4(d0, d1, Pv(a0 + g, k0 + tq), T1[(k0 + tq) * ld1 + n0 + g]);
                 const int a = a0 + g;
                 if (a >= ms) continue;
                 const int col = n0 + 2 * tq;
@@ -154,13 +164,18 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     const int ncol2p = rup_h(ip.mt * nc, 8);
     const int ldp = ld_g(nsp), ldf = ld_g(ntp), ld1 = ld_t(ncol2p);
     const int nin = ip.ns * ip.nt * nc;
-    auto smem_of = [&](int orows) {
-        return sizeof(double) * ((size_t)msp * ldp + (size_t)mtp * ldf + (size_t)((nin + 1) & ~1) +
+    auto smem_of = [&](int orows, int gm) {
+        return sizeof(double) * ((gm ? 0 : (size_t)msp * ldp + (size_t)mtp * ldf) + (size_t)((nin + 1) & ~1) +
                                  (size_t)nsp * ld1 + (size_t)orows * ip.mt * nc);
     };
-    int orows = msp;
-    while (orows > 8 && smem_of(orows) > 227 * 1024) orows -= 8;
-    const size_t smem = smem_of(orows);
+    int orows = msp, gmats = 0;
+    while (orows > 8 && smem_of(orows, 0) > 227 * 1024) orows -= 8;
+    if (smem_of(orows, 0) > 227 * 1024) {           // largest grids: matrices from global memory
+        gmats = 1;
+        orows = msp;
+        while (orows > 8 && smem_of(orows, 1) > 227 * 1024) orows -= 8;
+    }
+    const size_t smem = smem_of(orows, gmats);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "upsample: grid too large for shared memory");
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
@@ -170,7 +185,7 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     // one panel per CTA and pass; enough CTAs for every SM to hold several
     const unsigned grid = (unsigned)std::min<int64_t>(n_panels, (int64_t)num_sms() * 16);
     upsample_dmma_kernel<<<grid, kUpWarps * 32, smem, s>>>((int)kind, nc, n_panels, ip, sigma_coarse, sigma_fine, sc,
-                                                           dyn, plist, c_off, f_off, orows);
+                                                           dyn, plist, c_off, f_off, orows, gmats);
     ++g_launch_count;
     return check_launch("upsample_dmma_kernel");
 }

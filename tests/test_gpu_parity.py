@@ -284,3 +284,46 @@ def test_operator_rejects_bad_csr(S):
         Operator(row_ptr=cu(rp2, torch.int64), panel_idx=cu(pr.panel_idx, torch.int32), **kw)
     with pytest.raises(SlbError):
         S.slb_farfield_stokes_sldl(cu(pr.x_trg), cu(pr.y_f), cu(pr.n_f), cu(pr.w_f), cu(np.zeros((pr.M, 3))), eta=-1.0)
+
+
+# ------------------------------------------------------------------ edge cases: limits, empty operators
+@pytest.mark.parametrize("ns,nt,ms,mt", [(32, 64, 64, 128), (32, 2, 1, 2), (1, 2, 64, 128)])
+def test_upsample_compiled_limits(S, ns, nt, ms, mt):
+    """the largest grids the header allows (SLB_MAX_NS/NT/MS/MT) and degenerate 1-node / 2-angle
+    panels: interpolation matrices beyond the kernel-parameter budget live in a device buffer"""
+    rng = np.random.default_rng(ns + nt + ms)
+    P, nc = 3, 3
+    sc = rng.standard_normal(P * ns * nt * nc)
+    g = S.slb_upsample(cu(sc), P, ns, nt, ms, mt, nc).cpu().numpy()
+    assert rel(g, O.upsample(sc, P, ns, nt, ms, mt, nc).reshape(-1)) <= TOL
+
+
+def test_upsample_beyond_limits_rejected(S):
+    from paper_2310_00889_b200 import SlbError
+    with pytest.raises(SlbError, match="UNSUPPORTED"):
+        S.slb_upsample(cu(np.zeros(33 * 4)), 1, 33, 4, 66, 8, 1)
+
+
+def test_operator_without_targets(S):
+    """a rank may own sources but no targets (T_local = 0): the apply is a no-op that still runs"""
+    from paper_2310_00889_b200 import Operator
+    pr = make_config("c2", panels=4)
+    op = Operator(kernel=pr.kernel, ns=pr.Ns, nt=pr.Nt, ms=pr.Ms, mt=pr.Mt, n_panels_global=pr.P, panel_begin=0,
+                  panel_end=pr.P, x_trg=torch.zeros((0, 3), dtype=torch.float64, device="cuda"), n_on=0,
+                  y_fine=cu(pr.y_f), n_fine=cu(pr.n_f), w_fine=cu(pr.w_f),
+                  row_ptr=torch.zeros(1, dtype=torch.int64, device="cuda"),
+                  panel_idx=torch.zeros(1, dtype=torch.int32, device="cuda"),
+                  blocks=torch.zeros(2, dtype=torch.float64, device="cuda"), eta_fine=cu(pr.eta_f), c_identity=0.0)
+    u = op.matvec(cu(pr.sigma))
+    torch.cuda.synchronize()
+    assert u.shape == (0, 3)
+    op.close()
+
+
+def test_zero_density_gives_zero(S):
+    from harness import DeviceProblem
+    pr = make_config("c4", n_loops=2, panels=6)
+    dp = DeviceProblem(pr)
+    u = dp.matvec(cu(np.zeros_like(pr.sigma))).cpu().numpy()
+    dp.close()
+    assert np.all(u == 0.0)
