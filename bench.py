@@ -87,6 +87,16 @@ def setup_dist(args):
     return world, rank, local
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_run(pr, seconds_target=15.0, rows_n=None):
     """Time the oracle as it stands on a bounded row sample; extrapolate to one full apply."""
     import oracle
@@ -108,7 +118,8 @@ def cpu_baseline_run(pr, seconds_target=15.0, rows_n=None):
     orc.apply_rows(pr.sigma, rows, prepared=prep)
     t_rows = time.perf_counter() - t0
     t_full = t_prep + t_rows * pr.T / rows.size
-    return {"value": 1.0 / t_full, "unit": "matvec/s", "cores": thr, "kind": "oracle",
+    return {"value": 1.0 / t_full, "unit": "matvec/s", "cores": thr, "kind": "oracle", "cpu_model": _cpu_model(),
+            "nproc": os.cpu_count(),
             "sample": (f"{rows.size} of {pr.T} target rows of {pr.name} (full operator per row: far sum over "
                        f"{pr.M} fine sources + literal near correction + identity), plus the O(N) "
                        f"prepare (projector/upsample, {t_prep:.2f}s); extrapolated linearly in T"),
@@ -147,7 +158,7 @@ def run_reference(args, world, rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_info(pr, world, "n/a (CPU oracle)"),
             "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": res["cores"], "kind": "oracle",
-                             "sample": res["sample"]},
+                             "sample": res["sample"], "cpu_model": res.get("cpu_model"), "nproc": res.get("nproc")},
             "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

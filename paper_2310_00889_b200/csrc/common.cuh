@@ -190,6 +190,8 @@ struct RagNear {
     const int64_t* cn0 = nullptr;    // [P_global+1] first coarse node of each panel
     const int64_t* boff = nullptr;   // [nnz+1] first double of each block (CSR order)
     int max_cols = 0;                // largest nodes_per_panel * sdim
+    const int64_t* bmeta = nullptr;  // [nnz] (sigma double2 offset << 12) | (block width / 2): one
+                                     // independent load per block instead of panel_idx -> cn0
 };
 // fused finalize: u[t] = sum_c partials[c][t] + near(t) + c_id * sig_loc[t] (t < n_on) + Lsig[t]
 slb_status finalize_launch(const FarPlan& plan, int64_t n_trg, int tdim, int cols,

@@ -167,7 +167,8 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
                           const double* __restrict__ sigma_c, const double* __restrict__ partials, int64_t n_chunks,
                           int64_t n_on, double c_id, const double* __restrict__ sig_local,
                           const double* __restrict__ Lsig, double* __restrict__ u, int G,
-                          const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff, int sdim, int ucols2) {
+                          const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff, int sdim, int ucols2,
+                          const int64_t* __restrict__ bmeta) {
     // uniform panels (cn0 = boff = NULL): every block is TD x ucols2 double2
     extern __shared__ __align__(128) double2 ring[];      // [warps][STG][S]
     __shared__ __align__(8) uint64_t bars[kNearWarps * kNearStages];
@@ -207,9 +208,17 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
         for (int r = 0; r < TD; ++r) acc[r] = 0.0;
         const int64_t p1 = row_ptr[t + 1];
         for (int64_t p = row_ptr[t]; p < p1; ++p) {
-            const int64_t k = panel_idx[p];
-            const int ck = cn0 ? (int)((cn0[k + 1] - cn0[k]) * sdim / 2) : ucols2;
-            const double2* Sk = cn0 ? S2 + cn0[k] * sdim / 2 : S2 + k * (int64_t)ucols2;
+            int ck;
+            const double2* Sk;
+            if (bmeta) {
+                const int64_t bm = bmeta[p];
+                ck = (int)(bm & 4095);
+                Sk = S2 + (bm >> 12);
+            } else {
+                const int64_t k = panel_idx[p];
+                ck = cn0 ? (int)((cn0[k + 1] - cn0[k]) * sdim / 2) : ucols2;
+                Sk = cn0 ? S2 + cn0[k] * sdim / 2 : S2 + k * (int64_t)ucols2;
+            }
             const int len2 = TD * ck;
             for (int q0 = 0; q0 < len2; q0 += S, ++i) {
                 const int st = (int)(i % kNearStages);
@@ -260,9 +269,10 @@ near_stream_ragged_kernel(int64_t T, int S, const int64_t* __restrict__ row_ptr,
     }
 }
 
-// Chunked streaming for ragged blocks: slots of S <= kChunk2 double2 (measured on c3v: 800 double2
-// = 12.8 KB slots, one 4-warp CTA per SM, beat 576 with two CTAs per SM by 15 %).
-constexpr int kChunk2 = 800;
+// Chunked streaming for ragged blocks: slots of S <= kChunk2 double2.  Measured on c3v (blocks of
+// 10-74 KB): S = 320 (5 KB slots, 3 CTAs = 12 streaming warps per SM) 1.73 ms = 85 % of HBM;
+// 240: 1.89, 480: 1.96, 640: 2.78, 800: 2.75, 1152: 4.13 ms -- more warps per SM beat bigger copies.
+constexpr int kChunk2 = 320;
 
 static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_t* row_ptr, const int32_t* panel_idx,
                                      const double* blocks, const double* sigma_c, const double* partials,
@@ -271,7 +281,9 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
                                      int ucols = 0) {
     if (T <= 0) return SLB_OK;
     const int widest2 = tdim * (rag.boff ? rag.max_cols : ucols) / 2;
-    const int S = std::min(widest2, kChunk2);
+    static int chunk = -1;
+    if (chunk < 0) { const char* e = getenv("SLB_NEAR_CHUNK"); chunk = e ? std::max(64, atoi(e)) : kChunk2; }
+    const int S = std::min(widest2, chunk);
     const size_t smem = (size_t)kNearWarps * kNearStages * S * 16;
     G = std::max(1, G);
     const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
@@ -281,7 +293,7 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
         near_stream_ragged_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(                              \
             T, S, row_ptr, panel_idx, blocks, sigma_c, partials, n_chunks, n_on, c_id, sig_local, Lsig, u, G,  \
-            rag.cn0, rag.boff, tdim, ucols / 2);                                                              \
+            rag.cn0, rag.boff, tdim, ucols / 2, rag.bmeta);                                                   \
     } while (0)
     if (tdim == 1) {
         if (mode == 0) RAG_LAUNCH(1, 0); else RAG_LAUNCH(1, 1);
@@ -303,7 +315,12 @@ slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, c
                            const int64_t* row_ptr, const int32_t* panel_idx, const double* blocks,
                            const double* sigma_c_global, int64_t n_on, double c_id, const double* sig_local,
                            const double* Lsig, double* u, int G, cudaStream_t s, const RagNear& rag) {
-    if (rag.boff)
+    // uniform blocks wider than 600 double2 (c2: 11.5 KB, c3: 17 KB) also stream through the chunked
+    // kernel: c3 near 0.78 -> 0.62 ms, c2 0.150 -> 0.120 ms; c4/c5's 8.6 KB blocks stay on the plain
+    // ring (chunking them: c4 2.46 -> 2.84 ms)
+    static int chunk_uniform = -1;
+    if (chunk_uniform < 0) { const char* e = getenv("SLB_NEAR_CHUNKED_UNIFORM"); chunk_uniform = e ? atoi(e) : 600; }
+    if (rag.boff || (chunk_uniform && tdim * cols / 2 > chunk_uniform))
         return near_ragged_launch(1, T, tdim, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
                                   n_on, c_id, sig_local, Lsig, u, G, s, rag, cols);
     return near_stream_launch(1, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,

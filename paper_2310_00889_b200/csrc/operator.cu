@@ -52,7 +52,7 @@ static void free_op(slb_operator* op) {
     cudaFree(op->partials); cudaFree(op->Lsig); cudaFree(op->nb0); cudaFree(op->bodyc);
     cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev); cudaFree(op->rec);
     cudaFree(op->cn0_d); cudaFree(op->fn0_d); cudaFree(op->lc0_d); cudaFree(op->lf0_d); cudaFree(op->boff_d);
-    cudaFree(op->pbucket_d);
+    cudaFree(op->pbucket_d); cudaFree(op->bmeta_d);
     for (auto& b : op->buckets) { cudaFree(b.plist_d); cudaFree(b.ip_buf); }
     cudaFree(op->ip_buf);
     for (auto& e : op->ev) if (e) cudaEventDestroy(e);
@@ -316,6 +316,11 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         op->blk_total = bo[nnz];
         OPCUDA(cudaMalloc(&op->boff_d, sizeof(int64_t) * (nnz + 1)));
         OPCUDA(cudaMemcpy(op->boff_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice));
+        std::vector<int64_t> bm(std::max<int64_t>(nnz, 1));
+        for (int64_t p = 0; p < nnz; ++p)
+            bm[p] = ((op->cn0[pk[p]] * op->sdim / 2) << 12) | ((op->cn0[pk[p] + 1] - op->cn0[pk[p]]) * op->sdim / 2);
+        OPCUDA(cudaMalloc(&op->bmeta_d, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+        OPCUDA(cudaMemcpy(op->bmeta_d, bm.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice));
     }
     OPST(pack_geo(op->kind, op->M, d->y_fine, d->n_fine, d->eta_fine, d->eta, op->geo, s));
     OPST(pack_scale(op->kind, Mloc, d->n_fine + 3 * f0, d->w_fine + f0, d->eta_fine ? d->eta_fine + f0 : nullptr,
@@ -487,6 +492,7 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
         rag.cn0 = op->cn0_d;
         rag.boff = op->boff_d;
         rag.max_cols = op->max_cols;
+        rag.bmeta = op->bmeta_d;
     }
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
                          d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, op->near_G, s, rag);

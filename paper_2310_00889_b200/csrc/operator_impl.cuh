@@ -117,5 +117,6 @@ struct slb_operator {
     std::vector<Bucket> buckets;
     int max_cols = 0;                   // widest block (nodes * sdim)
     int64_t blk_total = 0;              // doubles in all local blocks (ragged)
+    int64_t* bmeta_d = nullptr;         // [nnz] packed sigma offset / width per block (ragged)
 };
 
