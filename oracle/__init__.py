@@ -142,7 +142,7 @@ def kernel_matrix(kind, r, n=(0.0, 0.0, 0.0), eta=0.0):
 
 
 def farfield(kind, x, y, n, w, sigma, eta=None):
-    """kind 1: Laplace DL; 2: Stokes eta S + D; 3: Laplace SL.  r = 0 pairs skipped."""
+    """kind 1: Laplace D + eta S_L (eta None: D); 2: Stokes eta S + D; 3: Laplace SL.  r = 0 skipped."""
     x, y, w, sigma = _c(x), _c(y), _c(w), _c(sigma)
     n = _c(n) if n is not None else None
     eta = _c(eta) if eta is not None else None

@@ -213,10 +213,10 @@ void or_stokes_dl(const double r[3], const double n[3], double D[9]) {
             D[i * 3 + j] = 3.0 / (4.0 * OR_PI) * rn * r[i] * r[j] / r5;
 }
 
-/* Combined kernel matrix K = eta S + D (Stokes, kind 2), or the Laplace DL (kind 1,
- * 1x1 in K[0]).  kind 3 = Laplace SL (pins only). */
+/* Combined kernel matrix K = eta S + D (Stokes, kind 2), or the Laplace combined field
+ * D + eta S_L (kind 1, 1x1 in K[0]; eta = 0: the Laplace DL).  kind 3 = Laplace SL. */
 void or_kernel_matrix(int kind, const double r[3], const double n[3], double eta, double K[9]) {
-    if (kind == 1) { K[0] = or_laplace_dl(r, n); return; }
+    if (kind == 1) { K[0] = or_laplace_dl(r, n) + eta * or_laplace_sl(r); return; }
     if (kind == 3) { K[0] = or_laplace_sl(r); return; }
     double S[9], D[9];
     or_stokes_sl(r, S);

@@ -274,14 +274,15 @@ CONFIGS = ("c1", "c2", "c3", "c3v", "c4", "c5", "c5alt")
 def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_DL, eta=None, extra_targets=None,
                        seed_offset=0, nt_panels=None, ns_panels=None):
     """Single torus (axis z, centre 0) with the 2 L_k near rule -- pin problems for the special
-    quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes; eta=0 -> pure DL."""
+    quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes, the pure DL for
+    Laplace; an explicit eta sets the single-layer weight of either kernel (0 -> pure DL)."""
     seed = BASE_SEED + 100 + seed_offset
     rng = np.random.default_rng(seed)
     b = torus_body(R, rho)
     pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng,
                    nt_panels=None if nt_panels is None else [np.asarray(nt_panels)],
                    ns_panels=None if ns_panels is None else [np.asarray(ns_panels)])
-    if kernel == STOKES_SLDL and eta is not None:
+    if eta is not None:       # Stokes eta S + D, or the Laplace combined field D + eta S_L (P:L1750)
         pr.eta_body[:] = eta
         pr.eta_f[:] = eta
     return pr

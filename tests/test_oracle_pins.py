@@ -192,6 +192,29 @@ def test_p9_green_identity_laplace():
     np.testing.assert_allclose(S - D, exact, rtol=1e-12, atol=0)
 
 
+def test_p9b_laplace_combined_field_kernel():
+    """the combined Laplace kernel D + eta S_L (kind 1 with eta, the CFIE of P:L1750) against Green's
+    identity: with zero normals and eta = 1 it is S_L, with eta = 0 it is D; and for a general eta it
+    is exactly the sum (u = S[du/dn] - D[u] inside)"""
+    b, g = pin_torus(R=1.0, rho=0.25, P=192, Ns=10, Nt=64)
+    x0 = np.array([1.0, 2.0, 3.0])
+    d = g.y - x0
+    rr = np.sqrt((d * d).sum(1))
+    u = 1 / (FOUR_PI * rr)
+    dudn = -(d * g.n).sum(1) / (FOUR_PI * rr ** 3)
+    ph = np.linspace(0, 2 * np.pi, 5)[:-1] + 0.4
+    X = np.stack([1.05 * np.cos(ph), 1.05 * np.sin(ph), 0.1 + 0 * ph], 1)
+    one = np.ones(g.w.size)
+    S = O.farfield(1, X, g.y, np.zeros_like(g.n), g.w, dudn, eta=one)
+    D = O.farfield(1, X, g.y, g.n, g.w, u, eta=0 * one)
+    exact = 1 / (FOUR_PI * np.sqrt(((X - x0) ** 2).sum(1)))
+    np.testing.assert_allclose(S - D, exact, rtol=1e-12, atol=0)
+    eta = 0.7
+    C = O.farfield(1, X, g.y, g.n, g.w, u, eta=eta * one)
+    SL = O.farfield(3, X, g.y, None, g.w, u)
+    np.testing.assert_allclose(C, D + eta * SL, rtol=1e-13, atol=0)
+
+
 # ---------------------------------------------------------------- P10 brute-force adaptive
 def test_p10_bruteforce_adaptive_quadrature():
     from scipy.integrate import quad
