@@ -35,10 +35,10 @@ class DeviceProblem:
         slice_only: a ONE-GPU operator over rank `rank`'s target rows of an `nranks` partition with all
         source panels (no communicator, identity term off) -- the per-rank compute of the sharded
         operator, for timing projections (tools/scaling_projection.py).
-        single_layer: the pure Stokes single layer S on the same nodes (eta = 1, zero normals, no
-        identity term, no projector; quad blocks with SLB_STOKES_SL) -- the `sl` of slb_mobility_solve."""
+        single_layer: the pure single layer (Stokes S or Laplace S_L) on the same nodes (eta = 1, zero
+        normals, no identity term, no projector; quad blocks with SLB_STOKES_SL / SLB_LAPLACE_SL) --
+        e.g. the `sl` of slb_mobility_solve."""
         if single_layer:
-            assert pr.kernel == 2
             import copy
             pr = copy.copy(pr)
             pr.n_f = np.zeros_like(pr.n_f)
@@ -78,16 +78,17 @@ class DeviceProblem:
         self.x_trg = f64(pr.x_trg[rows])
         if quad is not None and self.nnz > 0:
             trg_node = torch.from_numpy(np.where(rows < pr.n_on, rows, -1).astype(np.int64)).to(dev)
-            eta_panel = f64(pr.eta_body[pr.body_of_panel]) if pr.kernel == 2 else None
+            eta_panel = f64(pr.eta_body[pr.body_of_panel]) if (pr.kernel == 2 or np.any(pr.eta_body != 0)) else None
             rp_d = torch.from_numpy(row_ptr).to(dev)
             pi_d = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
-            slb_nearcorr_quad(3 if single_layer else pr.kernel, self.x_trg, rp_d, pi_d, pr.Ns, pr.Nt, f64(pr.y_c),
+            qk = (3 if pr.kernel == 2 else 4) if single_layer else pr.kernel
+            slb_nearcorr_quad(qk, self.x_trg, rp_d, pi_d, pr.Ns, pr.Nt, f64(pr.y_c),
                               self.blocks, trg_node=trg_node, eta_panel=None if single_layer else eta_panel, order=quad.get("order", 12),
                               beta=quad.get("beta", 0.6), panel_nt=pr.nt_of_panel() if pr.ragged else None,
                               panel_ns=pr.ns_of_panel() if pr.ragged else None)
         self.y_f, self.n_f, self.w_f = f64(pr.y_f), f64(pr.n_f), f64(pr.w_f)
         # pure double layer (all eta = 0) runs the DL kernel: eta_fine must then be NULL
-        self.eta_f = f64(pr.eta_f) if (pr.kernel == 2 and np.any(pr.eta_f != 0)) else None
+        self.eta_f = f64(pr.eta_f) if np.any(pr.eta_f != 0) else None
         self.row_ptr = torch.from_numpy(row_ptr).to(dev)
         self.panel_idx = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
         no = pr.node_off()

@@ -56,9 +56,11 @@ typedef enum {
     SLB_ERR_UNSUPPORTED = 5
 } slb_status;
 
-/* SLB_STOKES_SL (pure single layer S, weight 1) is accepted by slb_nearcorr_quad[_ragged] only; the
- * operator evaluates S as SLB_STOKES_SLDL with eta = 1 and zero normals. */
-typedef enum { SLB_LAPLACE_DL = 1, SLB_STOKES_SLDL = 2, SLB_STOKES_SL = 3 } slb_kernel;
+/* SLB_LAPLACE_DL also carries the Laplace combined field D + eta S_L when eta / eta_fine /
+ * eta_panel is given.  SLB_STOKES_SL / SLB_LAPLACE_SL (pure single layers, weight 1) are accepted by
+ * slb_nearcorr_quad[_ragged] only; the operator evaluates them as the combined kernels with eta = 1
+ * and zero normals. */
+typedef enum { SLB_LAPLACE_DL = 1, SLB_STOKES_SLDL = 2, SLB_STOKES_SL = 3, SLB_LAPLACE_SL = 4 } slb_kernel;
 
 /* Compiled limits (SLB_ERR_UNSUPPORTED beyond them). */
 #define SLB_MAX_NS 32
@@ -142,8 +144,9 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
  * exact action of the layer potential on panel k's interpolant, by a singularity-resolving
  * adaptive rule: geometry interpolated from the panel's coarse nodes
  * y_coarse [n_panels][ns][nt][3]; trg_node[t] = global coarse node id if target t is that node
- * (on-surface, singular) else -1 (may be NULL: all off-surface); eta_panel [n_panels] (Stokes
- * eta S + D; NULL for Laplace DL); order = GL points per cell direction (4..24), beta = accepted
+ * (on-surface, singular) else -1 (may be NULL: all off-surface); eta_panel [n_panels]: single-layer
+ * weight (required for SLB_STOKES_SLDL: eta S + D; optional for SLB_LAPLACE_DL: D + eta S_L; for the
+ * pure single layers SLB_STOKES_SL / SLB_LAPLACE_SL NULL means weight 1); order = GL points per cell direction (4..24), beta = accepted
  * distance / cell diameter.  blocks [nnz][tdim][ns*nt*sdim] written (unfolded B).  Synchronises s.
  * SLB_ERR_UNSUPPORTED if a target is too close for the cell budget, or if a panel's working set
  * exceeds shared memory (Stokes: N_s N_th <= 1024, e.g. 16 x 64). */
@@ -201,8 +204,9 @@ typedef struct {
     const double* y_fine;               /* [M][3] global fine nodes, M = n_panels_global*ms*mt */
     const double* n_fine;               /* [M][3] */
     const double* w_fine;               /* [M] */
-    const double* eta_fine;             /* [M] (Stokes, entries > 0) or NULL -> eta */
-    double eta;                         /* scalar eta when eta_fine == NULL (0 -> pure DL) */
+    const double* eta_fine;             /* [M] single-layer weight (Stokes: entries > 0; Laplace: the
+                                           combined field D + eta S_L) or NULL -> eta */
+    double eta;                         /* scalar eta when eta_fine == NULL (0 -> pure DL, either kernel) */
     const int64_t* row_ptr;             /* [n_trg_local+1] local CSR */
     const int32_t* panel_idx;           /* [nnz] GLOBAL panel ids */
     double* blocks;                     /* [nnz][tdim][ns*nt*sdim]; folded in place at create unless blocks_folded */

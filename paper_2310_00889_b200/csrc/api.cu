@@ -173,12 +173,12 @@ static slb_status farfield_common(FarKind kind, int64_t n_trg, const double* x, 
     SLB_REQUIRE(check_sticky("farfield") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
     unsigned long long* zc = coincident_counter();
     SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
-    const int tdim = (kind == FAR_LAPLACE) ? 1 : 3;
+    const int tdim = far_scalar(kind) ? 1 : 3;
     FarPlan plan = far_plan(n_src);
     double *geo = nullptr, *sc = nullptr, *dyn = nullptr, *part = nullptr;
     const int64_t M = n_src > 0 ? n_src : 1;
     SLB_CUDA(cudaMallocAsync(&geo, sizeof(double) * M * 6, s));
-    SLB_CUDA(cudaMallocAsync(&sc, sizeof(double) * M * 3, s));
+    SLB_CUDA(cudaMallocAsync(&sc, sizeof(double) * M * 4, s));
     SLB_CUDA(cudaMallocAsync(&dyn, sizeof(double) * M * 4, s));
     SLB_CUDA(cudaMallocAsync(&part, sizeof(double) * plan.n_chunks * n_trg * tdim, s));
     slb_status st = SLB_OK;
@@ -239,7 +239,7 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
     static InterpParams ip;
     double* owned = nullptr;
     SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip, &owned), SLB_ERR_OOM, "interpolation matrices: allocation failed");
-    FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE
+    FarKind kind = kernel == SLB_LAPLACE_DL ? ((eta_fine || eta > 0.0) ? FAR_LAPLACE_SLDL : FAR_LAPLACE)
                                             : ((eta_fine || eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL);
     slb_status st = fold_launch(kind, n_trg, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine, w_fine, eta_fine, eta,
                                 blocks, s);

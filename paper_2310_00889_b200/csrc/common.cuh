@@ -131,7 +131,9 @@ extern unsigned long long g_launch_count;
 int num_sms();
 
 // ---- far-field engine (farfield.cu) ----
-enum FarKind { FAR_LAPLACE = 0, FAR_STOKES_SLDL = 1, FAR_STOKES_DL = 2 };
+// FAR_LAPLACE_SLDL: the Laplace combined field D + eta S_L, records {q = w sigma n/4pi, s = eta w sigma/4pi}
+enum FarKind { FAR_LAPLACE = 0, FAR_STOKES_SLDL = 1, FAR_STOKES_DL = 2, FAR_LAPLACE_SLDL = 3 };
+__host__ __device__ constexpr bool far_scalar(int k) { return k == FAR_LAPLACE || k == FAR_LAPLACE_SLDL; }
 
 // Summation plan; depends ONLY on the source count M (bitwise determinism across ranks).
 struct FarPlan {
@@ -166,7 +168,7 @@ slb_status far_const_prepare();
 slb_status pack_geo(FarKind kind, int64_t M, const double* y, const double* n, const double* eta_src,
                     double eta, double* geo, cudaStream_t s);
 // per-source scale used by the dyn packing: Stokes -> sc[m] = e_m w_m (SLDL) or w_m (DL), 1 double;
-// Laplace -> sc[m] = w_m n_m / (4 pi), 3 doubles
+// Laplace -> sc[m] = {w_m n_m / (4 pi), eta_m w_m / (4 pi)}, 4 doubles
 slb_status pack_scale(FarKind kind, int64_t M, const double* n, const double* w, const double* eta_src,
                       double eta, double* sc, cudaStream_t s);
 slb_status pack_dyn(FarKind kind, int64_t M, const double* sc, const double* sigma, double* dyn,

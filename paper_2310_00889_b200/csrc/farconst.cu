@@ -67,6 +67,10 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
             acc[j][0] = fma(b, rx, acc[j][0]);
             acc[j][1] = fma(b, ry, acc[j][1]);
             acc[j][2] = fma(b, rz, acc[j][2]);
+        } else if constexpr (KIND == FAR_LAPLACE_SLDL) {
+            // Laplace D + eta S_L: u += rinv ((r.q) rinv^2 + s)
+            const double rq = fma(rx, s[6], fma(ry, s[7], rz * s[8]));
+            acc[j][0] = fma(rinv, fma(rq, rinv * rinv, s[9]), acc[j][0]);
         } else {
             // Laplace DL: u += (r.q) rinv^3
             const double rq = fma(rx, s[6], fma(ry, s[7], rz * s[8]));
@@ -79,7 +83,7 @@ template <int KIND, int J, int BUF, int CM, int UNR = 4, int MINB = 4>
 __global__ void __launch_bounds__(kConstThreads, MINB)
 far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
                  double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
-    constexpr int D = (KIND == FAR_LAPLACE) ? 1 : 3;
+    constexpr int D = far_scalar(KIND) ? 1 : 3;
     double x[J][3], acc[J][3];
     bool valid[J];
 #pragma unroll
@@ -135,7 +139,7 @@ __global__ void pack_rec_kernel(int64_t M, const double* __restrict__ geo, const
     o[0] = g[0]; o[1] = g[1]; o[2] = g[2];
     const double2 d0 = d[0], d1 = d[1];
     o[3] = d0;
-    o[4] = make_double2(d1.x, 0.0);
+    o[4] = d1;                 // {g_z, 0} (Stokes) or {q_z, s} (Laplace combined field)
 }
 
 constexpr int kJ = 2;
@@ -199,7 +203,7 @@ static void launch_tile_buf(int slot, int64_t T, const double* x, int n, int fir
 slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
                            double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
                            cudaEvent_t fork, cudaEvent_t* join, int64_t* launches) {
-    const int D = (kind == FAR_LAPLACE) ? 1 : 3;
+    const int D = far_scalar(kind) ? 1 : 3;
     const int nb = const_bufs_for(M);
     const int tile = kConstRecs / nb;                // 200 or 100 records per buffer
     const int stride = kMaxConstBufs / nb;           // buffer b occupies eighth b * stride
@@ -223,6 +227,7 @@ slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, 
             switch (kind) {
                 case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
                 case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
+                case FAR_LAPLACE_SLDL: launch_tile_buf<FAR_LAPLACE_SLDL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
                 default: launch_tile_buf<FAR_LAPLACE>(b * stride, T, x, n, first, part, zc, ws[b]); break;
             }
             ++*launches;
@@ -263,6 +268,7 @@ slb_status far_const_prepare() {
     PREP(FAR_STOKES_SLDL)
     PREP(FAR_STOKES_DL)
     PREP(FAR_LAPLACE)
+    PREP(FAR_LAPLACE_SLDL)
 #undef PREP
 #undef PREP1
     SLB_CUDA(cudaFuncGetAttributes(&fa, pack_rec_kernel));

@@ -102,6 +102,22 @@ struct Pair<FAR_LAPLACE> {
     }
 };
 
+template <>
+struct Pair<FAR_LAPLACE_SLDL> {
+    static constexpr int D = 1;
+    // u += (r.q) rinv^3 + s rinv = rinv ((r.q) rinv^2 + s):  17 FP64-pipe instructions
+    __device__ __forceinline__ static void run(const double x[3], const double* g, const double* d,
+                                               double acc[1], unsigned& zc) {
+        double rx = x[0] - g[0], ry = x[1] - g[1], rz = x[2] - g[2];
+        double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
+        double rinv = rsqrt_refined(r2);
+        bool z = is_zero_r2(r2);
+        rinv = z ? 0.0 : rinv;
+        zc += z;
+        double rq = fma(rx, d[0], fma(ry, d[1], rz * d[2]));
+        acc[0] = fma(rinv, fma(rq, rinv * rinv, d[3]), acc[0]);
+    }
+};
 
 // Op-major J-target Stokes SL+DL update for one source: every FP64 operation is issued for all J
 // targets back to back so the shared (source) operand sits in the same slot of consecutive
@@ -243,12 +259,12 @@ far_kernel(int64_t T, const double* __restrict__ x_trg, const double* __restrict
         const double* Dy = SDYN(st);
 #pragma unroll UNR
         for (int m = sl; m < n; m += SPLIT) {
-            double g[6], d[3];
+            double g[6], d[4];
             const double2* g2 = reinterpret_cast<const double2*>(G + m * kGeo);
             const double2* d2 = reinterpret_cast<const double2*>(Dy + m * kDyn);
             double2 a0 = g2[0], a1 = g2[1], a2 = g2[2], b0 = d2[0], b1 = d2[1];
             g[0] = a0.x; g[1] = a0.y; g[2] = a1.x; g[3] = a1.y; g[4] = a2.x; g[5] = a2.y;
-            d[0] = b0.x; d[1] = b0.y; d[2] = b1.x;
+            d[0] = b0.x; d[1] = b0.y; d[2] = b1.x; d[3] = b1.y;
             if constexpr (KIND == FAR_STOKES_SLDL) {
                 sldl_pairs<J>(x, g, d, acc, zc);
             } else {
@@ -333,6 +349,7 @@ slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t T, const doub
     if (plan.split == 1) {
         switch (kind) {
             case FAR_LAPLACE: return launch_far<FAR_LAPLACE, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_LAPLACE_SLDL: return launch_far<FAR_LAPLACE_SLDL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
             case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, 2, 1, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
             case FAR_STOKES_SLDL:
                 switch (far_variant()) {
@@ -349,6 +366,7 @@ slb_status far_partials(FarKind kind, const FarPlan& plan, int64_t T, const doub
     } else {
         switch (kind) {
             case FAR_LAPLACE: return launch_far<FAR_LAPLACE, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
+            case FAR_LAPLACE_SLDL: return launch_far<FAR_LAPLACE_SLDL, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
             case FAR_STOKES_SLDL: return launch_far<FAR_STOKES_SLDL, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
             case FAR_STOKES_DL: return launch_far<FAR_STOKES_DL, 2, 4, 2, 2>(plan, T, x, geo, dyn, partials, zc, s);
         }
@@ -399,9 +417,11 @@ __global__ void pack_scale_kernel(int kind, int64_t M, const double* __restrict_
                                   double eta, double* __restrict__ sc) {
     int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
-    if (kind == FAR_LAPLACE) {
+    if (far_scalar(kind)) {
         double f = w[m] / (4.0 * kPi);
-        sc[3 * m] = f * n[3 * m]; sc[3 * m + 1] = f * n[3 * m + 1]; sc[3 * m + 2] = f * n[3 * m + 2];
+        double e = (kind == FAR_LAPLACE_SLDL) ? (eta_src ? eta_src[m] : eta) : 0.0;
+        sc[4 * m] = f * n[3 * m]; sc[4 * m + 1] = f * n[3 * m + 1]; sc[4 * m + 2] = f * n[3 * m + 2];
+        sc[4 * m + 3] = e * f;
     } else if (kind == FAR_STOKES_SLDL) {
         double e = eta_src ? eta_src[m] : eta;
         sc[m] = (e / (8.0 * kPi)) * w[m];
@@ -415,9 +435,9 @@ __global__ void pack_dyn_kernel(int kind, int64_t M, const double* __restrict__ 
     int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     double4 o;
-    if (kind == FAR_LAPLACE) {
+    if (far_scalar(kind)) {
         double s = sigma[m];
-        o = make_double4(sc[3 * m] * s, sc[3 * m + 1] * s, sc[3 * m + 2] * s, 0.0);
+        o = make_double4(sc[4 * m] * s, sc[4 * m + 1] * s, sc[4 * m + 2] * s, sc[4 * m + 3] * s);
     } else {
         double f = sc[m];
         o = make_double4(f * sigma[3 * m], f * sigma[3 * m + 1], f * sigma[3 * m + 2], 0.0);

@@ -204,9 +204,9 @@ extern "C" slb_status slb_mobility_solve(slb_operator* mob, slb_operator* sl, co
                                          int* iters_out, double* relres_out, cudaStream_t s) {
     SLB_REQUIRE(mob && sl && force_torque && rigid_out && sigma, SLB_ERR_INVALID_ARG, "null argument");
     const int64_t nb = mob->d.n_bodies_local;
-    SLB_REQUIRE(mob->kind != FAR_LAPLACE && nb > 0 && mob->bodyc, SLB_ERR_INVALID_ARG,
+    SLB_REQUIRE(!far_scalar(mob->kind) && nb > 0 && mob->bodyc, SLB_ERR_INVALID_ARG,
                 "mob must be a Stokes operator with the rigid-motion projector");
-    SLB_REQUIRE(sl->kind != FAR_LAPLACE && sl->d.n_bodies_local == 0 && sl->N_loc == mob->N_loc &&
+    SLB_REQUIRE(!far_scalar(sl->kind) && sl->d.n_bodies_local == 0 && sl->N_loc == mob->N_loc &&
                     sl->d.n_trg_local == mob->d.n_trg_local,
                 SLB_ERR_INVALID_ARG, "sl must be a Stokes operator (no projector) on the same nodes and targets");
     const int64_t n = mob->N_loc * 3;

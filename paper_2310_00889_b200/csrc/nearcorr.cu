@@ -345,8 +345,8 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
     const double* Ps = ip.vg ? ip.vg : ip.v;
     const double* F = Ps + ms * ns;
     const int Mn = ms * mt, Nn = ns * nt;
-    const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
-    const int TD = (kind == FAR_LAPLACE) ? 1 : 3;
+    const int NG = far_scalar(kind) ? 1 : 6;
+    const int TD = far_scalar(kind) ? 1 : 3;
     const int Mc = rch * mt;        // fine nodes per pass
     double* G = sm;                 // [NG][rch * mt]
     double* H = sm + NG * Mc;       // [NG][rch][nt]
@@ -372,8 +372,9 @@ fold_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t
                 }
                 double ir = 1.0 / sqrt(r2);
                 double rn = r[0] * nn[0] + r[1] * nn[1] + r[2] * nn[2];
-                if (kind == FAR_LAPLACE) {
-                    G[q] = rn * ir * ir * ir / (4.0 * kPi) * w;
+                if (far_scalar(kind)) {
+                    const double e = (kind == FAR_LAPLACE_SLDL) ? (eta_f ? eta_f[m] : eta) : 0.0;
+                    G[q] = (rn * ir * ir * ir + e * ir) / (4.0 * kPi) * w;
                 } else {
                     double e = (kind == FAR_STOKES_SLDL) ? (eta_f ? eta_f[m] : eta) : 0.0;
                     double ir3 = ir * ir * ir;
@@ -420,7 +421,7 @@ slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64
                        const int64_t* boff) {
     if (T <= 0) return SLB_OK;
     SLB_REQUIRE(T <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets for fold");
-    const int NG = (kind == FAR_LAPLACE) ? 1 : 6;
+    const int NG = far_scalar(kind) ? 1 : 6;
     auto smem_of = [&](int r) { return sizeof(double) * (size_t)(NG * r * ip.mt + NG * r * ip.nt); };
     int rch = ip.ms;
     while (rch > 1 && smem_of(rch) > 227 * 1024) rch = (rch + 1) / 2;

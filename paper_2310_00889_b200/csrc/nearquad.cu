@@ -266,7 +266,10 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         const double* tg = P.tgl + ns * (ns - 1) / 2;
         const double* lm = P.lam + ns * (ns - 1) / 2;
         const int64_t c0 = cn0 ? cn0[k] : k * (int64_t)Nn;
-        const double eta = (kind == FAR_STOKES_SLDL) ? (eta_panel ? eta_panel[k] : 1.0) : 0.0;
+        // single-layer weight: Stokes eta_panel (or 1: pure S); Laplace eta_panel (combined field
+        // D + eta S_L), else 0 (pure D) or 1 (pure S_L, P.dl = 0)
+        const double eta = (kind == FAR_STOKES_SLDL) ? (eta_panel ? eta_panel[k] : 1.0)
+                                                     : (eta_panel ? eta_panel[k] : (P.dl == 0.0 ? 1.0 : 0.0));
         for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[c0 * 3 + e];
         for (int e = tid; e < nt; e += kQThreads) sincos(2.0 * kPi * e / nt, &TS[e], &TC[e]);
         for (int e = tid; e < NG * Nn; e += kQThreads) Bacc[e] = 0.0;
@@ -410,7 +413,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     const double ir = 1.0 / sqrt(r2);
                     const double rn = r[0] * nrm[0] + r[1] * nrm[1] + r[2] * nrm[2];
                     if (kind == FAR_LAPLACE) {
-                        G[0] = rn * ir * ir * ir / (4.0 * kPi) * wJ;
+                        G[0] = (P.dl * rn * ir * ir * ir + eta * ir) / (4.0 * kPi) * wJ;
                     } else {
                         const double ir3 = ir * ir * ir;
                         const double sl = eta / (8.0 * kPi), dl = P.dl * 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
@@ -480,7 +483,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                const int64_t* boff, const int32_t* pns) {
     static QuadParams P;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
-    P.dl = (kernel == SLB_STOKES_SL) ? 0.0 : 1.0;
+    P.dl = (kernel == SLB_STOKES_SL || kernel == SLB_LAPLACE_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
     for (int n = 2; n <= kMaxNsQ; ++n) {
         double* tg = P.tgl + n * (n - 1) / 2;
@@ -495,7 +498,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     gl_nodes(P.q, P.gx, P.gw);
     gl_nodes(P.qd, P.dx, P.dw);
     for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
-    const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
+    const int TD = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? 1 : 3;
     const int Nn = ns * nt;   // (largest) panel
     const size_t smem = sizeof(double) * ((size_t)Nn * 3 + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns + nt) +
                                           2 * (size_t)nt) + sizeof(Cell) * kMaxCells;
@@ -514,7 +517,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                                                         y_coarse, P, pnt, cn0, pns, cp);
         ++g_launch_count;
     }
-    const FarKind kind = kernel == SLB_LAPLACE_DL ? FAR_LAPLACE : FAR_STOKES_SLDL;
+    const FarKind kind = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? FAR_LAPLACE : FAR_STOKES_SLDL;
     nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem, s>>>((int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx,
                                                              y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff, pns, cp);
     ++g_launch_count;
@@ -535,7 +538,8 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
 }
 
 static slb_status nearquad_check(slb_kernel kernel, int64_t n_trg, int ns, int order, double beta) {
-    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL || kernel == SLB_STOKES_SL,
+    SLB_REQUIRE(kernel == SLB_LAPLACE_DL || kernel == SLB_STOKES_SLDL || kernel == SLB_STOKES_SL ||
+                    kernel == SLB_LAPLACE_SL,
                 SLB_ERR_INVALID_ARG, "bad kernel");
     SLB_REQUIRE(n_trg >= 0 && ns >= 2, SLB_ERR_INVALID_ARG, "bad sizes");
     SLB_REQUIRE(ns <= kMaxNsQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
@@ -571,7 +575,7 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
     SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks && panel_nt && panel_ns && n_panels > 0,
                 SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
-    const int TD = kernel == SLB_LAPLACE_DL ? 1 : 3;
+    const int TD = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? 1 : 3;
     std::vector<int64_t> c0(n_panels + 1, 0);
     int ntmax = 0, nsmax = 0;
     for (int64_t k = 0; k < n_panels; ++k) {

@@ -127,7 +127,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     op->d = *d;
     op->comm = comm;
     op->sdim = op->tdim = (d->kernel == SLB_LAPLACE_DL) ? 1 : 3;
-    if (d->kernel == SLB_LAPLACE_DL) op->kind = FAR_LAPLACE;
+    if (d->kernel == SLB_LAPLACE_DL) op->kind = (d->eta_fine || d->eta > 0.0) ? FAR_LAPLACE_SLDL : FAR_LAPLACE;
     else op->kind = (d->eta_fine || d->eta > 0.0) ? FAR_STOKES_SLDL : FAR_STOKES_DL;
     op->ragged = d->panel_nt || d->panel_mt || d->panel_ns || d->panel_ms;
     if (op->ragged) {
@@ -239,7 +239,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         set_error("slb_operator_create: n_on_local exceeds the local node count");
         return SLB_ERR_INVALID_ARG;
     }
-    if (d->n_bodies_local > 0 && op->kind == FAR_LAPLACE) {
+    if (d->n_bodies_local > 0 && far_scalar(op->kind)) {
         free_op(op);
         set_error("slb_operator_create: the projector needs the Stokes kernel");
         return SLB_ERR_INVALID_ARG;
@@ -294,7 +294,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     const int64_t Mloc = op->ragged ? op->fn0[d->panel_end] - op->fn0[d->panel_begin] : op->P_loc * op->Mn;
     const int64_t n_coarse_global = op->ragged ? op->cn0[d->n_panels_global] * op->sdim : d->n_panels_global * op->cols;
     OPCUDA(cudaMalloc(&op->geo, sizeof(double) * op->M * 6));
-    OPCUDA(cudaMalloc(&op->sc, sizeof(double) * std::max<int64_t>(Mloc, 1) * 3));
+    OPCUDA(cudaMalloc(&op->sc, sizeof(double) * std::max<int64_t>(Mloc, 1) * 4));
     OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
     OPCUDA(cudaMalloc(&op->coarse, sizeof(double) * n_coarse_global));
     OPCUDA(cudaMalloc(&op->partials, sizeof(double) * std::max<int64_t>(op->plan.n_chunks * T * op->tdim, 1)));

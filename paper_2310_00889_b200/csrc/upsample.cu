@@ -135,16 +135,17 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
                 for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
                     const int64_t m = m0 + e;
                     const int eo = e - e0;
-                    double v0, v1, v2;
-                    if (kind == FAR_LAPLACE) {
+                    double v0, v1, v2, v3 = 0.0;
+                    if (far_scalar(kind)) {
                         const double v = O[eo];
-                        v0 = scale[3 * m] * v; v1 = scale[3 * m + 1] * v; v2 = scale[3 * m + 2] * v;
+                        v0 = scale[4 * m] * v; v1 = scale[4 * m + 1] * v; v2 = scale[4 * m + 2] * v;
+                        v3 = scale[4 * m + 3] * v;
                     } else {
                         const double sc = scale[m];
                         v0 = sc * O[3 * eo]; v1 = sc * O[3 * eo + 1]; v2 = sc * O[3 * eo + 2];
                     }
                     D2[2 * m] = make_double2(v0, v1);
-                    D2[2 * m + 1] = make_double2(v2, 0.0);
+                    D2[2 * m + 1] = make_double2(v2, v3);
                 }
             } else {
                 for (int e = e0 * nc + threadIdx.x; e < e1 * nc; e += blockDim.x) sf_out[m0 * nc + e] = O[e - e0 * nc];
