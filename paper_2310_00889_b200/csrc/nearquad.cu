@@ -309,6 +309,17 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     stack[sp++] = c;
                 }
             const double cap = 2.0 * Sh;   // ~ tube diameter: keeps the opposite wall resolved
+            // distance used by the acceptance test: on the tube (radius ~ Sh) a target at distance d
+            // from the surface puts the kernel's complex singularity in th at acosh(1 + d^2 / (2 Sh (Sh + d)))
+            // from th*, closer than the flat proxy d / Sh (d = 2 rho: 1.1 instead of 2) -- use that strip
+            // width so cells around th* resolve the kernel (tests/test_gpu_bvp.py: 1e-9 -> 1e-12)
+            const double deff = (d > 0.0) ? Sh * acosh(1.0 + d * d / (2.0 * Sh * (Sh + d))) : 0.0;
+            // theta width for which a q-point GL rule integrates the degree-k = nt/2 trigonometric
+            // basis to the accuracy the distance criterion gives (~2.76^-2q at beta = 0.6): the GL
+            // error for e^{ik th} on a half-width h is ~ (e k h / 4q)^2q, so k h <= 4q / (2.76 e) and
+            // the width 2h <= 2.13 q / nt.  Without it, cells of moderate-distance targets spanning
+            // half the circumference under-resolve cos(nt th / 2) (tests/test_gpu_bvp.py: 1e-7 -> 1e-12)
+            const double hmax = 2.13 * P.q / nt;
             while (sp > 0) {
                 Cell c = stack[--sp];
                 const double wa = (c.t1 - c.t0) * St, wb = (c.h1 - c.h0) * Sh;
@@ -320,7 +331,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     // distance from (t*, th*) to the cell in scaled coordinates, plus the normal offset
                     const double da = (c.t0 > ts) ? (c.t0 - ts) * St : ((c.t1 < ts) ? (ts - c.t1) * St : 0.0);
                     const double db = (c.h0 > 0.0) ? c.h0 * Sh : ((c.h1 < 0.0) ? -c.h1 * Sh : 0.0);
-                    const double dist = sqrt(d * d + da * da + db * db);
+                    const double dist = sqrt(deff * deff + da * da + db * db);
                     if (da >= 2.0 * cap) {
                         // far along the fiber (more than two tube diameters): the whole cross-section
                         // is at true distance >= da - cap >= da / 2, so no size cap -- cells grow
@@ -330,6 +341,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                         accept = dist >= P.beta * diag && diag <= 2.0 * cap;
                     }
                 }
+                accept = accept && (c.h1 - c.h0) <= hmax;
                 if (accept) {
                     if (nc >= kMaxCells) { s_fail = 1; break; }
                     c.nodes = c.duffy ? 2 * P.qd * P.qd : P.q * P.q;
@@ -340,7 +352,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 }
                 if (sp + 4 > 64) { s_fail = 2; break; }
                 // split: the longer side in two (or both if comparable); Duffy keeps its corner cell
-                const bool sa = wa >= 0.5 * wb, sb = wb >= 0.5 * wa;
+                const bool sa = wa >= 0.5 * wb, sb = wb >= 0.5 * wa || (c.h1 - c.h0) > hmax;
                 const double tm = 0.5 * (c.t0 + c.t1), hm = 0.5 * (c.h0 + c.h1);
                 const double ta[3] = {c.t0, sa ? tm : c.t1, c.t1};
                 const double ha[3] = {c.h0, sb ? hm : c.h1, c.h1};
