@@ -448,27 +448,40 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             // (nodes n past the batch end carry zeros); each warp owns whole 8x8 output tiles.
             {
                 const int warp = tid >> 5, lane = tid & 31, fg = lane >> 2, ftq = lane & 3;
-                const int Mr = NG * ns, mtl = (Mr + 7) / 8, ntl = (nt + 7) / 8;
-                for (int tile = warp; tile < mtl * ntl; tile += kQThreads / 32) {
-                    const int m0 = (tile / ntl) * 8, n0 = (tile % ntl) * 8;
+                const int Mr = NG * ns, mtl = (Mr + 7) / 8, ntl = (nt + 7) / 8;   // ntl <= 8
+                // a warp owns whole 8-row strips and sweeps all column tiles with the A fragment
+                // (G l products) computed once per k-step
+                for (int strip = warp; strip < mtl; strip += kQThreads / 32) {
+                    const int m0 = strip * 8;
                     const int row = m0 + fg;                       // A row of this lane
                     const int q2 = row / ns, ia = row % ns;
                     const bool rok = row < Mr;
-                    const int col = n0 + fg;                       // B column of this lane
-                    const bool cok = col < nt;
-                    const int oc = n0 + 2 * ftq;                   // output columns oc, oc+1 of row m0+fg
-                    double d0 = (rok && oc < nt) ? Bacc[row * nt + oc] : 0.0;
-                    double d1 = (rok && oc + 1 < nt) ? Bacc[row * nt + oc + 1] : 0.0;
-#pragma unroll 4
+                    double d0[8], d1[8];
+#pragma unroll
+                    for (int tn = 0; tn < 8; ++tn) {
+                        const int oc = tn * 8 + 2 * ftq;           // output columns oc, oc+1 of row m0+fg
+                        d0[tn] = (tn < ntl && rok && oc < nt) ? Bacc[row * nt + oc] : 0.0;
+                        d1[tn] = (tn < ntl && rok && oc + 1 < nt) ? Bacc[row * nt + oc + 1] : 0.0;
+                    }
                     for (int k0 = 0; k0 < kQThreads; k0 += 4) {
                         const int n = k0 + ftq;
                         const double a = rok ? Gs[n * NG + q2] * Ls[n * ns + ia] : 0.0;
-                        const double b = cok ? Cs[n * nt + col] : 0.0;
-                        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                                     : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+#pragma unroll
+                        for (int tn = 0; tn < 8; ++tn) {
+                            if (tn < ntl) {                        // warp-uniform
+                                const int col = tn * 8 + fg;       // B column of this lane
+                                const double b = col < nt ? Cs[n * nt + col] : 0.0;
+                                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                                             : "+d"(d0[tn]), "+d"(d1[tn]) : "d"(a), "d"(b));
+                            }
+                        }
                     }
-                    if (rok && oc < nt) Bacc[row * nt + oc] = d0;
-                    if (rok && oc + 1 < nt) Bacc[row * nt + oc + 1] = d1;
+#pragma unroll
+                    for (int tn = 0; tn < 8; ++tn) {
+                        const int oc = tn * 8 + 2 * ftq;
+                        if (tn < ntl && rok && oc < nt) Bacc[row * nt + oc] = d0[tn];
+                        if (tn < ntl && rok && oc + 1 < nt) Bacc[row * nt + oc + 1] = d1[tn];
+                    }
                 }
             }
             __syncthreads();
