@@ -234,7 +234,8 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 const double* __restrict__ y_coarse, const double* __restrict__ eta_panel,
                 const __grid_constant__ QuadParams P, double* __restrict__ blocks, int* __restrict__ status,
                 const int32_t* __restrict__ pnt, const int64_t* __restrict__ cn0, const int64_t* __restrict__ boff,
-                const int32_t* __restrict__ pns, const double* __restrict__ cp) {
+                const int32_t* __restrict__ pns, const double* __restrict__ cp,
+                const int32_t* __restrict__ pclass, int cls) {
     extern __shared__ double sm[];
     // ragged (NEXT N4): panel k has pnt[k] angular nodes and starts at coarse node cn0[k]; block p at
     // boff[p]; the shared layout is sized for P.nt = the largest order.  NULL: uniform P.nt.
@@ -243,8 +244,11 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     const int NG = TD * TD;
     const int tid = threadIdx.x;
     // shared layout
-    double* Y = sm;                                   // [Nn][3]
-    double* Bacc = Y + Nnm * 3;                       // [NG][ns][nt]
+    // Y: the panel's nodes [Nn][3] for the closest point; then (same region) the rings' Fourier
+    // coefficients FA, FB [ns][nt/2+1][3] for the quadrature nodes
+    const int Ysz = max(Nnm * 3, nsm * (ntm / 2 + 1) * 6);
+    double* Y = sm;
+    double* Bacc = Y + Ysz;                           // [NG*ns][nt]  (Fourier-space accumulator)
     double* Gs = Bacc + NG * Nnm;                     // [128][NG]
     double* Ls = Gs + kQThreads * NG;                 // [128][ns]
     double* Cs = Ls + kQThreads * nsm;                // [128][nt]
@@ -252,7 +256,8 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
     Cell* cells = reinterpret_cast<Cell*>(TS + ntm);
     __shared__ double s_par[8];                       // t*, th*, d, St, Sh, node-singular flag
-    __shared__ int s_ncell, s_ntot, s_fail;
+    __shared__ int s_ncell, s_ntot, s_fail, s_K;
+    __shared__ unsigned long long s_amax;
     // per-thread scratch for the interpolation (registers / local)
     double lb[kMaxNsQ], dlb[kMaxNsQ], Cb[kMaxNtQ], dCb[kMaxNtQ];
 
@@ -262,6 +267,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     const int64_t node = trg_node ? trg_node[t] : -1;
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
+        if (pclass && pclass[k] != cls) continue;             // another size class's launch
         const int nt = pnt ? pnt[k] : ntm, ns = pns ? pns[k] : nsm, Nn = ns * nt;
         const double* tg = P.tgl + ns * (ns - 1) / 2;
         const double* lm = P.lam + ns * (ns - 1) / 2;
@@ -377,6 +383,41 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         }
         const double ts = s_par[0], hs = s_par[1];
         const int nc = s_ncell, ntot = s_ntot;
+        // ---------------- Fourier coefficients of every GL ring of the panel (trig interpolant in th):
+        //   ring(th) = A_0 + 2 sum_{l=1}^{N/2-1} (A_l cos l th + B_l sin l th) + A_{N/2} cos(N th / 2),
+        //   A_l = (1/N) sum_j Y_j cos(l th_j), B_l = (1/N) sum_j Y_j sin(l th_j).  Modes above K (the
+        //   last one with a coefficient > 1e-15 of the ring means; K = 1 for circular cross-sections)
+        //   are dropped, so a node costs O(N_s K) instead of O(N_s N_th).
+        const int H = nt / 2 + 1;
+        double* FA = Y;                               // [ns][H][3]
+        double* FB = Y + ns * H * 3;                  // [ns][H][3]
+        if (tid == 0) { s_K = 0; s_amax = 0ull; }
+        __syncthreads();
+        for (int e = tid; e < ns * H * 3; e += kQThreads) {
+            const int c = e % 3, l = (e / 3) % H, i = e / (3 * H);
+            const double* Yr = y_coarse + (c0 + (int64_t)i * nt) * 3 + c;
+            double a = 0.0, b = 0.0;
+            int idx = 0;
+            for (int j = 0; j < nt; ++j) {
+                a = fma(Yr[3 * j], TC[idx], a);
+                b = fma(Yr[3 * j], TS[idx], b);
+                idx += l;
+                if (idx >= nt) idx -= nt;
+            }
+            FA[e] = a / nt;
+            FB[e] = b / nt;
+            if (l == 0) atomicMax(&s_amax, (unsigned long long)__double_as_longlong(fabs(a / nt)));
+        }
+        __syncthreads();
+        {
+            const double tol = 1e-15 * __longlong_as_double((long long)s_amax);
+            for (int e = tid; e < ns * H * 3; e += kQThreads) {
+                const int l = (e / 3) % H;
+                if (l > 0 && (fabs(FA[e]) > tol || fabs(FB[e]) > tol)) atomicMax(&s_K, l);
+            }
+        }
+        __syncthreads();
+        const int K = s_K;
         // ---------------- quadrature nodes in batches of kQThreads
         for (int base = 0; base < ntot; base += kQThreads) {
             const int g = base + tid;
@@ -411,8 +452,46 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     hh = ch + u * (Ah + v * (Bh - Ah));
                     W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
                 }
-                double y[3], yt[3], yh[3];
-                geom_eval(ns, tg, lm, nt, Y, tt, hs + hh, y, yt, yh, lb, dlb, Cb, dCb, TC, TS);
+                double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
+                lagrange_eval(ns, tg, lm, tt, lb, dlb);
+                double c1, s1;
+                sincos(hs + hh, &s1, &c1);
+                for (int i = 0; i < ns; ++i) {                // ring i at th, and d/dth, from its modes
+                    const double* Ai = FA + i * H * 3;
+                    const double* Bi = FB + i * H * 3;
+                    double R[3] = {Ai[0], Ai[1], Ai[2]}, dR[3] = {0, 0, 0};
+                    double ck = c1, sk = s1;
+                    for (int l = 1; l <= K; ++l) {
+                        const double f = (2 * l == nt) ? 1.0 : 2.0;
+                        for (int c = 0; c < 3; ++c) {
+                            R[c] = fma(f, fma(Ai[3 * l + c], ck, Bi[3 * l + c] * sk), R[c]);
+                            dR[c] = fma(f * l, fma(Bi[3 * l + c], ck, -Ai[3 * l + c] * sk), dR[c]);
+                        }
+                        const double cn = ck * c1 - sk * s1;
+                        sk = sk * c1 + ck * s1;
+                        ck = cn;
+                    }
+                    for (int c = 0; c < 3; ++c) {
+                        y[c] = fma(lb[i], R[c], y[c]);
+                        yt[c] = fma(dlb[i], R[c], yt[c]);
+                        yh[c] = fma(lb[i], dR[c], yh[c]);
+                    }
+                }
+                // features of the trig cardinal basis: C_j(th) = sum_m f_m(th) phi_m(th_j) with
+                // f = (1, 2cos th, 2sin th, ..., 2cos (N/2-1)th, 2sin (N/2-1)th, cos(N th/2)) / N
+                {
+                    const double invN = 1.0 / nt;
+                    Cb[0] = invN;
+                    double ck = c1, sk = s1;
+                    for (int l = 1; l < nt / 2; ++l) {
+                        Cb[2 * l - 1] = 2.0 * invN * ck;
+                        Cb[2 * l] = 2.0 * invN * sk;
+                        const double cn = ck * c1 - sk * s1;
+                        sk = sk * c1 + ck * s1;
+                        ck = cn;
+                    }
+                    Cb[nt - 1] = invN * ck;                   // ck = cos(N th / 2) here
+                }
                 // outward normal (R8): n = y_th x y_t / |.|, J = |y_th x y_t|
                 const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
                                       yh[0] * yt[1] - yh[1] * yt[0]};
@@ -487,11 +566,22 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             __syncthreads();
         }
         // ---------------- write the block: [tdim][node (i,j)][sdim]
+        // back from the feature basis to the nodal basis: B[(q2,i)][j] = sum_m Bacc[(q2,i)][m] phi_m(th_j),
+        // phi = (1, cos th_j, sin th_j, ..., cos (N/2-1)th_j, sin (N/2-1)th_j, (-1)^j)
         double* Bp = blocks + (boff ? boff[p] : p * (int64_t)TD * Nn * TD);
         for (int o = tid; o < NG * Nn; o += kQThreads) {
-            const int q2 = o / Nn, ij = o % Nn;
+            const int q2 = o / Nn, ij = o % Nn, i = ij / nt, j = ij % nt;
+            const double* Fr = Bacc + (q2 * ns + i) * nt;
+            double acc = Fr[0];
+            int idx = 0;
+            for (int l = 1; l < nt / 2; ++l) {
+                idx += j;
+                if (idx >= nt) idx -= nt;
+                acc = fma(Fr[2 * l - 1], TC[idx], fma(Fr[2 * l], TS[idx], acc));
+            }
+            acc = fma((j & 1) ? -1.0 : 1.0, Fr[nt - 1], acc);
             const int a = q2 / TD, b = q2 % TD;
-            Bp[(a * Nn + ij) * TD + b] = Bacc[o];
+            Bp[(a * Nn + ij) * TD + b] = acc;
         }
         __syncthreads();
     }
@@ -501,11 +591,15 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
 
 using namespace slb;
 
+// One launch per panel size class (ragged panels: the shared-memory layout is sized by the class's
+// largest panel, so small panels keep several CTAs per SM -- c3v's 16 x 64 gap panels would otherwise
+// force one CTA per SM on every target).  classes: (ns_max, nt_max) per class; pclass [P] or NULL.
 static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
                                const int64_t* row_ptr, const int32_t* panel_idx, int ns, int nt,
                                const double* y_coarse, const double* eta_panel, int order, double beta,
                                double* blocks, cudaStream_t s, const int32_t* pnt, const int64_t* cn0,
-                               const int64_t* boff, const int32_t* pns) {
+                               const int64_t* boff, const int32_t* pns,
+                               const std::vector<std::pair<int, int>>& classes = {}, const int32_t* pclass = nullptr) {
     static QuadParams P;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
     P.dl = (kernel == SLB_STOKES_SL || kernel == SLB_LAPLACE_SL) ? 0.0 : 1.0;
@@ -524,11 +618,19 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     gl_nodes(P.qd, P.dx, P.dw);
     for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
     const int TD = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? 1 : 3;
-    const int Nn = ns * nt;   // (largest) panel
-    const size_t smem = sizeof(double) * ((size_t)Nn * 3 + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns + nt) +
-                                          2 * (size_t)nt) + sizeof(Cell) * kMaxCells;
-    SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
-    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto smem_of = [&](int ns_, int nt_) {
+        const size_t Nn = (size_t)ns_ * nt_;
+        const size_t Ysz = std::max(Nn * 3, (size_t)ns_ * (nt_ / 2 + 1) * 6);
+        return sizeof(double) * (Ysz + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns_ + nt_) +
+                                 2 * (size_t)nt_) + sizeof(Cell) * kMaxCells;
+    };
+    std::vector<std::pair<int, int>> cls = classes.empty() ? std::vector<std::pair<int, int>>{{ns, nt}} : classes;
+    size_t smem_max = 0;
+    for (auto& c : cls) {
+        SLB_REQUIRE(smem_of(c.first, c.second) <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
+        smem_max = std::max(smem_max, smem_of(c.first, c.second));
+    }
+    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     int* st = nullptr;
     SLB_CUDA(cudaMallocAsync(&st, sizeof(int), s));
     SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
@@ -543,10 +645,16 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         ++g_launch_count;
     }
     const FarKind kind = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? FAR_LAPLACE : FAR_STOKES_SLDL;
-    nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem, s>>>((int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx,
-                                                             y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff, pns, cp);
-    ++g_launch_count;
-    slb_status r = check_launch("nearquad_kernel");
+    slb_status r = SLB_OK;
+    for (int c = 0; c < (int)cls.size() && r == SLB_OK; ++c) {
+        P.ns = cls[c].first;
+        P.nt = cls[c].second;
+        nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem_of(P.ns, P.nt), s>>>(
+            (int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx, y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff,
+            pns, cp, pclass, c);
+        ++g_launch_count;
+        r = check_launch("nearquad_kernel");
+    }
     int h = 0;
     if (r == SLB_OK) {
         cudaError_t e = cudaMemcpyAsync(&h, st, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -622,13 +730,24 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
         SLB_REQUIRE(pk[p] >= 0 && pk[p] < n_panels, SLB_ERR_INVALID_ARG, "panel_idx entry outside [0, n_panels)");
         bo[p + 1] = bo[p] + (int64_t)TD * (c0[pk[p] + 1] - c0[pk[p]]) * TD;
     }
-    int32_t *pnt_d = nullptr, *pns_d = nullptr;
+    // size classes by nodes per panel: <= 192, <= 512, larger (each launch sized by its largest panel)
+    std::vector<int32_t> pc(n_panels);
+    std::vector<std::pair<int, int>> classes(3, {2, 4});
+    for (int64_t k = 0; k < n_panels; ++k) {
+        const int nn = panel_ns[k] * panel_nt[k];
+        const int c = nn <= 192 ? 0 : (nn <= 512 ? 1 : 2);
+        pc[k] = c;
+        classes[c].first = std::max(classes[c].first, (int)panel_ns[k]);
+        classes[c].second = std::max(classes[c].second, (int)panel_nt[k]);
+    }
+    int32_t *pnt_d = nullptr, *pns_d = nullptr, *pc_d = nullptr;
     int64_t *c0_d = nullptr, *bo_d = nullptr;
-    auto cleanup = [&]() { cudaFree(pnt_d); cudaFree(pns_d); cudaFree(c0_d); cudaFree(bo_d); };
+    auto cleanup = [&]() { cudaFree(pnt_d); cudaFree(pns_d); cudaFree(c0_d); cudaFree(bo_d); cudaFree(pc_d); };
     if (cudaMalloc(&pnt_d, sizeof(int32_t) * n_panels) != cudaSuccess ||
         cudaMalloc(&pns_d, sizeof(int32_t) * n_panels) != cudaSuccess ||
         cudaMalloc(&c0_d, sizeof(int64_t) * (n_panels + 1)) != cudaSuccess ||
-        cudaMalloc(&bo_d, sizeof(int64_t) * (nnz + 1)) != cudaSuccess) {
+        cudaMalloc(&bo_d, sizeof(int64_t) * (nnz + 1)) != cudaSuccess ||
+        cudaMalloc(&pc_d, sizeof(int32_t) * n_panels) != cudaSuccess) {
         cleanup();
         set_error("slb_nearcorr_quad_ragged: out of device memory");
         return SLB_ERR_OOM;
@@ -637,8 +756,9 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
     cudaMemcpy(pns_d, panel_ns, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
     cudaMemcpy(c0_d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
     cudaMemcpy(bo_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice);
+    cudaMemcpy(pc_d, pc.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
     slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse, eta_panel,
-                                order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d);
+                                order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d, classes, pc_d);
     cudaStreamSynchronize(s);
     cleanup();
     return r;

@@ -6,7 +6,7 @@ E = B - G U), and a GMRES solve (N2, slb_gmres) of the CFIE with the special blo
 time is CUDA-event (device) time after one warm-up call; rates are in the paper's units
 (unknowns per second of quadrature setup, P:L2315 / P:L2353 / P:L2527 / P:L2629).
 
-usage: python tools/setup_bench.py [names...]   (default: torus c2 c3) -> JSON lines on stdout
+usage: python tools/setup_bench.py [names...]   (default: torus torus_slender c2 c3 c3v) -> JSON lines
 """
 import json
 import os
@@ -52,22 +52,31 @@ def problem(name):
 def run(name):
     pr = problem(name)
     d = pr.sdim
-    res = {"workload": name, "nodes": pr.N, "unknowns": pr.N * d, "panels": pr.P, "grid": [pr.Ns, pr.Nt],
-           "near_pairs": pr.nnz, "block_shape": [pr.tdim, pr.Nn * d]}
-    # N3: near lists on the GPU (2 L_k rule + own panel)
-    own = cu(np.where(np.arange(pr.T) < pr.n_on, np.arange(pr.T) // pr.Nn, -1).astype(np.int64), torch.int64)
-    x, y, rad = cu(pr.x_trg), cu(pr.y_c.reshape(pr.P, pr.Nn, 3)), cu(2.0 * pr.panel_len)
+    no = pr.node_off()
+    cnt = np.diff(no)
+    res = {"workload": name, "nodes": pr.N, "unknowns": pr.N * d, "panels": pr.P,
+           "grid": [pr.Ns, pr.Nt] if not pr.ragged else "ragged (N_s, N_th)", "near_pairs": pr.nnz,
+           "block_entries": pr.n_blocks_entries()}
+    # N3: near lists on the GPU (2 L_k rule + own panel); ragged panels padded with their first node
+    own_h = np.full(pr.T, -1, np.int64)
+    own_h[:pr.n_on] = np.repeat(np.arange(pr.P), cnt)
+    own = cu(own_h, torch.int64)
+    j = np.arange(cnt.max())[None, :]
+    ypad = pr.y_c[no[:-1, None] + np.where(j < cnt[:, None], j, 0)]
+    x, y, rad = cu(pr.x_trg), cu(ypad), cu(2.0 * pr.panel_len)
     ms, (rp, pi) = timed(lambda: S.slb_near_build(x, y, rad, own))
     res["near_build_ms"] = ms
     res["near_build_target_panel_tests_per_s"] = pr.T * pr.P / (ms * 1e-3)
     # N1: special-quadrature blocks, two rule orders
     trg_node = cu(np.where(np.arange(pr.T) < pr.n_on, np.arange(pr.T), -1).astype(np.int64), torch.int64)
     eta_panel = cu(pr.eta_body[pr.body_of_panel]) if pr.kernel == 2 else None
-    blocks = torch.empty(pr.nnz * pr.block_len, dtype=torch.float64, device="cuda")
+    blocks = torch.empty(pr.n_blocks_entries(), dtype=torch.float64, device="cuda")
     rp_d, pi_d = cu(pr.row_ptr, torch.int64), cu(pr.panel_idx, torch.int32)
+    rag = dict(panel_nt=pr.nt_of_panel(), panel_ns=pr.ns_of_panel()) if pr.ragged else {}
     for order in (8, 14):
-        ms, _ = timed(lambda: S.slb_nearcorr_quad(pr.kernel, x, rp_d, pi_d, pr.Ns, pr.Nt, y, blocks,
-                                                  trg_node=trg_node, eta_panel=eta_panel, order=order, beta=0.6))
+        ms, _ = timed(lambda: S.slb_nearcorr_quad(pr.kernel, x, rp_d, pi_d, pr.Ns, pr.Nt, cu(pr.y_c), blocks,
+                                                  trg_node=trg_node, eta_panel=eta_panel, order=order, beta=0.6,
+                                                  **rag))
         res[f"quad_order{order}_ms"] = ms
         res[f"quad_order{order}_unknowns_per_s"] = pr.N * d / (ms * 1e-3)
         res[f"quad_order{order}_blocks_per_s"] = pr.nnz / (ms * 1e-3)
@@ -95,5 +104,5 @@ def run(name):
 
 
 if __name__ == "__main__":
-    for nm in sys.argv[1:] or ["torus", "torus_slender", "c2", "c3"]:
+    for nm in sys.argv[1:] or ["torus", "torus_slender", "c2", "c3", "c3v"]:
         print(json.dumps(run(nm)), flush=True)
