@@ -152,20 +152,24 @@ class Problem:
 
 
 def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 2),
-              extra_targets=None, c1_rule=False, projector=False, rng=None, nt_panels=None, ns_panels=None):
+              extra_targets=None, c1_rule=False, projector=False, rng=None, nt_panels=None, ns_panels=None,
+              breaks=None):
     """nt_panels / ns_panels: optional lists (per body) of per-panel angular / GL orders (ragged,
-    NEXT N4); Nt, Ns are then the base orders and q the fine factors of every panel."""
+    NEXT N4); Nt, Ns are then the base orders and q the fine factors of every panel.  breaks: optional
+    list (per body) of panel breakpoints in s (adaptive panels); default uniform."""
     Ms, Mt = q[0] * Ns, q[1] * Nt
+    breaks = breaks if breaks is not None else [None] * len(bodies)
     ragged = nt_panels is not None or ns_panels is not None
     if ragged:
         nt_panels = nt_panels if nt_panels is not None else [np.full(P, Nt) for P in P_per_body]
         ns_panels = ns_panels if ns_panels is not None else [np.full(P, Ns) for P in P_per_body]
-        coarse = [discretize_ragged(b, P, np.asarray(ns), nt) for b, P, ns, nt in zip(bodies, P_per_body, ns_panels, nt_panels)]
-        fine = [discretize_ragged(b, P, q[0] * np.asarray(ns), q[1] * np.asarray(nt))
-                for b, P, ns, nt in zip(bodies, P_per_body, ns_panels, nt_panels)]
+        coarse = [discretize_ragged(b, P, np.asarray(ns), nt, br)
+                  for b, P, ns, nt, br in zip(bodies, P_per_body, ns_panels, nt_panels, breaks)]
+        fine = [discretize_ragged(b, P, q[0] * np.asarray(ns), q[1] * np.asarray(nt), br)
+                for b, P, ns, nt, br in zip(bodies, P_per_body, ns_panels, nt_panels, breaks)]
     else:
-        coarse = [discretize(b, P, Ns, Nt) for b, P in zip(bodies, P_per_body)]
-        fine = [discretize(b, P, Ms, Mt) for b, P in zip(bodies, P_per_body)]
+        coarse = [discretize(b, P, Ns, Nt, br) for b, P, br in zip(bodies, P_per_body, breaks)]
+        fine = [discretize(b, P, Ms, Mt, br) for b, P, br in zip(bodies, P_per_body, breaks)]
     cat = lambda L, a: np.ascontiguousarray(np.concatenate([getattr(g, a) for g in L], axis=0))
     y_c, n_c, w_c = cat(coarse, "y"), cat(coarse, "n"), cat(coarse, "w")
     y_f, n_f, w_f = cat(fine, "y"), cat(fine, "n"), cat(fine, "w")
@@ -188,7 +192,7 @@ def _assemble(name, kernel, seed, bodies: List[Body], P_per_body, Ns, Nt, q=(2, 
         x_trg = np.ascontiguousarray(np.concatenate([x_trg, extra_targets], axis=0))
     sdim = 1 if kernel == LAPLACE_DL else 3
     sigma = rng.standard_normal((y_c.shape[0], sdim))
-    L = np.concatenate([panel_arclength(b, P) for b, P in zip(bodies, P_per_body)])
+    L = np.concatenate([panel_arclength(b, P, br) for b, P, br in zip(bodies, P_per_body, breaks)])
     # first node of every GL ring: its centerline point and radius (ragged-safe: panels with fewer
     # rings repeat their first ring, which leaves the min over rings unchanged)
     nsmax = int(ns_k.max())
@@ -272,7 +276,7 @@ CONFIGS = ("c1", "c2", "c3", "c3v", "c4", "c5", "c5alt")
 
 
 def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_DL, eta=None, extra_targets=None,
-                       seed_offset=0, nt_panels=None, ns_panels=None):
+                       seed_offset=0, nt_panels=None, ns_panels=None, breaks=None):
     """Single torus (axis z, centre 0) with the 2 L_k near rule -- pin problems for the special
     quadrature (N1).  eta=None -> the CFIE value 1/(2 rho ln(1/rho)) for Stokes, the pure DL for
     Laplace; an explicit eta sets the single-layer weight of either kernel (0 -> pure DL)."""
@@ -281,7 +285,8 @@ def make_torus_problem(R=1.0, rho=0.1, panels=12, Ns=10, Nt=12, kernel=LAPLACE_D
     b = torus_body(R, rho)
     pr = _assemble("torus", kernel, seed, [b], [panels], Ns, Nt, extra_targets=extra_targets, rng=rng,
                    nt_panels=None if nt_panels is None else [np.asarray(nt_panels)],
-                   ns_panels=None if ns_panels is None else [np.asarray(ns_panels)])
+                   ns_panels=None if ns_panels is None else [np.asarray(ns_panels)],
+                   breaks=None if breaks is None else [np.asarray(breaks)])
     if eta is not None:       # Stokes eta S + D, or the Laplace combined field D + eta S_L
         pr.eta_body[:] = eta
         pr.eta_f[:] = eta

@@ -140,10 +140,21 @@ class Grid:
     Nt: int
 
 
-def discretize(body: Body, P: int, Ns: int, Nt: int) -> Grid:
+def _breaks(P, breaks):
+    """panel breakpoints in s: uniform [k/P, (k+1)/P) unless given (P+1 increasing values 0 .. 1)"""
+    if breaks is None:
+        return np.arange(P + 1) / P
+    b = np.asarray(breaks, dtype=np.float64)
+    assert b.shape == (P + 1,) and b[0] == 0.0 and b[-1] == 1.0 and np.all(np.diff(b) > 0)
+    return b
+
+
+def discretize(body: Body, P: int, Ns: int, Nt: int, breaks=None) -> Grid:
+    """breaks: optional panel breakpoints in s (adaptive panels); default uniform"""
     t, wgl = gauss_legendre_np(Ns)
-    k = np.arange(P)[:, None]
-    s = ((k + (t[None, :] + 1) / 2) / P)                      # [P, Ns]
+    b = _breaks(P, breaks)
+    a, h = b[:-1, None], (b[1:] - b[:-1])[:, None]
+    s = a + h * (t[None, :] + 1) / 2                           # [P, Ns]
     th = 2 * np.pi * np.arange(Nt) / Nt                        # [Nt]
     S = np.broadcast_to(s[:, :, None], (P, Ns, Nt)).reshape(-1)
     TH = np.broadcast_to(th[None, None, :], (P, Ns, Nt)).reshape(-1)
@@ -153,7 +164,7 @@ def discretize(body: Body, P: int, Ns: int, Nt: int) -> Grid:
     cr = _cross(yt, ys)
     J = np.sqrt(np.sum(cr * cr, axis=-1))
     n = cr / J[:, None]
-    wpan = np.broadcast_to((wgl / (2 * P))[None, :, None], (P, Ns, Nt)).reshape(-1)
+    wpan = np.broadcast_to((wgl[None, :] * h / 2)[:, :, None], (P, Ns, Nt)).reshape(-1)
     w = J * wpan * (2 * np.pi / Nt)
     xc = body.xc(S)
     assert np.all(np.sum(n * (y - xc), axis=-1) > 0), "normals must point outward (S:L34)"
@@ -161,7 +172,7 @@ def discretize(body: Body, P: int, Ns: int, Nt: int) -> Grid:
                 J=J, s=S.copy(), th=TH.copy(), xc=xc, P=P, Ns=Ns, Nt=Nt)
 
 
-def discretize_ragged(body: Body, P: int, Ns, nt_panels) -> Grid:
+def discretize_ragged(body: Body, P: int, Ns, nt_panels, breaks=None) -> Grid:
     """Per-panel orders (§3.1: element k has N_s^(k) x N_th^(k) nodes).
     Ns: int or [P] array; nt_panels: [P].  Layout [panel][i][j], panel k contributing
     N_s^(k) N_th^(k) nodes; the node recipe per panel is discretize()'s.  Grid.Ns/Nt are 0 (ragged)."""
@@ -175,7 +186,7 @@ def discretize_ragged(body: Body, P: int, Ns, nt_panels) -> Grid:
     for k in range(P):
         ns, nt = int(ns_panels[k]), int(nt_panels[k])
         if (ns, nt) not in cache:
-            cache[(ns, nt)] = discretize(body, P, ns, nt)
+            cache[(ns, nt)] = discretize(body, P, ns, nt, breaks)
         g = cache[(ns, nt)]
         a, b = k * ns * nt, (k + 1) * ns * nt
         for f in fields:
@@ -184,13 +195,14 @@ def discretize_ragged(body: Body, P: int, Ns, nt_panels) -> Grid:
     return Grid(P=P, Ns=0, Nt=0, **cat)
 
 
-def panel_arclength(body: Body, P: int) -> np.ndarray:
+def panel_arclength(body: Body, P: int, breaks=None) -> np.ndarray:
     """Centerline arc length of each panel by 16-point GL."""
     t, wgl = gauss_legendre_np(16)
-    k = np.arange(P)[:, None]
-    s = (k + (t[None, :] + 1) / 2) / P
+    b = _breaks(P, breaks)
+    a, h = b[:-1, None], (b[1:] - b[:-1])[:, None]
+    s = a + h * (t[None, :] + 1) / 2
     sp = np.sqrt(np.sum(body.dxc(s) ** 2, axis=-1))
-    return np.sum(sp * wgl[None, :], axis=1) / (2 * P)
+    return np.sum(sp * wgl[None, :] * h / 2, axis=1)
 
 
 def centerline_min_distance(a: Body, b: Body, nsamp: int = 160) -> float:

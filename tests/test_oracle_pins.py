@@ -479,3 +479,21 @@ def test_n4_ragged_operator_vs_dense_assembly():
         ffar = O.farfield(2, pr.x_trg[t:t + 1], pr.y_f[keep], pr.n_f[keep], pr.w_f[keep], sf_ref[keep],
                           eta=eta[keep])[0]
         np.testing.assert_allclose(uf[q] + un[q], ffar + bsig, rtol=0, atol=1e-11 * (1 + np.abs(ffar).max()))
+
+
+def test_graded_panels_geometry_and_gauss_law():
+    """adaptive (non-uniform) panels in s: the generator's weights still integrate the
+    torus area exactly and the Laplace DL of 1 is -1 inside / 0 outside"""
+    from synth.geometry import discretize, panel_arclength
+    b = torus_body(1.0, 0.1)
+    P = 320
+    h = np.geomspace(1.0, 2.5, P // 2)
+    br = np.concatenate([[0.0], np.cumsum(np.concatenate([h, h[::-1]]))])
+    br /= br[-1]
+    g = discretize(b, P, 10, 48, br)
+    assert abs(g.w.sum() - 4 * np.pi ** 2 * 0.1) < 1e-13
+    assert abs(panel_arclength(b, P, br).sum() - 2 * np.pi) < 1e-13
+    xin, xout = _interior_exterior()
+    u = O.farfield(1, np.concatenate([xin, xout]), g.y, g.n, g.w, np.ones(g.w.size))
+    np.testing.assert_allclose(u[:len(xin)], -1.0, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(u[len(xin):], 0.0, rtol=0, atol=1e-11)
