@@ -3,6 +3,7 @@
 #include <cmath>
 #include <string>
 #include <array>
+#include <memory>
 #include <map>
 #include <string>
 #include <vector>
@@ -94,7 +95,8 @@ slb_status slb_upsample(int64_t n_panels, int ns, int nt, int ms, int mt, int nc
     if (n_panels == 0) return SLB_OK;
     SLB_REQUIRE(sigma_coarse && sigma_fine, SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(check_sticky("slb_upsample") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
-    static InterpParams ip;   // 29 KB: not on the stack
+    std::unique_ptr<InterpParams> ipp(new InterpParams);   // 29 KB: heap, per call (thread-safe)
+    InterpParams& ip = *ipp;
     double* owned = nullptr;  // device copy of large interpolation matrices (freed after the launch)
     SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip, &owned), SLB_ERR_OOM, "interpolation matrices: allocation failed");
     slb_status st = upsample_launch(FAR_STOKES_SLDL, n_panels, ip, ncomp, sigma_coarse, sigma_fine, nullptr, nullptr, s);
@@ -133,10 +135,15 @@ slb_status slb_upsample_ragged(int64_t n_panels, const int32_t* ns, const int32_
     }
     std::vector<int32_t> flat;
     for (auto& g : groups) flat.insert(flat.end(), g.second.begin(), g.second.end());
-    cudaMemcpy(c0d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
-    cudaMemcpy(f0d, f0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
-    cudaMemcpy(pl, flat.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
-    static InterpParams ip;
+    if (cudaMemcpy(c0d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(f0d, f0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pl, flat.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cleanup();
+        set_error("slb_upsample_ragged: copying the panel tables failed");
+        return SLB_ERR_CUDA;
+    }
+    std::unique_ptr<InterpParams> ipp(new InterpParams);
+    InterpParams& ip = *ipp;
     std::vector<double*> owned;
     int64_t off = 0;
     for (auto& g : groups) {
@@ -236,7 +243,8 @@ slb_status slb_nearcorr_fold(slb_kernel kernel, int64_t n_trg, const double* x_t
                 SLB_ERR_UNSUPPORTED, "grid beyond compiled limits");
     if (n_trg == 0) return SLB_OK;
     SLB_REQUIRE(x_trg && row_ptr && y_fine && n_fine && w_fine, SLB_ERR_INVALID_ARG, "null pointer");
-    static InterpParams ip;
+    std::unique_ptr<InterpParams> ipp(new InterpParams);
+    InterpParams& ip = *ipp;
     double* owned = nullptr;
     SLB_REQUIRE(make_interp(ns, nt, ms, mt, &ip, &owned), SLB_ERR_OOM, "interpolation matrices: allocation failed");
     FarKind kind = kernel == SLB_LAPLACE_DL ? ((eta_fine || eta > 0.0) ? FAR_LAPLACE_SLDL : FAR_LAPLACE)

@@ -23,6 +23,7 @@
 // One CTA per target row; fixed summation order -> deterministic.
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <string>
 #include <vector>
 #include "common.cuh"
@@ -600,7 +601,8 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                double* blocks, cudaStream_t s, const int32_t* pnt, const int64_t* cn0,
                                const int64_t* boff, const int32_t* pns,
                                const std::vector<std::pair<int, int>>& classes = {}, const int32_t* pclass = nullptr) {
-    static QuadParams P;
+    std::unique_ptr<QuadParams> Pp(new QuadParams);      // 10 KB: heap, per call (thread-safe)
+    QuadParams& P = *Pp;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
     P.dl = (kernel == SLB_STOKES_SL || kernel == SLB_LAPLACE_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
@@ -752,11 +754,15 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
         set_error("slb_nearcorr_quad_ragged: out of device memory");
         return SLB_ERR_OOM;
     }
-    cudaMemcpy(pnt_d, panel_nt, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
-    cudaMemcpy(pns_d, panel_ns, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
-    cudaMemcpy(c0_d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice);
-    cudaMemcpy(bo_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice);
-    cudaMemcpy(pc_d, pc.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice);
+    if (cudaMemcpy(pnt_d, panel_nt, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pns_d, panel_ns, sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c0_d, c0.data(), sizeof(int64_t) * (n_panels + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(bo_d, bo.data(), sizeof(int64_t) * (nnz + 1), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(pc_d, pc.data(), sizeof(int32_t) * n_panels, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cleanup();
+        set_error("slb_nearcorr_quad_ragged: copying the panel tables failed");
+        return SLB_ERR_CUDA;
+    }
     slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse, eta_panel,
                                 order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d, classes, pc_d);
     cudaStreamSynchronize(s);

@@ -193,11 +193,11 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
                    cudaMalloc(&op->lf0_d, sizeof(int64_t) * (Pl + 1)) == cudaSuccess &&
                    cudaMalloc(&op->pbucket_d, sizeof(int32_t) * P) == cudaSuccess;
         if (okm) {
-            cudaMemcpy(op->cn0_d, op->cn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice);
-            cudaMemcpy(op->fn0_d, op->fn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice);
-            cudaMemcpy(op->lc0_d, lc.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
-            cudaMemcpy(op->lf0_d, lf.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice);
-            cudaMemcpy(op->pbucket_d, pb.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice);
+            okm = cudaMemcpy(op->cn0_d, op->cn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(op->fn0_d, op->fn0.data(), sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(op->lc0_d, lc.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(op->lf0_d, lf.data(), sizeof(int64_t) * (Pl + 1), cudaMemcpyHostToDevice) == cudaSuccess &&
+                  cudaMemcpy(op->pbucket_d, pb.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice) == cudaSuccess;
             for (int bi = 0; bi < (int)op->buckets.size(); ++bi) {
                 auto& b = op->buckets[bi];
                 std::vector<int32_t> pl;
@@ -205,12 +205,14 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
                     if (pb[d->panel_begin + q] == bi) pl.push_back((int32_t)q);
                 if (pl.empty()) continue;
                 okm = okm && cudaMalloc(&b.plist_d, sizeof(int32_t) * pl.size()) == cudaSuccess;
-                if (okm) cudaMemcpy(b.plist_d, pl.data(), sizeof(int32_t) * pl.size(), cudaMemcpyHostToDevice);
+                if (okm)
+                    okm = cudaMemcpy(b.plist_d, pl.data(), sizeof(int32_t) * pl.size(), cudaMemcpyHostToDevice) ==
+                          cudaSuccess;
             }
         }
         if (!okm) {
             free_op(op);
-            set_error("slb_operator_create: out of device memory (ragged tables)");
+            set_error("slb_operator_create: allocating / copying the ragged tables failed");
             return SLB_ERR_OOM;
         }
     } else {

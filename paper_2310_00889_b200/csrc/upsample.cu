@@ -178,11 +178,8 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     }
     const size_t smem = smem_of(orows, gmats);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "upsample: grid too large for shared memory");
-    static size_t smem_set = 0;
-    if (smem > 48 * 1024 && smem > smem_set) {
+    if (smem > 48 * 1024)
         SLB_CUDA(cudaFuncSetAttribute(upsample_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-    }
     // one panel per CTA and pass; enough CTAs for every SM to hold several
     const unsigned grid = (unsigned)std::min<int64_t>(n_panels, (int64_t)num_sms() * 16);
     upsample_dmma_kernel<<<grid, kUpWarps * 32, smem, s>>>((int)kind, nc, n_panels, ip, sigma_coarse, sigma_fine, sc,
