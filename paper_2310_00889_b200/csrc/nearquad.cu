@@ -18,10 +18,13 @@
 //   * on-surface targets (d = 0): the four cells meeting at the node are integrated with the Duffy
 //     transform (two triangles each, Jacobian u cancels the 1/r singularity), refined until their
 //     aspect ratio and size are moderate;
-//   * q x q Gauss-Legendre per regular cell, 2 q_d^2 nodes per Duffy cell; the contraction with
-//     the basis is batched (128 nodes at a time) through shared memory.
-// One CTA per target row; fixed summation order -> deterministic.
+//   * q x q Gauss-Legendre per regular cell, 2 q_d^2 nodes per Duffy cell; the contraction with the
+//     basis runs on the FP64 tensor cores: Duffy nodes in batches of 128 through shared memory,
+//     regular cells sum-factorized (theta features first, then the Lagrange rows: the tensor-grid
+//     rule makes the per-node cost NG nt (1 + ns / q) instead of NG nt ns).
+// One CTA (16 warps) per target row; fixed summation order -> deterministic.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <memory>
 #include <string>
@@ -30,13 +33,14 @@
 
 namespace slb {
 
-constexpr int kQThreads = 128;
+constexpr int kQBatch = 128;     // Duffy-rule nodes per batch (sizes the per-node scratch region)
 constexpr int kMaxCells = 768;
 constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
 
 constexpr int kTri = kMaxNsQ * (kMaxNsQ + 1) / 2;   // GL tables for every n <= kMaxNsQ, at n (n-1) / 2
 struct QuadParams {
     int ns, nt, q, qd;        // ns, nt: the largest panel orders of the launch (shared-memory layout)
+    int region, nb;           // per-node / per-cell scratch (doubles); regular cells per Bacc update
     double beta;
     double dl;                // weight of the double layer: 1, or 0 for the pure single layer (SLB_STOKES_SL)
     double tgl[kTri];         // GL nodes on [-1,1] of every order n: tgl[n (n-1)/2 + i]
@@ -48,9 +52,14 @@ struct QuadParams {
 struct Cell {
     double t0, t1, h0, h1;    // parameter rectangle (t in [-1,1], th relative to th*)
     int duffy;                // 0 regular; 1 Duffy with singular corner (t*, th*)
-    int nodes;
-    int offset;
 };
+struct CellBox {              // accepted cell in shared memory; Duffy cells at the front, regular at the back
+    double t0, t1, h0, h1;
+};
+
+// shared-memory leading dimension for a DMMA operand row of n doubles: = 8 (mod 16), so the four
+// k-rows of an m8n8k4 B fragment fall into disjoint bank halves (2 wavefronts per load instead of 4)
+__host__ __device__ constexpr int ld_pad(int n) { return ((n + 7) / 16) * 16 + 8; }
 
 // Lagrange basis l_i(t) and l_i'(t) (barycentric second form + derivative formula)
 // tg / lm: the panel order's GL nodes and barycentric weights (QuadParams tables)
@@ -229,7 +238,156 @@ nearquad_cp_kernel(int64_t T, const double* __restrict__ x_trg, const int64_t* _
     cp[2 * p + 1] = hs;
 }
 
-__global__ void __launch_bounds__(kQThreads)
+// features of the trig cardinal basis at th (c1, s1 = cos th, sin th): C_j(th) = sum_m f_m(th) phi_m(th_j),
+// f = (1, 2cos th, 2sin th, ..., 2cos (N/2-1)th, 2sin (N/2-1)th, cos(N th/2)) / N
+__device__ __forceinline__ void trig_features(int nt, double c1, double s1, double* Cb) {
+    const double invN = 1.0 / nt;
+    Cb[0] = invN;
+    double ck = c1, sk = s1;
+    for (int l = 1; l < nt / 2; ++l) {
+        Cb[2 * l - 1] = 2.0 * invN * ck;
+        Cb[2 * l] = 2.0 * invN * sk;
+        const double cn = ck * c1 - sk * s1;
+        sk = sk * c1 + ck * s1;
+        ck = cn;
+    }
+    Cb[nt - 1] = invN * ck;                   // ck = cos(N th / 2) here
+}
+
+__device__ __forceinline__ void point_kernel(int kind, const double* y, const double* yt, const double* yh, double W,
+                                             double x0, double x1, double x2, double eta, double dlw, double* G);
+
+// kernel x weight at one quadrature node (t given by its Lagrange values lb, dlb; angle th; rule
+// weight W): surface point and tangents from the rings' Fourier modes FA / FB [ns][H][3] (modes <= K),
+// outward normal (R8) n = y_th x y_t / |.|, J = |y_th x y_t|; G[NG] = K(x - y; n) W J.
+__device__ __forceinline__ void node_kernel(int kind, int ns, int nt, int K, int H, const double* FA, const double* FB,
+                                            const double* lb, const double* dlb, double c1, double s1, double W,
+                                            double x0, double x1, double x2, double eta, double dlw, double* G) {
+    double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
+    for (int i = 0; i < ns; ++i) {                // ring i at th, and d/dth, from its modes
+        const double* Ai = FA + i * H * 3;
+        const double* Bi = FB + i * H * 3;
+        double R[3] = {Ai[0], Ai[1], Ai[2]}, dR[3] = {0, 0, 0};
+        double ck = c1, sk = s1;
+        for (int l = 1; l <= K; ++l) {
+            const double f = (2 * l == nt) ? 1.0 : 2.0;
+            for (int c = 0; c < 3; ++c) {
+                R[c] = fma(f, fma(Ai[3 * l + c], ck, Bi[3 * l + c] * sk), R[c]);
+                dR[c] = fma(f * l, fma(Bi[3 * l + c], ck, -Ai[3 * l + c] * sk), dR[c]);
+            }
+            const double cn = ck * c1 - sk * s1;
+            sk = sk * c1 + ck * s1;
+            ck = cn;
+        }
+        const double li = lb[i], dli = dlb[i];
+        for (int c = 0; c < 3; ++c) {
+            y[c] = fma(li, R[c], y[c]);
+            yt[c] = fma(dli, R[c], yt[c]);
+            yh[c] = fma(li, dR[c], yh[c]);
+        }
+    }
+    point_kernel(kind, y, yt, yh, W, x0, x1, x2, eta, dlw, G);
+}
+
+// G[NG] = K(x - y; n) W J at a surface point y with tangents yt, yh (n = y_th x y_t / |.|, J = |.|)
+__device__ __forceinline__ void point_kernel(int kind, const double* y, const double* yt, const double* yh, double W,
+                                             double x0, double x1, double x2, double eta, double dlw, double* G) {
+    const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
+                          yh[0] * yt[1] - yh[1] * yt[0]};
+    const double J = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+    const double nrm[3] = {cr[0] / J, cr[1] / J, cr[2] / J};
+    const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
+    const double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+    const double wJ = W * J;
+    const int NG = (kind == FAR_LAPLACE) ? 1 : 9;
+    for (int q2 = 0; q2 < NG; ++q2) G[q2] = 0.0;
+    if (r2 > 0.0) {
+        const double ir = 1.0 / sqrt(r2);
+        const double rn = r[0] * nrm[0] + r[1] * nrm[1] + r[2] * nrm[2];
+        if (kind == FAR_LAPLACE) {
+            G[0] = (dlw * rn * ir * ir * ir + eta * ir) / (4.0 * kPi) * wJ;
+        } else {
+            const double ir3 = ir * ir * ir;
+            const double sl = eta / (8.0 * kPi), dl = dlw * 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    G[a * 3 + b] = (sl * ((a == b ? ir : 0.0) + r[a] * r[b] * ir3) + dl * r[a] * r[b]) * wJ;
+        }
+    }
+}
+
+// C(m, n) (+)= sum_{k < Kn} A(m, k) B(k, n) for m < M, n < N on the FP64 tensor cores (DMMA m8n8k4,
+// K padded with zeros).  Row-dependent address parts are computed once per work unit: ra = arow(m),
+// then A(m, k) = fa(ra, k); rc = crow(m), then C(m, n) = fc(rc, n) (a shared-memory reference).  Work
+// unit of a warp: one 8-row strip x up to 8 column tiles, the A fragment loaded once per k-step.
+// acc = false: C is overwritten.
+template <int NT, class FRA, class FA, class FB, class FRC, class FC>
+__device__ __forceinline__ void dmma_gemm(int M, int N, int Kn, bool acc, FRA arow, FA fa, FB fb, FRC crow, FC fc) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, fg = lane >> 2, ftq = lane & 3;
+    const int mtl = (M + 7) / 8, ntl = (N + 7) / 8, ngrp = (ntl + 7) / 8;
+    for (int u = warp; u < mtl * ngrp; u += NT / 32) {
+        const int m0 = (u / ngrp) * 8, ct0 = (u % ngrp) * 8, nct = min(8, ntl - ct0);
+        const int row = m0 + fg;
+        const bool rok = row < M;
+        const int ra = rok ? arow(row) : 0, rc = rok ? crow(row) : 0;
+        double d0[8], d1[8];
+#pragma unroll
+        for (int tn = 0; tn < 8; ++tn) {
+            const int oc = (ct0 + tn) * 8 + 2 * ftq;           // output columns oc, oc+1 of row m0+fg
+            d0[tn] = (acc && tn < nct && rok && oc < N) ? fc(rc, oc) : 0.0;
+            d1[tn] = (acc && tn < nct && rok && oc + 1 < N) ? fc(rc, oc + 1) : 0.0;
+        }
+        for (int k0 = 0; k0 < Kn; k0 += 4) {
+            const int k = k0 + ftq;
+            const double a = (rok && k < Kn) ? fa(ra, k) : 0.0;
+#pragma unroll
+            for (int tn = 0; tn < 8; ++tn) {
+                if (tn < nct) {                                  // warp-uniform
+                    const int col = (ct0 + tn) * 8 + fg;         // B column of this lane
+                    const double b = (k < Kn && col < N) ? fb(k, col) : 0.0;
+                    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                        : "+d"(d0[tn]), "+d"(d1[tn]) : "d"(a), "d"(b));
+                }
+            }
+        }
+#pragma unroll
+        for (int tn = 0; tn < 8; ++tn) {
+            const int oc = (ct0 + tn) * 8 + 2 * ftq;
+            if (tn < nct && rok && oc < N) fc(rc, oc) = d0[tn];
+            if (tn < nct && rok && oc + 1 < N) fc(rc, oc + 1) = d1[tn];
+        }
+    }
+}
+
+// regular-cell scratch (doubles) for nb cells per Bacc update and all q t rows at once
+__host__ __device__ inline int regular_need(int q, int ns, int nt, int NG, int nb) {
+    return nb * q * ld_pad(nt) + ns * ld_pad(nb * q * NG) + 6 * ns * q + q * (4 * ld_pad(ns) + ld_pad(q * NG));
+}
+// one cell per update, t rows in chunks: the chunk `ac` that fits `region` (< 1: does not fit)
+__host__ __device__ inline int regular_chunk(int q, int ns, int nt, int NG, int region) {
+    const int fixed = q * ld_pad(nt) + ns * ld_pad(q * NG) + 6 * ns * q;
+    const int per_a = 4 * ld_pad(ns) + ld_pad(q * NG);
+    const int ac = (region - fixed) / per_a;
+    return ac < q ? ac : q;
+}
+
+// SLB_NQ_PROFILE (dev builds only): per-phase SM clocks of thread 0, summed over CTAs, printed by nearquad_run
+#ifdef SLB_NQ_PROFILE
+__device__ unsigned long long g_nq_prof[16], g_nq_cnt[4];
+#define NQ_MARK(k)                                                                                       \
+    if (threadIdx.x == 0) {                                                                              \
+        const long long nq_now = clock64();                                                              \
+        atomicAdd(&g_nq_prof[k], (unsigned long long)(nq_now - nq_tp));                                  \
+        nq_tp = nq_now;                                                                                  \
+    }
+#else
+#define NQ_MARK(k)
+#endif
+
+// NT threads per (target row) CTA: 256 (two CTAs per SM) for panel classes whose layout fits 113 KB,
+// else 512 (one CTA per SM, 16 warps to hide the phase latencies)
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : 1)
 nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int64_t* __restrict__ trg_node,
                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ panel_idx,
                 const double* __restrict__ y_coarse, const double* __restrict__ eta_panel,
@@ -251,13 +409,13 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     double* Y = sm;
     double* Bacc = Y + Ysz;                           // [NG*ns][nt]  (Fourier-space accumulator)
     double* Gs = Bacc + NG * Nnm;                     // [128][NG]
-    double* Ls = Gs + kQThreads * NG;                 // [128][ns]
-    double* Cs = Ls + kQThreads * nsm;                // [128][nt]
-    double* TC = Cs + kQThreads * ntm;                // [ntm] cos(2 pi m / nt) of the current panel
+    double* Ls = Gs + kQBatch * NG;                   // [128][ns]
+    double* Cs = Ls + kQBatch * nsm;                  // [128][ld_pad(nt)]
+    double* TC = Gs + P.region;                       // [ntm] cos(2 pi m / nt) of the current panel
     double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
-    Cell* cells = reinterpret_cast<Cell*>(TS + ntm);
+    CellBox* cells = reinterpret_cast<CellBox*>(TS + ntm);
     __shared__ double s_par[8];                       // t*, th*, d, St, Sh, node-singular flag
-    __shared__ int s_ncell, s_ntot, s_fail, s_K;
+    __shared__ int s_ncell, s_ntot, s_nreg, s_fail, s_K;
     __shared__ unsigned long long s_amax;
     // per-thread scratch for the interpolation (registers / local)
     double lb[kMaxNsQ], dlb[kMaxNsQ], Cb[kMaxNtQ], dCb[kMaxNtQ];
@@ -266,6 +424,9 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     if (t >= T) return;
     const double x0 = x_trg[3 * t], x1 = x_trg[3 * t + 1], x2 = x_trg[3 * t + 2];
     const int64_t node = trg_node ? trg_node[t] : -1;
+#ifdef SLB_NQ_PROFILE
+    long long nq_tp = clock64();
+#endif
     for (int64_t p = row_ptr[t]; p < row_ptr[t + 1]; ++p) {
         const int64_t k = panel_idx[p];
         if (pclass && pclass[k] != cls) continue;             // another size class's launch
@@ -277,10 +438,11 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         // D + eta S_L), else 0 (pure D) or 1 (pure S_L, P.dl = 0)
         const double eta = (kind == FAR_STOKES_SLDL) ? (eta_panel ? eta_panel[k] : 1.0)
                                                      : (eta_panel ? eta_panel[k] : (P.dl == 0.0 ? 1.0 : 0.0));
-        for (int e = tid; e < Nn * 3; e += kQThreads) Y[e] = y_coarse[c0 * 3 + e];
-        for (int e = tid; e < nt; e += kQThreads) sincos(2.0 * kPi * e / nt, &TS[e], &TC[e]);
-        for (int e = tid; e < NG * Nn; e += kQThreads) Bacc[e] = 0.0;
+        for (int e = tid; e < Nn * 3; e += NT) Y[e] = y_coarse[c0 * 3 + e];
+        for (int e = tid; e < nt; e += NT) sincos(2.0 * kPi * e / nt, &TS[e], &TC[e]);
+        for (int e = tid; e < NG * Nn; e += NT) Bacc[e] = 0.0;
         __syncthreads();
+        NQ_MARK(0);
         // ---------------- closest point and the cell list (thread 0)
         if (tid == 0) {
             s_fail = 0;
@@ -304,7 +466,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             s_par[0] = ts; s_par[1] = hs; s_par[2] = d; s_par[3] = St; s_par[4] = Sh;
             // quadtree over the parameter rectangle [-1,1] x [hs - pi, hs + pi], split at (ts, hs)
             Cell stack[64];
-            int sp = 0, nc = 0, ntot = 0;
+            int sp = 0, nc = 0, nr = 0, ntot = 0;       // Duffy cells from the front, regular from the back
             const double T0[2] = {-1.0, ts}, T1[2] = {ts, 1.0};
             const double H0[2] = {-kPi, 0.0}, H1[2] = {0.0, kPi};
             for (int a = 0; a < 2; ++a)
@@ -350,11 +512,14 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                 }
                 accept = accept && (c.h1 - c.h0) <= hmax;
                 if (accept) {
-                    if (nc >= kMaxCells) { s_fail = 1; break; }
-                    c.nodes = c.duffy ? 2 * P.qd * P.qd : P.q * P.q;
-                    c.offset = ntot;
-                    ntot += c.nodes;
-                    cells[nc++] = c;
+                    if (nc + nr >= kMaxCells) { s_fail = 1; break; }
+                    const CellBox cb = {c.t0, c.t1, c.h0, c.h1};
+                    if (c.duffy) {
+                        ntot += 2 * P.qd * P.qd;
+                        cells[nc++] = cb;
+                    } else {
+                        cells[kMaxCells - 1 - nr++] = cb;
+                    }
                     continue;
                 }
                 if (sp + 4 > 64) { s_fail = 2; break; }
@@ -375,15 +540,20 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             }
             s_ncell = nc;
             s_ntot = ntot;
+            s_nreg = nr;
         }
         __syncthreads();
+        NQ_MARK(1);
         if (s_fail) {
             if (tid == 0) atomicOr(status, s_fail);
             __syncthreads();
             continue;
         }
         const double ts = s_par[0], hs = s_par[1];
-        const int nc = s_ncell, ntot = s_ntot;
+        const int ntot = s_ntot, nreg = s_nreg;   // Duffy-rule nodes, regular cells
+#ifdef SLB_NQ_PROFILE
+        if (tid == 0) { atomicAdd(&g_nq_cnt[0], (unsigned long long)s_nreg); atomicAdd(&g_nq_cnt[1], (unsigned long long)s_ntot); atomicAdd(&g_nq_cnt[2], 1ull); }
+#endif
         // ---------------- Fourier coefficients of every GL ring of the panel (trig interpolant in th):
         //   ring(th) = A_0 + 2 sum_{l=1}^{N/2-1} (A_l cos l th + B_l sin l th) + A_{N/2} cos(N th / 2),
         //   A_l = (1/N) sum_j Y_j cos(l th_j), B_l = (1/N) sum_j Y_j sin(l th_j).  Modes above K (the
@@ -394,7 +564,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         double* FB = Y + ns * H * 3;                  // [ns][H][3]
         if (tid == 0) { s_K = 0; s_amax = 0ull; }
         __syncthreads();
-        for (int e = tid; e < ns * H * 3; e += kQThreads) {
+        for (int e = tid; e < ns * H * 3; e += NT) {
             const int c = e % 3, l = (e / 3) % H, i = e / (3 * H);
             const double* Yr = y_coarse + (c0 + (int64_t)i * nt) * 3 + c;
             double a = 0.0, b = 0.0;
@@ -412,167 +582,225 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         __syncthreads();
         {
             const double tol = 1e-15 * __longlong_as_double((long long)s_amax);
-            for (int e = tid; e < ns * H * 3; e += kQThreads) {
+            for (int e = tid; e < ns * H * 3; e += NT) {
                 const int l = (e / 3) % H;
                 if (l > 0 && (fabs(FA[e]) > tol || fabs(FB[e]) > tol)) atomicMax(&s_K, l);
             }
         }
         __syncthreads();
+        NQ_MARK(2);
         const int K = s_K;
-        // ---------------- quadrature nodes in batches of kQThreads
-        for (int base = 0; base < ntot; base += kQThreads) {
+        // Bacc layout [ns][NG][nt]: row (i, q2) holds the feature coefficients of l_i(t) C_m(th) for the
+        // kernel component q2 -- so that the sum-factorized step (3b) below is ONE GEMM with N = NG nt.
+        // ---------------- (1) Duffy cells: nodes in batches of kQBatch (non-separable rule)
+        const int ldc = ld_pad(nt);
+        for (int base = 0; base < ntot; base += kQBatch) {
             const int g = base + tid;
             double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-            if (g < ntot) {
-                int lo = 0, hi = nc - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (cells[mid].offset <= g) lo = mid; else hi = mid - 1;
-                }
-                const Cell c = cells[lo];
-                const int li = g - c.offset;
-                double tt, hh, W;
-                if (!c.duffy) {
-                    const int a = li / P.q, b = li % P.q;
-                    const double ht = 0.5 * (c.t1 - c.t0), hh2 = 0.5 * (c.h1 - c.h0);
-                    tt = c.t0 + ht * (P.gx[a] + 1.0);
-                    hh = c.h0 + hh2 * (P.gx[b] + 1.0);
-                    W = P.gw[a] * P.gw[b] * ht * hh2;
-                } else {
-                    // rectangle with the singular corner at (ts, 0): corner C0, opposite corners
-                    const double ct = (c.t0 == ts) ? c.t0 : c.t1, ch = (c.h0 == 0.0) ? c.h0 : c.h1;
-                    const double ot = (c.t0 == ts) ? c.t1 : c.t0, oh = (c.h0 == 0.0) ? c.h1 : c.h0;
-                    const int tri = li / (P.qd * P.qd), r = li % (P.qd * P.qd);
-                    const int ia = r / P.qd, ib = r % P.qd;
-                    const double u = P.dx[ia], v = P.dx[ib];
-                    // triangle 0: C0, (ot, ch), (ot, oh); triangle 1: C0, (ot, oh), (ct, oh)
-                    double At, Ah, Bt, Bh;
-                    if (tri == 0) { At = ot - ct; Ah = 0.0; Bt = ot - ct; Bh = oh - ch; }
-                    else { At = ot - ct; Ah = oh - ch; Bt = 0.0; Bh = oh - ch; }
-                    tt = ct + u * (At + v * (Bt - At));
-                    hh = ch + u * (Ah + v * (Bh - Ah));
-                    W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
-                }
-                double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
+            if (tid < kQBatch && g < ntot) {
+                const CellBox c = cells[g / (2 * P.qd * P.qd)];     // every Duffy cell has 2 qd^2 nodes
+                const int li = g % (2 * P.qd * P.qd);
+                // rectangle with the singular corner at (ts, 0): corner C0, opposite corners
+                const double ct = (c.t0 == ts) ? c.t0 : c.t1, ch = (c.h0 == 0.0) ? c.h0 : c.h1;
+                const double ot = (c.t0 == ts) ? c.t1 : c.t0, oh = (c.h0 == 0.0) ? c.h1 : c.h0;
+                const int tri = li / (P.qd * P.qd), r = li % (P.qd * P.qd);
+                const int ia = r / P.qd, ib = r % P.qd;
+                const double u = P.dx[ia], v = P.dx[ib];
+                // triangle 0: C0, (ot, ch), (ot, oh); triangle 1: C0, (ot, oh), (ct, oh)
+                double At, Ah, Bt, Bh;
+                if (tri == 0) { At = ot - ct; Ah = 0.0; Bt = ot - ct; Bh = oh - ch; }
+                else { At = ot - ct; Ah = oh - ch; Bt = 0.0; Bh = oh - ch; }
+                const double tt = ct + u * (At + v * (Bt - At));
+                const double hh = ch + u * (Ah + v * (Bh - Ah));
+                const double W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
                 lagrange_eval(ns, tg, lm, tt, lb, dlb);
                 double c1, s1;
                 sincos(hs + hh, &s1, &c1);
-                for (int i = 0; i < ns; ++i) {                // ring i at th, and d/dth, from its modes
-                    const double* Ai = FA + i * H * 3;
-                    const double* Bi = FB + i * H * 3;
-                    double R[3] = {Ai[0], Ai[1], Ai[2]}, dR[3] = {0, 0, 0};
-                    double ck = c1, sk = s1;
-                    for (int l = 1; l <= K; ++l) {
-                        const double f = (2 * l == nt) ? 1.0 : 2.0;
-                        for (int c = 0; c < 3; ++c) {
-                            R[c] = fma(f, fma(Ai[3 * l + c], ck, Bi[3 * l + c] * sk), R[c]);
-                            dR[c] = fma(f * l, fma(Bi[3 * l + c], ck, -Ai[3 * l + c] * sk), dR[c]);
-                        }
-                        const double cn = ck * c1 - sk * s1;
-                        sk = sk * c1 + ck * s1;
-                        ck = cn;
-                    }
-                    for (int c = 0; c < 3; ++c) {
-                        y[c] = fma(lb[i], R[c], y[c]);
-                        yt[c] = fma(dlb[i], R[c], yt[c]);
-                        yh[c] = fma(lb[i], dR[c], yh[c]);
-                    }
-                }
-                // features of the trig cardinal basis: C_j(th) = sum_m f_m(th) phi_m(th_j) with
-                // f = (1, 2cos th, 2sin th, ..., 2cos (N/2-1)th, 2sin (N/2-1)th, cos(N th/2)) / N
-                {
-                    const double invN = 1.0 / nt;
-                    Cb[0] = invN;
-                    double ck = c1, sk = s1;
-                    for (int l = 1; l < nt / 2; ++l) {
-                        Cb[2 * l - 1] = 2.0 * invN * ck;
-                        Cb[2 * l] = 2.0 * invN * sk;
-                        const double cn = ck * c1 - sk * s1;
-                        sk = sk * c1 + ck * s1;
-                        ck = cn;
-                    }
-                    Cb[nt - 1] = invN * ck;                   // ck = cos(N th / 2) here
-                }
-                // outward normal (R8): n = y_th x y_t / |.|, J = |y_th x y_t|
-                const double cr[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2],
-                                      yh[0] * yt[1] - yh[1] * yt[0]};
-                const double J = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
-                const double nrm[3] = {cr[0] / J, cr[1] / J, cr[2] / J};
-                const double r[3] = {x0 - y[0], x1 - y[1], x2 - y[2]};
-                const double r2 = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
-                const double wJ = W * J;
-                if (r2 > 0.0) {
-                    const double ir = 1.0 / sqrt(r2);
-                    const double rn = r[0] * nrm[0] + r[1] * nrm[1] + r[2] * nrm[2];
-                    if (kind == FAR_LAPLACE) {
-                        G[0] = (P.dl * rn * ir * ir * ir + eta * ir) / (4.0 * kPi) * wJ;
-                    } else {
-                        const double ir3 = ir * ir * ir;
-                        const double sl = eta / (8.0 * kPi), dl = P.dl * 3.0 / (4.0 * kPi) * rn * ir3 * ir * ir;
-                        for (int a = 0; a < 3; ++a)
-                            for (int b = 0; b < 3; ++b)
-                                G[a * 3 + b] = (sl * ((a == b ? ir : 0.0) + r[a] * r[b] * ir3) + dl * r[a] * r[b]) * wJ;
-                    }
-                }
+                node_kernel(kind, ns, nt, K, H, FA, FB, lb, dlb, c1, s1, W, x0, x1, x2, eta, P.dl, G);
+                trig_features(nt, c1, s1, Cb);
                 for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = G[q2];
                 for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = lb[i];
-                for (int j = 0; j < nt; ++j) Cs[tid * nt + j] = Cb[j];
-            } else {
+                for (int j = 0; j < nt; ++j) Cs[tid * ldc + j] = Cb[j];
+            } else if (tid < kQBatch) {
                 for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = 0.0;
                 for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = 0.0;
-                for (int j = 0; j < nt; ++j) Cs[tid * nt + j] = 0.0;
+                for (int j = 0; j < nt; ++j) Cs[tid * ldc + j] = 0.0;
             }
             __syncthreads();
-            // contraction with the basis as a GEMM on the FP64 tensor cores (DMMA m8n8k4):
-            //   Bacc[(q2,i)][j] += sum_n W[(q2,i)][n] C[n][j],   W[(q2,i)][n] = G[n][q2] l_i(t_n)
-            // (nodes n past the batch end carry zeros); each warp owns whole 8x8 output tiles.
-            {
-                const int warp = tid >> 5, lane = tid & 31, fg = lane >> 2, ftq = lane & 3;
-                const int Mr = NG * ns, mtl = (Mr + 7) / 8, ntl = (nt + 7) / 8;   // ntl <= 8
-                // a warp owns whole 8-row strips and sweeps all column tiles with the A fragment
-                // (G l products) computed once per k-step
-                for (int strip = warp; strip < mtl; strip += kQThreads / 32) {
-                    const int m0 = strip * 8;
-                    const int row = m0 + fg;                       // A row of this lane
-                    const int q2 = row / ns, ia = row % ns;
-                    const bool rok = row < Mr;
-                    double d0[8], d1[8];
-#pragma unroll
-                    for (int tn = 0; tn < 8; ++tn) {
-                        const int oc = tn * 8 + 2 * ftq;           // output columns oc, oc+1 of row m0+fg
-                        d0[tn] = (tn < ntl && rok && oc < nt) ? Bacc[row * nt + oc] : 0.0;
-                        d1[tn] = (tn < ntl && rok && oc + 1 < nt) ? Bacc[row * nt + oc + 1] : 0.0;
-                    }
-                    for (int k0 = 0; k0 < kQThreads; k0 += 4) {
-                        const int n = k0 + ftq;
-                        const double a = rok ? Gs[n * NG + q2] * Ls[n * ns + ia] : 0.0;
-#pragma unroll
-                        for (int tn = 0; tn < 8; ++tn) {
-                            if (tn < ntl) {                        // warp-uniform
-                                const int col = tn * 8 + fg;       // B column of this lane
-                                const double b = col < nt ? Cs[n * nt + col] : 0.0;
-                                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                                             : "+d"(d0[tn]), "+d"(d1[tn]) : "d"(a), "d"(b));
+            // Bacc[(i,q2)][j] += sum_n G[n][q2] l_i(t_n) C[n][j]  (nodes past the batch end carry zeros)
+            dmma_gemm<NT>(ns * NG, nt, kQBatch, true,
+                      [&](int row) { return (row % NG) | ((row / NG) << 8); },
+                      [&](int ra, int k) { return Gs[k * NG + (ra & 255)] * Ls[k * ns + (ra >> 8)]; },
+                      [&](int k, int col) { return Cs[k * ldc + col]; },
+                      [&](int row) { return row * nt; },
+                      [&](int rc, int col) -> double& { return Bacc[rc + col]; });
+            __syncthreads();
+            NQ_MARK(3);
+        }
+        // ---------------- (2) regular cells: q x q tensor Gauss grids, contraction sum-factorized
+        //   U[i][(b,q2)]     = sum_a l_i(t_a) G[(a,b)][q2]       (GEMM: M = ns, N = q NG, K = q; t rows in chunks)
+        //   Bacc[(i,q2)][j] += sum_b U[i][(b,q2)] C_j(th_b)      (GEMM: M = ns NG, N = nt, K = q)
+        // i.e. q^2 NG ns + q NG ns nt multiply-adds per cell instead of q^2 NG ns nt.  The per-cell tables
+        // (features and rings at the q theta nodes, Lagrange rows at the t nodes) are built by all
+        // threads, one entry each; they live in the Duffy batch region (Gs..Cs).
+        {
+            const int q = P.q;
+            const int nb = P.nb;                      // cells per Bacc update (their U, C stacked along K)
+            const int ldC = ld_pad(nt), ldL = ld_pad(ns), ldG = ld_pad(q * NG), ldU = ld_pad(nb * q * NG);
+            const int ac = nb > 1 ? q : max(1, regular_chunk(q, ns, nt, NG, P.region));
+            double* Cc = Gs;                          // [nb q][ldC] features at the cells' th nodes
+            double* Uc = Cc + nb * q * ldC;           // [ns][ldU]   (cell, b, q2)
+            double* Rg = Uc + ns * ldU;               // [ns][6][q]  rings and d/dth at the th nodes
+            double* Lc = Rg + 6 * ns * q;             // [ac][ldL]   l_i(t_a)
+            double* dLc = Lc + ac * ldL;              // [ac][ldL]   l_i'(t_a)
+            double* Xc = dLc + ac * ldL;              // [ac][ldL]   t_a - t_i
+            double* iXc = Xc + ac * ldL;              // [ac][ldL]   1 / (t_a - t_i)
+            double* Gc = iXc + ac * ldL;              // [ac][ldG]   (b, q2): kernel x weight at the nodes
+            const int nl = nt / 2;                    // feature pairs (cos l th, sin l th), l = 1 .. nt/2
+            const int nparts = 4, lper = (nl + nparts - 1) / nparts;
+            for (int rc = 0; rc < nreg; ++rc) {
+                const CellBox c = cells[kMaxCells - 1 - rc];
+                const double ht = 0.5 * (c.t1 - c.t0), hh2 = 0.5 * (c.h1 - c.h0);
+                const int slot = rc % nb;
+                double* Ccs = Cc + slot * q * ldC;
+                for (int a0 = 0; a0 < q; a0 += ac) {
+                    const int na = min(ac, q - a0);
+                    if (a0 == 0) {
+                        // features C[b][m] (trig_features layout) by (b, quarter of the l range)
+                        for (int e = tid; e < q * nparts; e += NT) {
+                            const int b2 = e / nparts, l0 = 1 + (e % nparts) * lper, l1 = min(nl, l0 + lper - 1);
+                            const double th = hs + c.h0 + hh2 * (P.gx[b2] + 1.0);
+                            double* Cr = Ccs + b2 * ldC;
+                            const double invN = 1.0 / nt;
+                            if (l0 == 1) Cr[0] = invN;
+                            if (l0 <= l1) {
+                                double c1, s1, ck, sk;
+                                sincos(th, &s1, &c1);
+                                sincos(l0 * th, &sk, &ck);
+                                for (int l = l0; l <= l1; ++l) {
+                                    if (l < nl) { Cr[2 * l - 1] = 2.0 * invN * ck; Cr[2 * l] = 2.0 * invN * sk; }
+                                    else Cr[nt - 1] = invN * ck;                  // l = N/2: cos(N th / 2)
+                                    const double cn = ck * c1 - sk * s1;
+                                    sk = sk * c1 + ck * s1;
+                                    ck = cn;
+                                }
+                            }
+                        }
+                        // ring i at the q theta nodes from its Fourier modes (<= K): R_i(th_b), dR_i/dth (th_b)
+                        for (int e = tid; e < ns * q; e += NT) {
+                            const int i = e / q, b2 = e % q;
+                            double c1, s1;
+                            sincos(hs + c.h0 + hh2 * (P.gx[b2] + 1.0), &s1, &c1);
+                            const double* Ai = FA + i * H * 3;
+                            const double* Bi = FB + i * H * 3;
+                            double R[3] = {Ai[0], Ai[1], Ai[2]}, dR[3] = {0, 0, 0};
+                            double ck = c1, sk = s1;
+                            for (int l = 1; l <= K; ++l) {
+                                const double f = (2 * l == nt) ? 1.0 : 2.0;
+                                for (int cc = 0; cc < 3; ++cc) {
+                                    R[cc] = fma(f, fma(Ai[3 * l + cc], ck, Bi[3 * l + cc] * sk), R[cc]);
+                                    dR[cc] = fma(f * l, fma(Bi[3 * l + cc], ck, -Ai[3 * l + cc] * sk), dR[cc]);
+                                }
+                                const double cn = ck * c1 - sk * s1;
+                                sk = sk * c1 + ck * s1;
+                                ck = cn;
+                            }
+                            for (int cc = 0; cc < 3; ++cc) {
+                                Rg[(i * 6 + cc) * q + b2] = R[cc];
+                                Rg[(i * 6 + 3 + cc) * q + b2] = dR[cc];
                             }
                         }
                     }
-#pragma unroll
-                    for (int tn = 0; tn < 8; ++tn) {
-                        const int oc = tn * 8 + 2 * ftq;
-                        if (tn < ntl && rok && oc < nt) Bacc[row * nt + oc] = d0[tn];
-                        if (tn < ntl && rok && oc + 1 < nt) Bacc[row * nt + oc + 1] = d1[tn];
+                    // Lagrange rows, barycentric (as lagrange_eval): differences and their reciprocals
+                    for (int e = tid; e < na * ns; e += NT) {
+                        const int a2 = e / ns, i = e % ns;
+                        const double X = (c.t0 + ht * (P.gx[a0 + a2] + 1.0)) - tg[i];
+                        Xc[a2 * ldL + i] = X;
+                        iXc[a2 * ldL + i] = 1.0 / X;
                     }
+                    __syncthreads();
+                    NQ_MARK(6);
+                    for (int e = tid; e < na * ns; e += NT) {
+                        const int a2 = e / ns, i = e % ns;
+                        const double* X = Xc + a2 * ldL;
+                        const double* iX = iXc + a2 * ldL;
+                        int hit = -1;
+                        double den = 0.0, dden = 0.0;
+                        for (int k = 0; k < ns; ++k) {
+                            if (fabs(X[k]) < 1e-15) hit = k;
+                            const double ck = lm[k] * iX[k];
+                            den += ck;
+                            dden -= ck * iX[k];
+                        }
+                        double l, dl;
+                        if (hit >= 0) {                   // t_a on a node: l = delta, l' by the node formula
+                            l = (i == hit) ? 1.0 : 0.0;
+                            if (i != hit) {
+                                dl = (lm[i] / lm[hit]) / (tg[hit] - tg[i]);
+                            } else {
+                                dl = 0.0;
+                                for (int k = 0; k < ns; ++k)
+                                    if (k != hit) dl -= (lm[k] / lm[hit]) / (tg[hit] - tg[k]);
+                            }
+                        } else {
+                            const double ci = lm[i] * iX[i], dci = -ci * iX[i], iden = 1.0 / den;
+                            l = ci * iden;
+                            dl = (dci * den - ci * dden) * iden * iden;
+                        }
+                        Lc[a2 * ldL + i] = l;
+                        dLc[a2 * ldL + i] = dl;
+                    }
+                    __syncthreads();
+                    NQ_MARK(7);
+                    for (int n = tid; n < na * q; n += NT) {
+                        const int a2 = n / q, b2 = n % q;
+                        const double* la = Lc + a2 * ldL;
+                        const double* dla = dLc + a2 * ldL;
+                        double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
+                        for (int i = 0; i < ns; ++i) {
+                            const double li = la[i], dli = dla[i];
+                            const double* Ri = Rg + i * 6 * q + b2;
+                            for (int cc = 0; cc < 3; ++cc) {
+                                y[cc] = fma(li, Ri[cc * q], y[cc]);
+                                yt[cc] = fma(dli, Ri[cc * q], yt[cc]);
+                                yh[cc] = fma(li, Ri[(3 + cc) * q], yh[cc]);
+                            }
+                        }
+                        const double W = P.gw[a0 + a2] * P.gw[b2] * ht * hh2;
+                        double G[9];
+                        point_kernel(kind, y, yt, yh, W, x0, x1, x2, eta, P.dl, G);
+                        for (int q2 = 0; q2 < NG; ++q2) Gc[a2 * ldG + b2 * NG + q2] = G[q2];
+                    }
+                    __syncthreads();
+                    NQ_MARK(8);
+                    dmma_gemm<NT>(ns, q * NG, na, a0 > 0,
+                              [&](int row) { return row; },
+                              [&](int ra, int k) { return Lc[k * ldL + ra]; },
+                              [&](int k, int col) { return Gc[k * ldG + col]; },
+                              [&](int row) { return row * ldU + slot * q * NG; },
+                              [&](int rc2, int col) -> double& { return Uc[rc2 + col]; });
+                    __syncthreads();
+                    NQ_MARK(9);
+                }
+                if (slot == nb - 1 || rc == nreg - 1) {
+                    dmma_gemm<NT>(ns * NG, nt, (slot + 1) * q, true,
+                              [&](int row) { return (row / NG) * ldU + row % NG; },
+                              [&](int ra, int k) { return Uc[ra + k * NG]; },
+                              [&](int k, int col) { return Cc[k * ldC + col]; },
+                              [&](int row) { return row * nt; },
+                              [&](int rc2, int col) -> double& { return Bacc[rc2 + col]; });
+                    __syncthreads();
+                    NQ_MARK(10);
                 }
             }
-            __syncthreads();
         }
         // ---------------- write the block: [tdim][node (i,j)][sdim]
         // back from the feature basis to the nodal basis: B[(q2,i)][j] = sum_m Bacc[(q2,i)][m] phi_m(th_j),
         // phi = (1, cos th_j, sin th_j, ..., cos (N/2-1)th_j, sin (N/2-1)th_j, (-1)^j)
         double* Bp = blocks + (boff ? boff[p] : p * (int64_t)TD * Nn * TD);
-        for (int o = tid; o < NG * Nn; o += kQThreads) {
+        for (int o = tid; o < NG * Nn; o += NT) {
             const int q2 = o / Nn, ij = o % Nn, i = ij / nt, j = ij % nt;
-            const double* Fr = Bacc + (q2 * ns + i) * nt;
+            const double* Fr = Bacc + (i * NG + q2) * nt;
             double acc = Fr[0];
             int idx = 0;
             for (int l = 1; l < nt / 2; ++l) {
@@ -585,6 +813,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             Bp[(a * Nn + ij) * TD + b] = acc;
         }
         __syncthreads();
+        NQ_MARK(5);
     }
 }
 
@@ -603,6 +832,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                const std::vector<std::pair<int, int>>& classes = {}, const int32_t* pclass = nullptr) {
     std::unique_ptr<QuadParams> Pp(new QuadParams);      // 10 KB: heap, per call (thread-safe)
     QuadParams& P = *Pp;
+    P.region = 0; P.nb = 1;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
     P.dl = (kernel == SLB_STOKES_SL || kernel == SLB_LAPLACE_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
@@ -620,19 +850,37 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     gl_nodes(P.qd, P.dx, P.dw);
     for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
     const int TD = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? 1 : 3;
-    auto smem_of = [&](int ns_, int nt_) {
+    // shared layout per class: the scratch region holds a Duffy batch (kQBatch nodes) or the regular-cell
+    // tables of nb cells; nb (<= 4) as large as the CTA shape allows -- 256 threads and <= 113 KB (two
+    // CTAs per SM) when the Duffy-only layout fits that, else 512 threads and <= 227 KB -- else one cell
+    // per update with t rows in chunks
+    struct Layout { int region, nb, threads; size_t smem; };
+    const int NGh = TD * TD;
+    auto layout_of = [&](int ns_, int nt_) -> Layout {
         const size_t Nn = (size_t)ns_ * nt_;
         const size_t Ysz = std::max(Nn * 3, (size_t)ns_ * (nt_ / 2 + 1) * 6);
-        return sizeof(double) * (Ysz + (size_t)TD * TD * Nn + (size_t)kQThreads * (TD * TD + ns_ + nt_) +
-                                 2 * (size_t)nt_) + sizeof(Cell) * kMaxCells;
+        const size_t base = sizeof(double) * (Ysz + (size_t)NGh * Nn + 2 * (size_t)nt_) + sizeof(CellBox) * kMaxCells;
+        const int duffy = kQBatch * (NGh + ns_ + ld_pad(nt_));
+        const bool small = base + sizeof(double) * duffy <= 113 * 1024;
+        const size_t budget = small ? 113 * 1024 : 227 * 1024;
+        const int threads = small ? 256 : 512;
+        for (int nb = 4; nb >= 1; --nb) {
+            const int region = std::max(duffy, regular_need(order, ns_, nt_, NGh, nb));
+            if (base + sizeof(double) * region <= budget) return {region, nb, threads, base + sizeof(double) * region};
+        }
+        return {duffy, 1, threads, base + sizeof(double) * duffy};
     };
     std::vector<std::pair<int, int>> cls = classes.empty() ? std::vector<std::pair<int, int>>{{ns, nt}} : classes;
     size_t smem_max = 0;
     for (auto& c : cls) {
-        SLB_REQUIRE(smem_of(c.first, c.second) <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
-        smem_max = std::max(smem_max, smem_of(c.first, c.second));
+        const Layout L = layout_of(c.first, c.second);
+        SLB_REQUIRE(L.smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "nearquad: shared memory");
+        SLB_REQUIRE(regular_chunk(order, c.first, c.second, NGh, L.region) >= 1, SLB_ERR_UNSUPPORTED,
+                    "nearquad: rule order too large for the panel grid");
+        smem_max = std::max(smem_max, L.smem);
     }
-    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
     int* st = nullptr;
     SLB_CUDA(cudaMallocAsync(&st, sizeof(int), s));
     SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
@@ -651,9 +899,17 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     for (int c = 0; c < (int)cls.size() && r == SLB_OK; ++c) {
         P.ns = cls[c].first;
         P.nt = cls[c].second;
-        nearquad_kernel<<<(unsigned)n_trg, kQThreads, smem_of(P.ns, P.nt), s>>>(
-            (int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx, y_coarse, eta_panel, P, blocks, st, pnt, cn0, boff,
-            pns, cp, pclass, c);
+        const Layout L = layout_of(P.ns, P.nt);
+        P.region = L.region;
+        P.nb = L.nb;
+        if (L.threads == 256)
+            nearquad_kernel<256><<<(unsigned)n_trg, 256, L.smem, s>>>(
+                (int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx, y_coarse, eta_panel, P, blocks, st, pnt, cn0,
+                boff, pns, cp, pclass, c);
+        else
+            nearquad_kernel<512><<<(unsigned)n_trg, 512, L.smem, s>>>(
+                (int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx, y_coarse, eta_panel, P, blocks, st, pnt, cn0,
+                boff, pns, cp, pclass, c);
         ++g_launch_count;
         r = check_launch("nearquad_kernel");
     }
@@ -663,6 +919,17 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) { set_error(std::string("nearquad: ") + cudaGetErrorString(e)); r = SLB_ERR_CUDA; }
     }
+#ifdef SLB_NQ_PROFILE
+    {
+        unsigned long long pr[16], cn[4];
+        cudaMemcpyFromSymbol(pr, g_nq_prof, sizeof(pr));
+        cudaMemcpyFromSymbol(cn, g_nq_cnt, sizeof(cn));
+        fprintf(stderr, "nearquad profile (Mclk): setup %.0f tree %.0f modes %.0f duffy %.0f tables %.0f lagr %.0f nodes %.0f "
+                "gemm1 %.0f gemm2 %.0f write %.0f | pairs %llu regular cells %llu duffy nodes %llu\n",
+                pr[0] * 1e-6, pr[1] * 1e-6, pr[2] * 1e-6, pr[3] * 1e-6, pr[6] * 1e-6, pr[7] * 1e-6, pr[8] * 1e-6,
+                pr[9] * 1e-6, pr[10] * 1e-6, pr[5] * 1e-6, cn[2], cn[0], cn[1]);
+    }
+#endif
     cudaFreeAsync(st, s);
     cudaFreeAsync(cp, s);
     if (r == SLB_OK && h) {
