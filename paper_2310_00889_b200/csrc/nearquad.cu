@@ -40,7 +40,7 @@ constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
 constexpr int kTri = kMaxNsQ * (kMaxNsQ + 1) / 2;   // GL tables for every n <= kMaxNsQ, at n (n-1) / 2
 struct QuadParams {
     int ns, nt, q, qd;        // ns, nt: the largest panel orders of the launch (shared-memory layout)
-    int region, nb;           // per-node / per-cell scratch (doubles); regular cells per Bacc update
+    int region, nb, gp;       // per-node / per-cell scratch (doubles); regular cells per Bacc update / per phase
     double beta;
     double dl;                // weight of the double layer: 1, or 0 for the pure single layer (SLB_STOKES_SL)
     double tgl[kTri];         // GL nodes on [-1,1] of every order n: tgl[n (n-1)/2 + i]
@@ -359,14 +359,16 @@ __device__ __forceinline__ void dmma_gemm(int M, int N, int Kn, bool acc, FRA ar
     }
 }
 
-// regular-cell scratch (doubles) for nb cells per Bacc update and all q t rows at once
-__host__ __device__ inline int regular_need(int q, int ns, int nt, int NG, int nb) {
-    return nb * q * ld_pad(nt) + ns * ld_pad(nb * q * NG) + 6 * ns * q + q * (4 * ld_pad(ns) + ld_pad(q * NG));
+// regular-cell scratch (doubles): U and C of nb cells (one Bacc update), per-phase tables of gp cells
+// (gp divides nb), all q t rows at once; the rings alias U when gp == nb
+__host__ __device__ inline int regular_need(int q, int ns, int nt, int NG, int nb, int gp) {
+    const int u = ns * ld_pad(nb * q * NG), r = gp * 6 * ns * q;
+    return nb * q * ld_pad(nt) + (gp == nb ? (u > r ? u : r) : u + r) + gp * q * (3 * ld_pad(ns) + ld_pad(q * NG));
 }
-// one cell per update, t rows in chunks: the chunk `ac` that fits `region` (< 1: does not fit)
+// one cell per group, t rows in chunks: the chunk `ac` that fits `region` (< 1: does not fit)
 __host__ __device__ inline int regular_chunk(int q, int ns, int nt, int NG, int region) {
     const int fixed = q * ld_pad(nt) + ns * ld_pad(q * NG) + 6 * ns * q;
-    const int per_a = 4 * ld_pad(ns) + ld_pad(q * NG);
+    const int per_a = 3 * ld_pad(ns) + ld_pad(q * NG);
     const int ac = (region - fixed) / per_a;
     return ac < q ? ac : q;
 }
@@ -638,39 +640,41 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             NQ_MARK(3);
         }
         // ---------------- (2) regular cells: q x q tensor Gauss grids, contraction sum-factorized
-        //   U[i][(b,q2)]     = sum_a l_i(t_a) G[(a,b)][q2]       (GEMM: M = ns, N = q NG, K = q; t rows in chunks)
+        //   U[i][(b,q2)]     = sum_a l_i(t_a) G[(a,b)][q2]       (GEMM: M = ns, N = q NG, K = q)
         //   Bacc[(i,q2)][j] += sum_b U[i][(b,q2)] C_j(th_b)      (GEMM: M = ns NG, N = nt, K = q)
-        // i.e. q^2 NG ns + q NG ns nt multiply-adds per cell instead of q^2 NG ns nt.  The per-cell tables
-        // (features and rings at the q theta nodes, Lagrange rows at the t nodes) are built by all
-        // threads, one entry each; they live in the Duffy batch region (Gs..Cs).
+        // i.e. q^2 NG ns + q NG ns nt multiply-adds per cell instead of q^2 NG ns nt.  Every phase
+        // (tables: features and rings at the q theta nodes, Lagrange rows at the q t nodes; kernel at the
+        // nodes; U) covers a group of P.gp cells, one entry per thread; the U and C of P.nb cells (a
+        // multiple of gp) are stacked along K for one Bacc update.  All in the Duffy batch region (Gs..Cs).
+        // Without room for one whole cell (nb = gp = 1 only) the t rows go in chunks of ac.
         {
-            const int q = P.q;
-            const int nb = P.nb;                      // cells per Bacc update (their U, C stacked along K)
-            const int ldC = ld_pad(nt), ldL = ld_pad(ns), ldG = ld_pad(q * NG), ldU = ld_pad(nb * q * NG);
-            const int ac = nb > 1 ? q : max(1, regular_chunk(q, ns, nt, NG, P.region));
-            double* Cc = Gs;                          // [nb q][ldC] features at the cells' th nodes
-            double* Uc = Cc + nb * q * ldC;           // [ns][ldU]   (cell, b, q2)
-            double* Rg = Uc + ns * ldU;               // [ns][6][q]  rings and d/dth at the th nodes
-            double* Lc = Rg + 6 * ns * q;             // [ac][ldL]   l_i(t_a)
-            double* dLc = Lc + ac * ldL;              // [ac][ldL]   l_i'(t_a)
-            double* Xc = dLc + ac * ldL;              // [ac][ldL]   t_a - t_i
-            double* iXc = Xc + ac * ldL;              // [ac][ldL]   1 / (t_a - t_i)
-            double* Gc = iXc + ac * ldL;              // [ac][ldG]   (b, q2): kernel x weight at the nodes
+            const int q = P.q, nk = P.nb, ng = P.gp;
+            const int ldC = ld_pad(nt), ldL = ld_pad(ns), ldG = ld_pad(q * NG), ldU = ld_pad(nk * q * NG);
+            const int ac = nk > 1 ? q : max(1, regular_chunk(q, ns, nt, NG, P.region));
+            // rings alias U when a group fills U (U dead between the node phase and the U GEMM)
+            const bool alias = ac == q && ng == nk;
+            double* Cc = Gs;                          // [nk q][ldC]      features at the cells' th nodes
+            double* Uc = Cc + nk * q * ldC;           // [ns][ldU]        (cell, b, q2)
+            double* Rg = alias ? Uc : Uc + ns * ldU;  // [ng][ns][6][q]   rings and d/dth at the th nodes
+            double* Lc = alias ? Uc + max(ns * ldU, ng * 6 * ns * q) : Rg + ng * 6 * ns * q;   // [ng][ac][ldL]
+            double* dLc = Lc + ng * ac * ldL;         // [ng][ac][ldL]    l_i'(t_a)
+            double* iXc = dLc + ng * ac * ldL;        // [ng][ac][ldL]    1 / (t_a - t_i)
+            double* Gc = iXc + ng * ac * ldL;         // [ng][ac][ldG]    (b, q2): kernel x weight at the nodes
             const int nl = nt / 2;                    // feature pairs (cos l th, sin l th), l = 1 .. nt/2
             const int nparts = 4, lper = (nl + nparts - 1) / nparts;
-            for (int rc = 0; rc < nreg; ++rc) {
-                const CellBox c = cells[kMaxCells - 1 - rc];
-                const double ht = 0.5 * (c.t1 - c.t0), hh2 = 0.5 * (c.h1 - c.h0);
-                const int slot = rc % nb;
-                double* Ccs = Cc + slot * q * ldC;
+            const CellBox* creg = cells + kMaxCells - 1;   // regular cell r: creg[-r]
+            for (int g0 = 0; g0 < nreg; g0 += ng) {
+                const int gn = min(ng, nreg - g0);
                 for (int a0 = 0; a0 < q; a0 += ac) {
                     const int na = min(ac, q - a0);
                     if (a0 == 0) {
-                        // features C[b][m] (trig_features layout) by (b, quarter of the l range)
-                        for (int e = tid; e < q * nparts; e += NT) {
-                            const int b2 = e / nparts, l0 = 1 + (e % nparts) * lper, l1 = min(nl, l0 + lper - 1);
-                            const double th = hs + c.h0 + hh2 * (P.gx[b2] + 1.0);
-                            double* Cr = Ccs + b2 * ldC;
+                        // features C[b][m] (trig_features layout) by (cell, b, quarter of the l range)
+                        for (int e = tid; e < gn * q * nparts; e += NT) {
+                            const int sl = e / (q * nparts), b2 = (e / nparts) % q;
+                            const int l0 = 1 + (e % nparts) * lper, l1 = min(nl, l0 + lper - 1);
+                            const CellBox c = creg[-(g0 + sl)];
+                            const double th = hs + c.h0 + 0.5 * (c.h1 - c.h0) * (P.gx[b2] + 1.0);
+                            double* Cr = Cc + (((g0 + sl) % nk) * q + b2) * ldC;
                             const double invN = 1.0 / nt;
                             if (l0 == 1) Cr[0] = invN;
                             if (l0 <= l1) {
@@ -687,10 +691,11 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                             }
                         }
                         // ring i at the q theta nodes from its Fourier modes (<= K): R_i(th_b), dR_i/dth (th_b)
-                        for (int e = tid; e < ns * q; e += NT) {
-                            const int i = e / q, b2 = e % q;
+                        for (int e = tid; e < gn * ns * q; e += NT) {
+                            const int sl = e / (ns * q), i = (e / q) % ns, b2 = e % q;
+                            const CellBox c = creg[-(g0 + sl)];
                             double c1, s1;
-                            sincos(hs + c.h0 + hh2 * (P.gx[b2] + 1.0), &s1, &c1);
+                            sincos(hs + c.h0 + 0.5 * (c.h1 - c.h0) * (P.gx[b2] + 1.0), &s1, &c1);
                             const double* Ai = FA + i * H * 3;
                             const double* Bi = FB + i * H * 3;
                             double R[3] = {Ai[0], Ai[1], Ai[2]}, dR[3] = {0, 0, 0};
@@ -705,29 +710,29 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                                 sk = sk * c1 + ck * s1;
                                 ck = cn;
                             }
+                            double* Rs = Rg + sl * 6 * ns * q;
                             for (int cc = 0; cc < 3; ++cc) {
-                                Rg[(i * 6 + cc) * q + b2] = R[cc];
-                                Rg[(i * 6 + 3 + cc) * q + b2] = dR[cc];
+                                Rs[(i * 6 + cc) * q + b2] = R[cc];
+                                Rs[(i * 6 + 3 + cc) * q + b2] = dR[cc];
                             }
                         }
                     }
-                    // Lagrange rows, barycentric (as lagrange_eval): differences and their reciprocals
-                    for (int e = tid; e < na * ns; e += NT) {
-                        const int a2 = e / ns, i = e % ns;
-                        const double X = (c.t0 + ht * (P.gx[a0 + a2] + 1.0)) - tg[i];
-                        Xc[a2 * ldL + i] = X;
-                        iXc[a2 * ldL + i] = 1.0 / X;
+                    // Lagrange rows, barycentric (as lagrange_eval): reciprocals of t_a - t_i first
+                    for (int e = tid; e < gn * na * ns; e += NT) {
+                        const int sl = e / (na * ns), a2 = (e / ns) % na, i = e % ns;
+                        const CellBox c = creg[-(g0 + sl)];
+                        const double X = (c.t0 + 0.5 * (c.t1 - c.t0) * (P.gx[a0 + a2] + 1.0)) - tg[i];
+                        iXc[(sl * ac + a2) * ldL + i] = (fabs(X) < 1e-15) ? 0.0 : 1.0 / X;    // 0: t_a on node i
                     }
                     __syncthreads();
                     NQ_MARK(6);
-                    for (int e = tid; e < na * ns; e += NT) {
-                        const int a2 = e / ns, i = e % ns;
-                        const double* X = Xc + a2 * ldL;
-                        const double* iX = iXc + a2 * ldL;
+                    for (int e = tid; e < gn * na * ns; e += NT) {
+                        const int sl = e / (na * ns), a2 = (e / ns) % na, i = e % ns;
+                        const double* iX = iXc + (sl * ac + a2) * ldL;
                         int hit = -1;
                         double den = 0.0, dden = 0.0;
                         for (int k = 0; k < ns; ++k) {
-                            if (fabs(X[k]) < 1e-15) hit = k;
+                            if (iX[k] == 0.0) hit = k;
                             const double ck = lm[k] * iX[k];
                             den += ck;
                             dden -= ck * iX[k];
@@ -747,48 +752,52 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                             l = ci * iden;
                             dl = (dci * den - ci * dden) * iden * iden;
                         }
-                        Lc[a2 * ldL + i] = l;
-                        dLc[a2 * ldL + i] = dl;
+                        Lc[(sl * ac + a2) * ldL + i] = l;
+                        dLc[(sl * ac + a2) * ldL + i] = dl;
                     }
                     __syncthreads();
                     NQ_MARK(7);
-                    for (int n = tid; n < na * q; n += NT) {
-                        const int a2 = n / q, b2 = n % q;
-                        const double* la = Lc + a2 * ldL;
-                        const double* dla = dLc + a2 * ldL;
+                    for (int n = tid; n < gn * na * q; n += NT) {
+                        const int sl = n / (na * q), a2 = (n / q) % na, b2 = n % q;
+                        const CellBox c = creg[-(g0 + sl)];
+                        const double* la = Lc + (sl * ac + a2) * ldL;
+                        const double* dla = dLc + (sl * ac + a2) * ldL;
+                        const double* Rs = Rg + sl * 6 * ns * q + b2;
                         double y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
                         for (int i = 0; i < ns; ++i) {
                             const double li = la[i], dli = dla[i];
-                            const double* Ri = Rg + i * 6 * q + b2;
+                            const double* Ri = Rs + i * 6 * q;
                             for (int cc = 0; cc < 3; ++cc) {
                                 y[cc] = fma(li, Ri[cc * q], y[cc]);
                                 yt[cc] = fma(dli, Ri[cc * q], yt[cc]);
                                 yh[cc] = fma(li, Ri[(3 + cc) * q], yh[cc]);
                             }
                         }
-                        const double W = P.gw[a0 + a2] * P.gw[b2] * ht * hh2;
+                        const double W = P.gw[a0 + a2] * P.gw[b2] * (0.5 * (c.t1 - c.t0)) * (0.5 * (c.h1 - c.h0));
                         double G[9];
                         point_kernel(kind, y, yt, yh, W, x0, x1, x2, eta, P.dl, G);
-                        for (int q2 = 0; q2 < NG; ++q2) Gc[a2 * ldG + b2 * NG + q2] = G[q2];
+                        double* Gn = Gc + (sl * ac + a2) * ldG + b2 * NG;
+                        for (int q2 = 0; q2 < NG; ++q2) Gn[q2] = G[q2];
                     }
                     __syncthreads();
                     NQ_MARK(8);
-                    dmma_gemm<NT>(ns, q * NG, na, a0 > 0,
-                              [&](int row) { return row; },
-                              [&](int ra, int k) { return Lc[k * ldL + ra]; },
-                              [&](int k, int col) { return Gc[k * ldG + col]; },
-                              [&](int row) { return row * ldU + slot * q * NG; },
-                              [&](int rc2, int col) -> double& { return Uc[rc2 + col]; });
+                    for (int sl = 0; sl < gn; ++sl)
+                        dmma_gemm<NT>(ns, q * NG, na, a0 > 0,
+                                      [&](int row) { return row; },
+                                      [&](int ra, int k) { return Lc[(sl * ac + k) * ldL + ra]; },
+                                      [&](int k, int col) { return Gc[(sl * ac + k) * ldG + col]; },
+                                      [&](int row) { return row * ldU + ((g0 + sl) % nk) * q * NG; },
+                                      [&](int rc2, int col) -> double& { return Uc[rc2 + col]; });
                     __syncthreads();
                     NQ_MARK(9);
                 }
-                if (slot == nb - 1 || rc == nreg - 1) {
-                    dmma_gemm<NT>(ns * NG, nt, (slot + 1) * q, true,
-                              [&](int row) { return (row / NG) * ldU + row % NG; },
-                              [&](int ra, int k) { return Uc[ra + k * NG]; },
-                              [&](int k, int col) { return Cc[k * ldC + col]; },
-                              [&](int row) { return row * nt; },
-                              [&](int rc2, int col) -> double& { return Bacc[rc2 + col]; });
+                if ((g0 + gn) % nk == 0 || g0 + gn == nreg) {
+                    dmma_gemm<NT>(ns * NG, nt, ((g0 + gn - 1) % nk + 1) * q, true,
+                                  [&](int row) { return (row / NG) * ldU + row % NG; },
+                                  [&](int ra, int k) { return Uc[ra + k * NG]; },
+                                  [&](int k, int col) { return Cc[k * ldC + col]; },
+                                  [&](int row) { return row * nt; },
+                                  [&](int rc2, int col) -> double& { return Bacc[rc2 + col]; });
                     __syncthreads();
                     NQ_MARK(10);
                 }
@@ -832,7 +841,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                                const std::vector<std::pair<int, int>>& classes = {}, const int32_t* pclass = nullptr) {
     std::unique_ptr<QuadParams> Pp(new QuadParams);      // 10 KB: heap, per call (thread-safe)
     QuadParams& P = *Pp;
-    P.region = 0; P.nb = 1;
+    P.region = 0; P.nb = 1; P.gp = 1;
     P.ns = ns; P.nt = nt; P.q = order; P.qd = std::min(kMaxQ, order + 4); P.beta = beta;
     P.dl = (kernel == SLB_STOKES_SL || kernel == SLB_LAPLACE_SL) ? 0.0 : 1.0;
     double w[kMaxNsQ];
@@ -854,7 +863,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     // tables of nb cells; nb (<= 4) as large as the CTA shape allows -- 256 threads and <= 113 KB (two
     // CTAs per SM) when the Duffy-only layout fits that, else 512 threads and <= 227 KB -- else one cell
     // per update with t rows in chunks
-    struct Layout { int region, nb, threads; size_t smem; };
+    struct Layout { int region, nb, gp, threads; size_t smem; };
     const int NGh = TD * TD;
     auto layout_of = [&](int ns_, int nt_) -> Layout {
         const size_t Nn = (size_t)ns_ * nt_;
@@ -864,11 +873,17 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         const bool small = base + sizeof(double) * duffy <= 113 * 1024;
         const size_t budget = small ? 113 * 1024 : 227 * 1024;
         const int threads = small ? 256 : 512;
-        for (int nb = 4; nb >= 1; --nb) {
-            const int region = std::max(duffy, regular_need(order, ns_, nt_, NGh, nb));
-            if (base + sizeof(double) * region <= budget) return {region, nb, threads, base + sizeof(double) * region};
+        static int nb_max = -1;          // SLB_NQ_NB: cap on the cells per group (tuning knob)
+        if (nb_max < 0) { const char* e = getenv("SLB_NQ_NB"); nb_max = e ? std::max(1, std::min(4, atoi(e))) : 4; }
+        // (cells per update, per phase): K-stacking first, then phase groups
+        static const int cand[8][2] = {{4, 4}, {4, 2}, {3, 3}, {2, 2}, {4, 1}, {3, 1}, {2, 1}, {1, 1}};
+        for (const auto& c : cand) {
+            if (c[0] > nb_max) continue;
+            const int region = std::max(duffy, regular_need(order, ns_, nt_, NGh, c[0], c[1]));
+            if (base + sizeof(double) * region <= budget)
+                return {region, c[0], c[1], threads, base + sizeof(double) * region};
         }
-        return {duffy, 1, threads, base + sizeof(double) * duffy};
+        return {duffy, 1, 1, threads, base + sizeof(double) * duffy};
     };
     std::vector<std::pair<int, int>> cls = classes.empty() ? std::vector<std::pair<int, int>>{{ns, nt}} : classes;
     size_t smem_max = 0;
@@ -902,6 +917,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         const Layout L = layout_of(P.ns, P.nt);
         P.region = L.region;
         P.nb = L.nb;
+        P.gp = L.gp;
         if (L.threads == 256)
             nearquad_kernel<256><<<(unsigned)n_trg, 256, L.smem, s>>>(
                 (int)kind, n_trg, x_trg, trg_node, row_ptr, panel_idx, y_coarse, eta_panel, P, blocks, st, pnt, cn0,
