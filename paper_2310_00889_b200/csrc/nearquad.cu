@@ -35,6 +35,7 @@ namespace slb {
 
 constexpr int kQBatch = 128;     // Duffy-rule nodes per batch (sizes the per-node scratch region)
 constexpr int kMaxCells = 768;
+constexpr int kMaxLevels = 64;    // quadtree depth bound
 constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
 
 constexpr int kTri = kMaxNsQ * (kMaxNsQ + 1) / 2;   // GL tables for every n <= kMaxNsQ, at n (n-1) / 2
@@ -373,6 +374,33 @@ __host__ __device__ inline int regular_chunk(int q, int ns, int nt, int NG, int 
     return ac < q ? ac : q;
 }
 
+// exclusive block-wide prefix sums of three per-thread counts (o*) and their totals (t*); all NT
+// threads call it; sh: 3 NT / 32 ints of shared scratch
+template <int NT>
+__device__ __forceinline__ void block_scan3(int a, int b, int c, int& oa, int& ob, int& oc, int& ta, int& tb, int& tc,
+                                            int* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int va = a, vb = b, vc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int xa = __shfl_up_sync(0xffffffffu, va, o), xb = __shfl_up_sync(0xffffffffu, vb, o),
+                  xc = __shfl_up_sync(0xffffffffu, vc, o);
+        if (lane >= o) { va += xa; vb += xb; vc += xc; }
+    }
+    if (lane == 31) { sh[3 * warp] = va; sh[3 * warp + 1] = vb; sh[3 * warp + 2] = vc; }
+    __syncthreads();
+    int pa = 0, pb = 0, pc = 0;
+    ta = 0; tb = 0; tc = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const int wa = sh[3 * w], wb = sh[3 * w + 1], wc = sh[3 * w + 2];
+        if (w < warp) { pa += wa; pb += wb; pc += wc; }
+        ta += wa; tb += wb; tc += wc;
+    }
+    oa = pa + va - a; ob = pb + vb - b; oc = pc + vc - c;
+    __syncthreads();
+}
+
 // SLB_NQ_PROFILE (dev builds only): per-phase SM clocks of thread 0, summed over CTAs, printed by nearquad_run
 #ifdef SLB_NQ_PROFILE
 __device__ unsigned long long g_nq_prof[16], g_nq_cnt[4];
@@ -417,7 +445,8 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
     CellBox* cells = reinterpret_cast<CellBox*>(TS + ntm);
     __shared__ double s_par[8];                       // t*, th*, d, St, Sh, node-singular flag
-    __shared__ int s_ncell, s_ntot, s_nreg, s_fail, s_K;
+    __shared__ int s_ncell, s_ntot, s_nreg, s_fail, s_K, s_nlvl;
+    __shared__ int s_scan[3 * (NT / 32)];
     __shared__ unsigned long long s_amax;
     // per-thread scratch for the interpolation (registers / local)
     double lb[kMaxNsQ], dlb[kMaxNsQ], Cb[kMaxNtQ], dCb[kMaxNtQ];
@@ -466,19 +495,33 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             const double St = sqrt(yt[0] * yt[0] + yt[1] * yt[1] + yt[2] * yt[2]);
             const double Sh = sqrt(yh[0] * yh[0] + yh[1] * yh[1] + yh[2] * yh[2]);
             s_par[0] = ts; s_par[1] = hs; s_par[2] = d; s_par[3] = St; s_par[4] = Sh;
-            // quadtree over the parameter rectangle [-1,1] x [hs - pi, hs + pi], split at (ts, hs)
-            Cell stack[64];
-            int sp = 0, nc = 0, nr = 0, ntot = 0;       // Duffy cells from the front, regular from the back
-            const double T0[2] = {-1.0, ts}, T1[2] = {ts, 1.0};
-            const double H0[2] = {-kPi, 0.0}, H1[2] = {0.0, kPi};
-            for (int a = 0; a < 2; ++a)
-                for (int b = 0; b < 2; ++b) {
-                    if (T1[a] - T0[a] <= 0.0) continue;
-                    Cell c;
-                    c.t0 = T0[a]; c.t1 = T1[a]; c.h0 = H0[b]; c.h1 = H1[b];
-                    c.duffy = singular ? 1 : 0;
-                    stack[sp++] = c;
-                }
+            s_par[5] = singular ? 1.0 : 0.0;
+            s_ncell = 0; s_nreg = 0; s_nlvl = 0;
+        }
+        __syncthreads();
+        // ---------------- quadtree over the parameter rectangle [-1,1] x [hs - pi, hs + pi], split at
+        // (ts, hs), level by level: one thread per cell of the level, accepted cells and children placed by
+        // block-wide prefix sums (deterministic order).  Level buffers live in the scratch region.
+        {
+            const double ts = s_par[0], d = s_par[2], St = s_par[3], Sh = s_par[4];
+            const bool singular = s_par[5] != 0.0;
+            const int lmax = (int)((size_t)P.region * sizeof(double) / (2 * sizeof(Cell)));
+            Cell* lvl[2] = {reinterpret_cast<Cell*>(Gs), reinterpret_cast<Cell*>(Gs) + lmax};
+            if (tid == 0) {
+                const double T0[2] = {-1.0, ts}, T1[2] = {ts, 1.0};
+                const double H0[2] = {-kPi, 0.0}, H1[2] = {0.0, kPi};
+                int n0 = 0;
+                for (int a = 0; a < 2; ++a)
+                    for (int b = 0; b < 2; ++b) {
+                        if (T1[a] - T0[a] <= 0.0) continue;
+                        Cell c;
+                        c.t0 = T0[a]; c.t1 = T1[a]; c.h0 = H0[b]; c.h1 = H1[b];
+                        c.duffy = singular ? 1 : 0;
+                        lvl[0][n0++] = c;
+                    }
+                s_nlvl = n0;
+            }
+            __syncthreads();
             const double cap = 2.0 * Sh;   // ~ tube diameter: keeps the opposite wall resolved
             // distance used by the acceptance test: on the tube (radius ~ Sh) a target at distance d
             // from the surface puts the kernel's complex singularity in th at acosh(1 + d^2 / (2 Sh (Sh + d)))
@@ -491,58 +534,79 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
             // the width 2h <= 2.13 q / nt.  Without it, cells of moderate-distance targets spanning
             // half the circumference under-resolve cos(nt th / 2) (tests/test_gpu_bvp.py: 1e-7 -> 1e-12)
             const double hmax = 2.13 * P.q / nt;
-            while (sp > 0) {
-                Cell c = stack[--sp];
-                const double wa = (c.t1 - c.t0) * St, wb = (c.h1 - c.h0) * Sh;
-                const double diag = sqrt(wa * wa + wb * wb);
-                bool accept;
-                if (c.duffy) {
-                    accept = (fmax(wa, wb) <= 2.5 * fmin(wa, wb)) && diag <= cap;
-                } else {
-                    // distance from (t*, th*) to the cell in scaled coordinates, plus the normal offset
-                    const double da = (c.t0 > ts) ? (c.t0 - ts) * St : ((c.t1 < ts) ? (ts - c.t1) * St : 0.0);
-                    const double db = (c.h0 > 0.0) ? c.h0 * Sh : ((c.h1 < 0.0) ? -c.h1 * Sh : 0.0);
-                    const double dist = sqrt(deff * deff + da * da + db * db);
-                    if (da >= 2.0 * cap) {
-                        // far along the fiber (more than two tube diameters): the whole cross-section
-                        // is at true distance >= da - cap >= da / 2, so no size cap -- cells grow
-                        // geometrically along t (slender panels, rho << panel length)
-                        accept = fmax(0.5 * da, d) >= P.beta * diag;
-                    } else {
-                        accept = dist >= P.beta * diag && diag <= 2.0 * cap;
+            int cur = 0;
+            for (int level = 0; level < kMaxLevels; ++level) {
+                const int n = s_nlvl;
+                if (n == 0 || s_fail) break;
+                int nout = 0;                                     // children written so far (uniform)
+                for (int base = 0; base < n; base += NT) {
+                    const int i = base + tid;
+                    int accd = 0, accr = 0, nch = 0;
+                    Cell ch[4];
+                    Cell c;
+                    if (i < n) {
+                        c = lvl[cur][i];
+                        const double wa = (c.t1 - c.t0) * St, wb = (c.h1 - c.h0) * Sh;
+                        const double diag = sqrt(wa * wa + wb * wb);
+                        bool accept;
+                        if (c.duffy) {
+                            accept = (fmax(wa, wb) <= 2.5 * fmin(wa, wb)) && diag <= cap;
+                        } else {
+                            // distance from (t*, th*) to the cell in scaled coordinates, plus the normal offset
+                            const double da = (c.t0 > ts) ? (c.t0 - ts) * St : ((c.t1 < ts) ? (ts - c.t1) * St : 0.0);
+                            const double db = (c.h0 > 0.0) ? c.h0 * Sh : ((c.h1 < 0.0) ? -c.h1 * Sh : 0.0);
+                            const double dist = sqrt(deff * deff + da * da + db * db);
+                            if (da >= 2.0 * cap) {
+                                // far along the fiber (more than two tube diameters): the whole cross-section
+                                // is at true distance >= da - cap >= da / 2, so no size cap -- cells grow
+                                // geometrically along t (slender panels, rho << panel length)
+                                accept = fmax(0.5 * da, d) >= P.beta * diag;
+                            } else {
+                                accept = dist >= P.beta * diag && diag <= 2.0 * cap;
+                            }
+                        }
+                        accept = accept && (c.h1 - c.h0) <= hmax;
+                        if (accept) {
+                            (c.duffy ? accd : accr) = 1;
+                        } else {
+                            // split: the longer side in two (or both if comparable); Duffy keeps its corner cell
+                            const bool sa = wa >= 0.5 * wb, sb = wb >= 0.5 * wa || (c.h1 - c.h0) > hmax;
+                            const double tm = 0.5 * (c.t0 + c.t1), hm = 0.5 * (c.h0 + c.h1);
+                            const double ta[3] = {c.t0, sa ? tm : c.t1, c.t1};
+                            const double ha[3] = {c.h0, sb ? hm : c.h1, c.h1};
+                            for (int a = 0; a < (sa ? 2 : 1); ++a)
+                                for (int b = 0; b < (sb ? 2 : 1); ++b) {
+                                    Cell sc;
+                                    sc.t0 = ta[a]; sc.t1 = ta[a + 1]; sc.h0 = ha[b]; sc.h1 = ha[b + 1];
+                                    // the singular corner is (ts, 0): a sub-cell keeps Duffy if it touches it
+                                    const bool touch = (sc.t0 == ts || sc.t1 == ts) && (sc.h0 == 0.0 || sc.h1 == 0.0);
+                                    sc.duffy = c.duffy && touch;
+                                    ch[nch++] = sc;
+                                }
+                        }
                     }
+                    int od, orr, och, td, tr, tch;
+                    block_scan3<NT>(accd, accr, nch, od, orr, och, td, tr, tch, s_scan);
+                    const int nc0 = s_ncell, nr0 = s_nreg;                // before this chunk
+                    if (nc0 + nr0 + td + tr > kMaxCells || nout + tch > lmax) {
+                        if (tid == 0) s_fail = (nout + tch > lmax) ? 2 : 1;
+                        __syncthreads();
+                        break;
+                    }
+                    if (accd) cells[nc0 + od] = CellBox{c.t0, c.t1, c.h0, c.h1};
+                    if (accr) cells[kMaxCells - 1 - (nr0 + orr)] = CellBox{c.t0, c.t1, c.h0, c.h1};
+                    for (int k = 0; k < nch; ++k) lvl[cur ^ 1][nout + och + k] = ch[k];
+                    __syncthreads();
+                    if (tid == 0) { s_ncell = nc0 + td; s_nreg = nr0 + tr; }
+                    nout += tch;
+                    __syncthreads();
                 }
-                accept = accept && (c.h1 - c.h0) <= hmax;
-                if (accept) {
-                    if (nc + nr >= kMaxCells) { s_fail = 1; break; }
-                    const CellBox cb = {c.t0, c.t1, c.h0, c.h1};
-                    if (c.duffy) {
-                        ntot += 2 * P.qd * P.qd;
-                        cells[nc++] = cb;
-                    } else {
-                        cells[kMaxCells - 1 - nr++] = cb;
-                    }
-                    continue;
-                }
-                if (sp + 4 > 64) { s_fail = 2; break; }
-                // split: the longer side in two (or both if comparable); Duffy keeps its corner cell
-                const bool sa = wa >= 0.5 * wb, sb = wb >= 0.5 * wa || (c.h1 - c.h0) > hmax;
-                const double tm = 0.5 * (c.t0 + c.t1), hm = 0.5 * (c.h0 + c.h1);
-                const double ta[3] = {c.t0, sa ? tm : c.t1, c.t1};
-                const double ha[3] = {c.h0, sb ? hm : c.h1, c.h1};
-                for (int a = 0; a < (sa ? 2 : 1); ++a)
-                    for (int b = 0; b < (sb ? 2 : 1); ++b) {
-                        Cell s;
-                        s.t0 = ta[a]; s.t1 = ta[a + 1]; s.h0 = ha[b]; s.h1 = ha[b + 1];
-                        // the singular corner is (ts, 0): a sub-cell keeps Duffy if it touches it
-                        const bool touch = (s.t0 == ts || s.t1 == ts) && (s.h0 == 0.0 || s.h1 == 0.0);
-                        s.duffy = c.duffy && touch;
-                        stack[sp++] = s;
-                    }
+                if (tid == 0) s_nlvl = s_fail ? 0 : nout;
+                cur ^= 1;
+                __syncthreads();
+                if (level == kMaxLevels - 1 && s_nlvl > 0 && tid == 0) s_fail = 2;
             }
-            s_ncell = nc;
-            s_ntot = ntot;
-            s_nreg = nr;
+            if (tid == 0) s_ntot = s_ncell * 2 * P.qd * P.qd;
         }
         __syncthreads();
         NQ_MARK(1);
