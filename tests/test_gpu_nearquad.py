@@ -80,6 +80,34 @@ def test_stokes_dl_rigid_motion_with_special_blocks(mode):
     np.testing.assert_allclose(u[pr.n_on:], np.where(inside[:, None], -vx, 0.0), atol=1e-8 * np.abs(v).max())
 
 
+# panel grids x rule orders that take every shared-memory layout of the regular-cell path (see
+# nearquad_run's layout_of): t rows in chunks (12 x 20 and 8 x 8 at order 24, 256 threads), groups of 4
+# cells (10 x 12 at order 6), 512-thread CTAs with groups of 2 (16 x 64 at order 14) and the rings
+# kept apart from U (Laplace 16 x 64 at order 24: 4 cells per update, 2 per phase)
+LAYOUTS = [(2, 12, 20, 24, 1e-9), (2, 8, 8, 24, 1e-9), (2, 10, 12, 6, 1e-5), (2, 16, 64, 14, 1e-9),
+           (1, 16, 64, 24, 1e-9)]
+
+
+@pytest.mark.parametrize("kernel,Ns,Nt,order,tol", LAYOUTS)
+def test_jump_relations_across_layouts(kernel, Ns, Nt, order, tol):
+    """the same jump relations as above for each layout variant (tolerance from the rule's
+    ~2.76^(-2q) accuracy at beta = 0.6): Laplace (I/2 + D)[1] = 0, D[1] = -1 / 0; Stokes (I/2 + D)[v] = 0,
+    D[v] = -v / 0 for a rigid translation v"""
+    _skip()
+    from harness import DeviceProblem
+    X, inside = near_surface_targets(seed=5)
+    pr = make_torus_problem(panels=16, Ns=Ns, Nt=Nt, kernel=kernel, eta=0.0 if kernel == 2 else None,
+                            extra_targets=X)
+    a = np.array([0.3, -1.0, 0.7])[:pr.sdim] if kernel == 2 else np.ones(1)
+    v = np.tile(a, (pr.N, 1))
+    dp = DeviceProblem(pr, quad=dict(order=order, beta=0.6))
+    u = dp.matvec(cu(v)).cpu().numpy()
+    dp.close()
+    assert np.abs(u[:pr.n_on]).max() < tol, np.abs(u[:pr.n_on]).max()
+    exp = np.where(inside[:, None], -np.tile(a, (X.shape[0], 1)), 0.0)
+    np.testing.assert_allclose(u[pr.n_on:], exp, atol=tol)
+
+
 # ------------------------------------------------------------------ independent integrator
 def _exact_panel_integral(body, P, k, Ns, Nt, sig_panel, x, kind, eta, t0=None, h0=None):
     """int int K(x - y(t,th)) sigma_interp(t,th) J dt dth over panel k, t in [-1,1] local, polar
