@@ -33,7 +33,7 @@
 
 namespace slb {
 
-constexpr int kQBatch = 128;     // Duffy-rule nodes per batch (sizes the per-node scratch region)
+constexpr int kQBatch = 128;     // scratch region >= kQBatch (NG + ns + ld_pad(nt)) doubles
 constexpr int kMaxCells = 768;
 constexpr int kMaxLevels = 64;    // quadtree depth bound
 constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
@@ -414,6 +414,110 @@ __device__ unsigned long long g_nq_prof[16], g_nq_cnt[4];
 #define NQ_MARK(k)
 #endif
 
+// (1) of nearquad_kernel: the Duffy cells of a singular pair (see the comment inside)
+template <int NT>
+__device__ __noinline__ void duffy_cells(int kind, int ns, int nt, int NG, int K, int H, const double* FA,
+                                         const double* FB, const double* tg, const double* lm, const QuadParams& P,
+                                         const CellBox* cells, int ncells, double ts, double hs, double x0, double x1,
+                                         double x2, double eta, double* Gs, double* Bacc) {
+    const int tid = threadIdx.x;
+    double lb[kMaxNsQ], dlb[kMaxNsQ];
+    // ---------------- (1) Duffy cells (on-surface targets): two triangles per cell, each a qd x qd
+    // Gauss grid in (u, v) with the singular corner C0 = (ct, ch) at u = 0.  Neither is a tensor grid
+    // in (t, th), but each is separable in one direction, and the contraction is factorized along it:
+    //   triangle 0 (C0, (ot, ch), (ot, oh)):  t = ct + u At (row u only),     th = ch + u v Bh
+    //     T[a][q2][j] = sum_b G[(a,b)][q2] C_j(th_ab)   (DFMA),  Bacc[i][(q2,j)] += sum_a l_i(t_a) T[a][(q2,j)]
+    //   triangle 1 (C0, (ot, oh), (ct, oh)):  th = ch + u Ah (row u only),    t = ct + u At (1 - v)
+    //     V[a][(i,q2)] = sum_b l_i(t_ab) G[(a,b)][q2] (DFMA),  Bacc[(i,q2)][j] += sum_a V[a][(i,q2)] C_j(th_a)
+    // (second steps on DMMA), u rows in chunks that fit the scratch region.
+    {
+        const int qd = P.qd, ldC = ld_pad(nt), ldL = ld_pad(ns), ldT = ld_pad(NG * nt), ldV = ld_pad(ns * NG);
+        const int r0 = qd * (ldC + NG) + ldL + ldT, r1 = qd * (ldL + NG) + ldC + ldV;   // doubles per u row
+        const int nc0 = max(1, min(qd, P.region / r0)), nc1 = max(1, min(qd, P.region / r1));
+        for (int dc = 0; dc < ncells; ++dc) {
+            const CellBox c = cells[dc];
+            // rectangle with the singular corner at (ts, 0): corner C0, opposite corners
+            const double ct = (c.t0 == ts) ? c.t0 : c.t1, ch = (c.h0 == 0.0) ? c.h0 : c.h1;
+            const double ot = (c.t0 == ts) ? c.t1 : c.t0, oh = (c.h0 == 0.0) ? c.h1 : c.h0;
+            const double At = ot - ct, Bh = oh - ch, Wc = fabs(At * Bh);
+            for (int tri = 0; tri < 2; ++tri) {
+                const int nc = tri == 0 ? nc0 : nc1;
+                for (int a0 = 0; a0 < qd; a0 += nc) {
+                    const int na = min(nc, qd - a0);
+                    // scratch: tri 0  Cn [na qd][ldC], Gn [na qd][NG], Lr [na][ldL], Tr [na][ldT]
+                    //          tri 1  Ln [na qd][ldL], Gn [na qd][NG], Cr [na][ldC], Vr [na][ldV]
+                    double* Xn = Gs;                                   // Cn or Ln
+                    double* Gn = Xn + na * qd * (tri == 0 ? ldC : ldL);
+                    double* Xr = Gn + na * qd * NG;                    // Lr or Cr
+                    double* Yr = Xr + na * (tri == 0 ? ldL : ldC);     // Tr or Vr
+                    for (int n = tid; n < na * qd; n += NT) {
+                        const int a2 = n / qd, ib = n % qd, ia = a0 + a2;
+                        const double u = P.dx[ia], v = P.dx[ib];
+                        const double tt = tri == 0 ? ct + u * At : ct + u * At * (1.0 - v);
+                        const double hh = tri == 0 ? ch + u * v * Bh : ch + u * Bh;
+                        const double W = P.dw[ia] * P.dw[ib] * u * Wc;
+                        lagrange_eval(ns, tg, lm, tt, lb, dlb);
+                        double c1, s1;
+                        sincos(hs + hh, &s1, &c1);
+                        double G[9];
+                        node_kernel(kind, ns, nt, K, H, FA, FB, lb, dlb, c1, s1, W, x0, x1, x2, eta, P.dl, G);
+                        for (int q2 = 0; q2 < NG; ++q2) Gn[n * NG + q2] = G[q2];
+                        if (tri == 0) {
+                            trig_features(nt, c1, s1, Xn + n * ldC);
+                            if (ib == 0) for (int i = 0; i < ns; ++i) Xr[a2 * ldL + i] = lb[i];
+                        } else {
+                            for (int i = 0; i < ns; ++i) Xn[n * ldL + i] = lb[i];
+                            if (ib == 0) trig_features(nt, c1, s1, Xr + a2 * ldC);
+                        }
+                    }
+                    __syncthreads();
+                    if (tri == 0) {
+                        // T[a][q2][j] = sum_b G[(a,b)][q2] C_j(th_ab): one (a, j) per thread, NG sums
+                        for (int e = tid; e < na * nt; e += NT) {
+                            const int a2 = e / nt, j = e % nt;
+                            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                            for (int ib = 0; ib < qd; ++ib) {
+                                const int n = a2 * qd + ib;
+                                const double cj = Xn[n * ldC + j];
+                                for (int q2 = 0; q2 < NG; ++q2) acc[q2] = fma(Gn[n * NG + q2], cj, acc[q2]);
+                            }
+                            for (int q2 = 0; q2 < NG; ++q2) Yr[a2 * ldT + q2 * nt + j] = acc[q2];
+                        }
+                    } else {
+                        // V[a][(i,q2)] = sum_b l_i(t_ab) G[(a,b)][q2]: one (a, i) per thread, NG sums
+                        for (int e = tid; e < na * ns; e += NT) {
+                            const int a2 = e / ns, i = e % ns;
+                            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                            for (int ib = 0; ib < qd; ++ib) {
+                                const int n = a2 * qd + ib;
+                                const double li = Xn[n * ldL + i];
+                                for (int q2 = 0; q2 < NG; ++q2) acc[q2] = fma(Gn[n * NG + q2], li, acc[q2]);
+                            }
+                            for (int q2 = 0; q2 < NG; ++q2) Yr[a2 * ldV + i * NG + q2] = acc[q2];
+                        }
+                    }
+                    __syncthreads();
+                    if (tri == 0)
+                        dmma_gemm<NT>(ns, NG * nt, na, true,
+                                      [&](int row) { return row; },
+                                      [&](int ra, int k) { return Xr[k * ldL + ra]; },
+                                      [&](int k, int col) { return Yr[k * ldT + col]; },
+                                      [&](int row) { return row * (NG * nt); },
+                                      [&](int rc, int col) -> double& { return Bacc[rc + col]; });
+                    else
+                        dmma_gemm<NT>(ns * NG, nt, na, true,
+                                      [&](int row) { return row; },
+                                      [&](int ra, int k) { return Yr[k * ldV + ra]; },
+                                      [&](int k, int col) { return Xr[k * ldC + col]; },
+                                      [&](int row) { return row * nt; },
+                                      [&](int rc, int col) -> double& { return Bacc[rc + col]; });
+                    __syncthreads();
+                }
+            }
+        }
+    }
+}
+
 // NT threads per (target row) CTA: 256 (two CTAs per SM) for panel classes whose layout fits 113 KB,
 // else 512 (one CTA per SM, 16 warps to hide the phase latencies)
 template <int NT>
@@ -438,9 +542,8 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
     const int Ysz = max(Nnm * 3, nsm * (ntm / 2 + 1) * 6);
     double* Y = sm;
     double* Bacc = Y + Ysz;                           // [NG*ns][nt]  (Fourier-space accumulator)
-    double* Gs = Bacc + NG * Nnm;                     // [128][NG]
-    double* Ls = Gs + kQBatch * NG;                   // [128][ns]
-    double* Cs = Ls + kQBatch * nsm;                  // [128][ld_pad(nt)]
+    double* Gs = Bacc + NG * Nnm;                     // scratch region: P.region doubles (level buffers of
+                                                      // the quadtree, then the Duffy / regular-cell tables)
     double* TC = Gs + P.region;                       // [ntm] cos(2 pi m / nt) of the current panel
     double* TS = TC + ntm;                            // [ntm] sin(2 pi m / nt)
     CellBox* cells = reinterpret_cast<CellBox*>(TS + ntm);
@@ -658,58 +761,17 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         const int K = s_K;
         // Bacc layout [ns][NG][nt]: row (i, q2) holds the feature coefficients of l_i(t) C_m(th) for the
         // kernel component q2 -- so that the sum-factorized step (3b) below is ONE GEMM with N = NG nt.
-        // ---------------- (1) Duffy cells: nodes in batches of kQBatch (non-separable rule)
-        const int ldc = ld_pad(nt);
-        for (int base = 0; base < ntot; base += kQBatch) {
-            const int g = base + tid;
-            double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-            if (tid < kQBatch && g < ntot) {
-                const CellBox c = cells[g / (2 * P.qd * P.qd)];     // every Duffy cell has 2 qd^2 nodes
-                const int li = g % (2 * P.qd * P.qd);
-                // rectangle with the singular corner at (ts, 0): corner C0, opposite corners
-                const double ct = (c.t0 == ts) ? c.t0 : c.t1, ch = (c.h0 == 0.0) ? c.h0 : c.h1;
-                const double ot = (c.t0 == ts) ? c.t1 : c.t0, oh = (c.h0 == 0.0) ? c.h1 : c.h0;
-                const int tri = li / (P.qd * P.qd), r = li % (P.qd * P.qd);
-                const int ia = r / P.qd, ib = r % P.qd;
-                const double u = P.dx[ia], v = P.dx[ib];
-                // triangle 0: C0, (ot, ch), (ot, oh); triangle 1: C0, (ot, oh), (ct, oh)
-                double At, Ah, Bt, Bh;
-                if (tri == 0) { At = ot - ct; Ah = 0.0; Bt = ot - ct; Bh = oh - ch; }
-                else { At = ot - ct; Ah = oh - ch; Bt = 0.0; Bh = oh - ch; }
-                const double tt = ct + u * (At + v * (Bt - At));
-                const double hh = ch + u * (Ah + v * (Bh - Ah));
-                const double W = P.dw[ia] * P.dw[ib] * u * fabs(At * Bh - Ah * Bt);
-                lagrange_eval(ns, tg, lm, tt, lb, dlb);
-                double c1, s1;
-                sincos(hs + hh, &s1, &c1);
-                node_kernel(kind, ns, nt, K, H, FA, FB, lb, dlb, c1, s1, W, x0, x1, x2, eta, P.dl, G);
-                trig_features(nt, c1, s1, Cb);
-                for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = G[q2];
-                for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = lb[i];
-                for (int j = 0; j < nt; ++j) Cs[tid * ldc + j] = Cb[j];
-            } else if (tid < kQBatch) {
-                for (int q2 = 0; q2 < NG; ++q2) Gs[tid * NG + q2] = 0.0;
-                for (int i = 0; i < ns; ++i) Ls[tid * ns + i] = 0.0;
-                for (int j = 0; j < nt; ++j) Cs[tid * ldc + j] = 0.0;
-            }
-            __syncthreads();
-            // Bacc[(i,q2)][j] += sum_n G[n][q2] l_i(t_n) C[n][j]  (nodes past the batch end carry zeros)
-            dmma_gemm<NT>(ns * NG, nt, kQBatch, true,
-                      [&](int row) { return (row % NG) | ((row / NG) << 8); },
-                      [&](int ra, int k) { return Gs[k * NG + (ra & 255)] * Ls[k * ns + (ra >> 8)]; },
-                      [&](int k, int col) { return Cs[k * ldc + col]; },
-                      [&](int row) { return row * nt; },
-                      [&](int rc, int col) -> double& { return Bacc[rc + col]; });
-            __syncthreads();
-            NQ_MARK(3);
-        }
+        // ---------------- (1) Duffy cells (on-surface targets), in a function of its own (registers)
+        duffy_cells<NT>(kind, ns, nt, NG, K, H, FA, FB, tg, lm, P, cells, ntot / (2 * P.qd * P.qd), ts, hs, x0, x1, x2,
+                        eta, Gs, Bacc);
+        NQ_MARK(3);
         // ---------------- (2) regular cells: q x q tensor Gauss grids, contraction sum-factorized
         //   U[i][(b,q2)]     = sum_a l_i(t_a) G[(a,b)][q2]       (GEMM: M = ns, N = q NG, K = q)
         //   Bacc[(i,q2)][j] += sum_b U[i][(b,q2)] C_j(th_b)      (GEMM: M = ns NG, N = nt, K = q)
         // i.e. q^2 NG ns + q NG ns nt multiply-adds per cell instead of q^2 NG ns nt.  Every phase
         // (tables: features and rings at the q theta nodes, Lagrange rows at the q t nodes; kernel at the
         // nodes; U) covers a group of P.gp cells, one entry per thread; the U and C of P.nb cells (a
-        // multiple of gp) are stacked along K for one Bacc update.  All in the Duffy batch region (Gs..Cs).
+        // multiple of gp) are stacked along K for one Bacc update.  All in the scratch region (Gs..).
         // Without room for one whole cell (nb = gp = 1 only) the t rows go in chunks of ac.
         {
             const int q = P.q, nk = P.nb, ng = P.gp;
@@ -923,7 +985,7 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
     gl_nodes(P.qd, P.dx, P.dw);
     for (int a = 0; a < P.qd; ++a) { P.dx[a] = 0.5 * (P.dx[a] + 1.0); P.dw[a] *= 0.5; }
     const int TD = (kernel == SLB_LAPLACE_DL || kernel == SLB_LAPLACE_SL) ? 1 : 3;
-    // shared layout per class: the scratch region holds a Duffy batch (kQBatch nodes) or the regular-cell
+    // shared layout per class: the scratch region holds the quadtree levels, Duffy u-row chunks or the regular-cell
     // tables of nb cells; nb (<= 4) as large as the CTA shape allows -- 256 threads and <= 113 KB (two
     // CTAs per SM) when the Duffy-only layout fits that, else 512 threads and <= 227 KB -- else one cell
     // per update with t rows in chunks
