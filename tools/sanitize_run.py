@@ -1,4 +1,5 @@
-"""Tiny end-to-end exercise of every libslb kernel, for compute-sanitizer (dev tool):
+"""Tiny end-to-end exercise of every libslb kernel, for compute-sanitizer (dev tool; the shared
+GPU pool does not allow compute-sanitizer, so this is for a local machine):
     compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize_run.py
 Run it a second time with SLB_NEAR_CHUNKED_UNIFORM=1 (read once per process) to send the
 uniform blocks through the chunked near stream.  Covers both far paths, uniform and ragged (N4) meshes, the chunked near stream, the fold, GMRES,
