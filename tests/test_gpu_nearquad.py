@@ -224,3 +224,49 @@ def test_blocks_vs_independent_integrator(kind):
         ref = _exact_panel_integral(body, pr.P, k, pr.Ns, pr.Nt, sp, pr.x_trg[t], kind, eta, t0, h0)
         err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-3)
         assert err < 1e-8, (t, k, got, ref, err)
+
+
+# ------------------------------------------------------------------ edge cases of the entry point
+def _torus_inputs(pr):
+    rp = cu(pr.row_ptr, torch.int64)
+    pi = cu(pr.panel_idx, torch.int32)
+    return cu(pr.x_trg), rp, pi, cu(pr.y_c)
+
+
+def test_nearcorr_quad_edge_cases():
+    """empty CSR rows leave the blocks untouched; bad orders / panel grids are rejected with the
+    library's error codes; a target 1e-12 rho off the surface (but off the nodes) either gets finite
+    blocks or a clean 'cell budget' error -- never NaN, never a hang"""
+    _skip()
+    import paper_2310_00889_b200 as S
+    from paper_2310_00889_b200 import SlbError
+    pr = make_torus_problem(panels=6, Ns=8, Nt=8)
+    x, rp, pi, y = _torus_inputs(pr)
+    # every row empty
+    rp0 = torch.zeros_like(rp)
+    blocks = torch.full((8,), 7.0, dtype=torch.float64, device="cuda")
+    S.slb_nearcorr_quad(1, x, rp0, pi[:1], pr.Ns, pr.Nt, y, blocks)
+    assert torch.all(blocks == 7.0)
+    nb = pr.n_blocks_entries()
+    blocks = torch.empty(nb, dtype=torch.float64, device="cuda")
+    for order in (3, 25):
+        with pytest.raises(SlbError, match="INVALID_ARG|order"):
+            S.slb_nearcorr_quad(1, x, rp, pi, pr.Ns, pr.Nt, y, blocks, order=order)
+    with pytest.raises(SlbError, match="UNSUPPORTED|too large"):
+        S.slb_nearcorr_quad(1, x, rp, pi, pr.Ns, 66, y, blocks)
+    # a target just off the surface, between nodes, against its own panel (no trg_node: off-surface)
+    body = torus_body(1.0, 0.1)
+    s0, th0 = (0.5 + 0.37) / 6, 0.41                          # inside panel 0, between its nodes
+    p0 = body.surface(np.array([s0]), np.array([th0]))[0]
+    c0 = body.surface(np.array([s0]), np.array([th0 + np.pi]))[0]
+    nrm = (p0 - c0) / np.linalg.norm(p0 - c0)                 # outward (circular cross-section)
+    xt = cu((p0 + 1e-12 * 0.1 * nrm)[None, :])
+    rp1 = cu(np.array([0, 1]), torch.int64)
+    pi1 = cu(np.array([0]), torch.int32)
+    b1 = torch.empty(pr.Ns * pr.Nt, dtype=torch.float64, device="cuda")
+    try:
+        S.slb_nearcorr_quad(1, xt, rp1, pi1, pr.Ns, pr.Nt, y, b1, order=14)
+    except SlbError as e:
+        assert "cell budget" in str(e) or "UNSUPPORTED" in str(e), e
+    else:
+        assert torch.isfinite(b1).all()
