@@ -144,16 +144,15 @@ __global__ void pack_rec_kernel(int64_t M, const double* __restrict__ geo, const
 
 constexpr int kJ = 2;
 
+// environment knobs: read once (function-local statics: thread-safe initialisation)
 static int const_count_mode() {
-    static int v = -1;
     // 1 (default): per-pair count -- measured faster than flag+recount (profiles/r01_bench_c4_cm*.json)
-    if (v < 0) { const char* e = getenv("SLB_CONST_COUNT"); v = (e && e[0] == '0') ? 0 : 1; }
+    static const int v = [] { const char* e = getenv("SLB_CONST_COUNT"); return (e && e[0] == '0') ? 0 : 1; }();
     return v;
 }
 
 static int const_variant() {
-    static int v = -1;
-    if (v < 0) { const char* e = getenv("SLB_CONST_VARIANT"); v = e ? atoi(e) : 0; }
+    static const int v = [] { const char* e = getenv("SLB_CONST_VARIANT"); return e ? atoi(e) : 0; }();
     return v;
 }
 

@@ -333,11 +333,7 @@ static slb_status launch_far(const FarPlan& plan, int64_t T, const double* x, co
 
 // Tuning variants of the large-M Stokes kernel (selected by SLB_FAR_VARIANT; 0 = default).
 static int far_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("SLB_FAR_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
+    static const int v = [] { const char* e = getenv("SLB_FAR_VARIANT"); return e ? atoi(e) : 0; }();
     return v;
 }
 

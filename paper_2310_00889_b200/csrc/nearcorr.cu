@@ -281,8 +281,10 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
                                      int ucols = 0) {
     if (T <= 0) return SLB_OK;
     const int widest2 = tdim * (rag.boff ? rag.max_cols : ucols) / 2;
-    static int chunk = -1;
-    if (chunk < 0) { const char* e = getenv("SLB_NEAR_CHUNK"); chunk = e ? std::max(64, atoi(e)) : kChunk2; }
+    static const int chunk = [] {
+        const char* e = getenv("SLB_NEAR_CHUNK");
+        return e ? std::max(64, atoi(e)) : kChunk2;
+    }();
     const int S = std::min(widest2, chunk);
     const size_t smem = (size_t)kNearWarps * kNearStages * S * 16;
     G = std::max(1, G);
@@ -318,8 +320,10 @@ slb_status finalize_launch(const FarPlan& plan, int64_t T, int tdim, int cols, c
     // uniform blocks wider than 600 double2 (c2: 11.5 KB, c3: 17 KB) also stream through the chunked
     // kernel: c3 near 0.78 -> 0.62 ms, c2 0.150 -> 0.120 ms; c4/c5's 8.6 KB blocks stay on the plain
     // ring (chunking them: c4 2.46 -> 2.84 ms)
-    static int chunk_uniform = -1;
-    if (chunk_uniform < 0) { const char* e = getenv("SLB_NEAR_CHUNKED_UNIFORM"); chunk_uniform = e ? atoi(e) : 600; }
+    static const int chunk_uniform = [] {
+        const char* e = getenv("SLB_NEAR_CHUNKED_UNIFORM");
+        return e ? atoi(e) : 600;
+    }();
     if (rag.boff || (chunk_uniform && tdim * cols / 2 > chunk_uniform))
         return near_ragged_launch(1, T, tdim, row_ptr, panel_idx, blocks, sigma_c_global, partials, plan.n_chunks,
                                   n_on, c_id, sig_local, Lsig, u, G, s, rag, cols);

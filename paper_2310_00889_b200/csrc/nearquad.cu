@@ -721,7 +721,11 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
         const double ts = s_par[0], hs = s_par[1];
         const int ntot = s_ntot, nreg = s_nreg;   // Duffy-rule nodes, regular cells
 #ifdef SLB_NQ_PROFILE
-        if (tid == 0) { atomicAdd(&g_nq_cnt[0], (unsigned long long)s_nreg); atomicAdd(&g_nq_cnt[1], (unsigned long long)s_ntot); atomicAdd(&g_nq_cnt[2], 1ull); }
+        if (tid == 0) {
+            atomicAdd(&g_nq_cnt[0], (unsigned long long)s_nreg);
+            atomicAdd(&g_nq_cnt[1], (unsigned long long)s_ntot);
+            atomicAdd(&g_nq_cnt[2], 1ull);
+        }
 #endif
         // ---------------- Fourier coefficients of every GL ring of the panel (trig interpolant in th):
         //   ring(th) = A_0 + 2 sum_{l=1}^{N/2-1} (A_l cos l th + B_l sin l th) + A_{N/2} cos(N th / 2),
@@ -999,8 +1003,11 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
         const bool small = base + sizeof(double) * duffy <= 113 * 1024;
         const size_t budget = small ? 113 * 1024 : 227 * 1024;
         const int threads = small ? 256 : 512;
-        static int nb_max = -1;          // SLB_NQ_NB: cap on the cells per group (tuning knob)
-        if (nb_max < 0) { const char* e = getenv("SLB_NQ_NB"); nb_max = e ? std::max(1, std::min(4, atoi(e))) : 4; }
+        // SLB_NQ_NB: cap on the cells per group (tuning knob; read once, thread-safe static)
+        static const int nb_max = [] {
+            const char* e = getenv("SLB_NQ_NB");
+            return e ? std::max(1, std::min(4, atoi(e))) : 4;
+        }();
         // (cells per update, per phase): K-stacking first, then phase groups
         static const int cand[8][2] = {{4, 4}, {4, 2}, {3, 3}, {2, 2}, {4, 1}, {3, 1}, {2, 1}, {1, 1}};
         for (const auto& c : cand) {
