@@ -322,12 +322,13 @@ __device__ __forceinline__ void point_kernel(int kind, const double* y, const do
 // then A(m, k) = fa(ra, k); rc = crow(m), then C(m, n) = fc(rc, n) (a shared-memory reference).  Work
 // unit of a warp: one 8-row strip x up to 8 column tiles, the A fragment loaded once per k-step.
 // acc = false: C is overwritten.
-template <int NT, class FRA, class FA, class FB, class FRC, class FC>
+template <int NT, int TPG = 8, class FRA, class FA, class FB, class FRC, class FC>
 __device__ __forceinline__ void dmma_gemm(int M, int N, int Kn, bool acc, FRA arow, FA fa, FB fb, FRC crow, FC fc) {
+    // TPG: column tiles per work unit (<= 8; fewer = more, smaller units for many warps)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, fg = lane >> 2, ftq = lane & 3;
-    const int mtl = (M + 7) / 8, ntl = (N + 7) / 8, ngrp = (ntl + 7) / 8;
+    const int mtl = (M + 7) / 8, ntl = (N + 7) / 8, ngrp = (ntl + TPG - 1) / TPG;
     for (int u = warp; u < mtl * ngrp; u += NT / 32) {
-        const int m0 = (u / ngrp) * 8, ct0 = (u % ngrp) * 8, nct = min(8, ntl - ct0);
+        const int m0 = (u / ngrp) * 8, ct0 = (u % ngrp) * TPG, nct = min(TPG, ntl - ct0);
         const int row = m0 + fg;
         const bool rok = row < M;
         const int ra = rok ? arow(row) : 0, rc = rok ? crow(row) : 0;
@@ -922,7 +923,8 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     NQ_MARK(9);
                 }
                 if ((g0 + gn) % nk == 0 || g0 + gn == nreg) {
-                    dmma_gemm<NT>(ns * NG, nt, ((g0 + gn - 1) % nk + 1) * q, true,
+                    // 16 warps: half-width units balance the 18 row strips of a 16 x 64 panel
+                    dmma_gemm<NT, NT == 512 ? 4 : 8>(ns * NG, nt, ((g0 + gn - 1) % nk + 1) * q, true,
                                   [&](int row) { return (row / NG) * ldU + row % NG; },
                                   [&](int ra, int k) { return Uc[ra + k * NG]; },
                                   [&](int k, int col) { return Cc[k * ldC + col]; },
