@@ -19,10 +19,11 @@
 //     transform (two triangles each, Jacobian u cancels the 1/r singularity), refined until their
 //     aspect ratio and size are moderate;
 //   * q x q Gauss-Legendre per regular cell, 2 q_d^2 nodes per Duffy cell; the contraction with the
-//     basis runs on the FP64 tensor cores: Duffy nodes in batches of 128 through shared memory,
-//     regular cells sum-factorized (theta features first, then the Lagrange rows: the tensor-grid
-//     rule makes the per-node cost NG nt (1 + ns / q) instead of NG nt ns).
-// One CTA (16 warps) per target row; fixed summation order -> deterministic.
+//     basis is sum-factorized and runs on the FP64 tensor cores: regular cells are tensor grids in
+//     (t, th) (Lagrange rows first, then the theta features: per-node cost NG ns (1 + nt / q)
+//     instead of NG ns nt), each Duffy triangle is separable in one direction (factorized along it);
+//   * the quadtree is built level by level across the CTA (block prefix sums place the cells).
+// One CTA (8 or 16 warps by panel class) per target row; fixed summation order -> deterministic.
 #include <algorithm>
 #include <cstdio>
 #include <cmath>
@@ -33,7 +34,7 @@
 
 namespace slb {
 
-constexpr int kQBatch = 128;     // scratch region >= kQBatch (NG + ns + ld_pad(nt)) doubles
+constexpr int kQBatch = 128;     // minimum scratch region: kQBatch (NG + ns + ld_pad(nt)) doubles
 constexpr int kMaxCells = 768;
 constexpr int kMaxLevels = 64;    // quadtree depth bound
 constexpr int kMaxNsQ = 32, kMaxNtQ = 64, kMaxQ = 24;
