@@ -500,14 +500,14 @@ __device__ __noinline__ void duffy_cells(int kind, int ns, int nt, int NG, int K
                     }
                     __syncthreads();
                     if (tri == 0)
-                        dmma_gemm<NT>(ns, NG * nt, na, true,
+                        dmma_gemm<NT, 4>(ns, NG * nt, na, true,
                                       [&](int row) { return row; },
                                       [&](int ra, int k) { return Xr[k * ldL + ra]; },
                                       [&](int k, int col) { return Yr[k * ldT + col]; },
                                       [&](int row) { return row * (NG * nt); },
                                       [&](int rc, int col) -> double& { return Bacc[rc + col]; });
                     else
-                        dmma_gemm<NT>(ns * NG, nt, na, true,
+                        dmma_gemm<NT, 4>(ns * NG, nt, na, true,
                                       [&](int row) { return row; },
                                       [&](int ra, int k) { return Yr[k * ldV + ra]; },
                                       [&](int k, int col) { return Xr[k * ldC + col]; },
@@ -914,7 +914,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     __syncthreads();
                     NQ_MARK(8);
                     for (int sl = 0; sl < gn; ++sl)
-                        dmma_gemm<NT>(ns, q * NG, na, a0 > 0,
+                        dmma_gemm<NT, 4>(ns, q * NG, na, a0 > 0,
                                       [&](int row) { return row; },
                                       [&](int ra, int k) { return Lc[(sl * ac + k) * ldL + ra]; },
                                       [&](int k, int col) { return Gc[(sl * ac + k) * ldG + col]; },
