@@ -914,7 +914,7 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
                     __syncthreads();
                     NQ_MARK(8);
                     for (int sl = 0; sl < gn; ++sl)
-                        dmma_gemm<NT, 4>(ns, q * NG, na, a0 > 0,
+                        dmma_gemm<NT, NT == 512 ? 2 : 4>(ns, q * NG, na, a0 > 0,
                                       [&](int row) { return row; },
                                       [&](int ra, int k) { return Lc[(sl * ac + k) * ldL + ra]; },
                                       [&](int k, int col) { return Gc[(sl * ac + k) * ldG + col]; },
