@@ -81,9 +81,39 @@ class ClockSampler:
 
 
 def setup_dist(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """World from torchrun's env.  `--gpus N` (N > 1) without WORLD_SIZE re-launches this script
+    under torch.distributed.run with N ranks (one per GPU); fewer visible GPUs than N is an error."""
+    if "WORLD_SIZE" not in os.environ:
+        n = args.gpus if args.gpus is not None else 1
+        if n > 1:
+            if args.impl == "ours":
+                import torch
+                have = torch.cuda.device_count()
+                if have < n:
+                    sys.stderr.write(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible\n")
+                    sys.exit(2)
+            import socket
+            so = socket.socket()
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+            so.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                   "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            sys.stdout.flush()
+            os.execv(sys.executable, cmd)
+        return 1, 0, 0
+    world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus is not None and args.gpus != world:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
+    if args.impl == "ours":
+        import torch
+        if torch.cuda.device_count() <= local:
+            sys.stderr.write(f"bench.py: rank {rank} (LOCAL_RANK {local}) has no GPU: "
+                             f"{torch.cuda.device_count()} visible\n")
+            sys.exit(2)
     return world, rank, local
 
 
@@ -132,7 +162,16 @@ def cpu_baseline_run(pr, seconds_target=15.0, rows_n=None, gpu_u=None):
             "seconds": t_prep + t_rows, "pairs_per_s": pr.pairs() / t_full}
 
 
-def config_info(pr, world, l2_note):
+def l2_note(pr):
+    """Timing rule: inputs larger than L2 between timed iterations (stated per workload; identical in
+    both arms' config)."""
+    big = pr.M * 80 + pr.n_blocks_entries() * 8
+    return (f"inputs larger than L2 (fine sources {pr.M * 80 / 1e6:.0f} MB, near blocks "
+            f"{pr.n_blocks_entries() * 8 / 1e9:.1f} GB)" if big > 126e6 else
+            f"inputs {big / 1e6:.1f} MB < 126 MB L2: L2-resident between applies (small config)")
+
+
+def config_info(pr, world):
     return {"workload": pr.name, "kernel": "laplace_dl" if pr.kernel == 1 else "stokes_sl+dl",
             "operator": "K(I-L)+L mobility" if pr.projector else ("I/2 + D" if pr.kernel == 1 else "I/2 + D + eta S"),
             "bodies": pr.n_bodies, "panels": pr.P,
@@ -143,7 +182,7 @@ def config_info(pr, world, l2_note):
             "pairs_per_apply": pr.pairs(), "near_blocks": pr.nnz,
             "block_shape": [pr.tdim, pr.Nn * pr.sdim] if not pr.ragged else [pr.tdim, "N_n^(k) s_dim (ragged)"],
             "parallelism": f"targets sharded over {world} GPU(s), all-gather of fine density",
-            "l2": l2_note, "seed": pr.seed}
+            "l2": l2_note(pr), "seed": pr.seed}
 
 
 def run_reference(args, world, rank):
@@ -162,7 +201,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "matvec/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_info(pr, world, "n/a (CPU oracle)"),
+            "config": config_info(pr, world),
             "cpu_baseline": {"value": v, "unit": "matvec/s", "cores": res["cores"], "kind": "oracle",
                              "sample": res["sample"], "cpu_model": res.get("cpu_model"), "nproc": res.get("nproc")},
             "e2e": {"value": v, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -171,7 +210,7 @@ def run_reference(args, world, rank):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("SLB_BENCH_CONFIG", "c5"))
@@ -293,8 +332,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_info(pr, world, "inputs larger than L2 (fine sources "
-                                  f"{pr.M * 80 / 1e6:.0f} MB, near blocks {pr.n_blocks_entries() * 8 / 1e9:.1f} GB)"),
+            "config": config_info(pr, world),
             "pairs_per_s": pr.pairs() * value,
             "roofline": {"bound": "alu", "kernel": "far_const_kernel (FP64 DFMA pipe; far_kernel below M = 2^16)", "achieved": far_tf,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": far_tf / FP64_PEAK_TFLOPS,

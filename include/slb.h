@@ -34,6 +34,14 @@
  * Determinism: for fixed inputs every function is bitwise reproducible, and slb_matvec gives
  * bitwise-identical u for any number of ranks (the per-target summation order depends only
  * on the global source count M).
+ * Concurrency: one operator must not be used from two threads at once; DISTINCT operators and the
+ *   stand-alone calls may run concurrently on any streams and host threads.  The one library-wide
+ *   device resource -- the 64 KB __constant__ source-tile bank of the large-M far field -- is
+ *   serialised inside the library: each slb_matvec that uses it takes a host lock, makes its stream
+ *   wait on the device's "bank" event (recorded by the previous user), launches its tile graph and
+ *   re-records the event, so users of the bank run one after another on the device in issue order.
+ *   (Consequence: two large operators applied "concurrently" overlap everything except their far
+ *   fields.)  Kernel shared-memory limits are raised once per kernel to the device maximum.
  */
 #ifndef SLB_H
 #define SLB_H
@@ -191,6 +199,14 @@ typedef struct slb_operator slb_operator;
 slb_status slb_comm_unique_id(unsigned char id[128]);
 slb_status slb_comm_create(const unsigned char id[128], int nranks, int rank, slb_comm** out);
 slb_status slb_comm_destroy(slb_comm* c);
+/* Collectives issued through c so far: out[0] = ncclAllGather calls (create-time panel-range gather
+ * and the per-apply in-place gathers of the fine records and the coarse density), out[1] =
+ * ncclBroadcast calls (the grouped in-place broadcasts that replace the all-gather when the rank
+ * shards are unequal, or when SLB_FORCE_GROUPED_GATHER=1), out[2] = ncclAllReduce calls (slb_gmres
+ * dot products).  Every operator/solver holding a communicator issues them, a one-rank
+ * communicator included (NCCL's gather is then an identity, the offsets and counts are the
+ * multi-rank ones).  Host counters; no synchronisation. */
+slb_status slb_comm_collective_counts(const slb_comm* c, long long out[3]);
 
 typedef struct {
     slb_kernel kernel;

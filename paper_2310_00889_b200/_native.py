@@ -47,6 +47,7 @@ _SIGS = {
     "slb_comm_unique_id": (I32, [P]),
     "slb_comm_create": (I32, [P, I32, I32, ctypes.POINTER(P)]),
     "slb_comm_destroy": (I32, [P]),
+    "slb_comm_collective_counts": (I32, [P, ctypes.POINTER(ctypes.c_longlong)]),
     "slb_operator_create": (I32, [ctypes.POINTER(OperatorDesc), P, ctypes.POINTER(P)]),
     "slb_matvec": (I32, [P, P, P, P]),
     "slb_matvec_host": (I32, [P, P, P, P]),

@@ -196,6 +196,12 @@ class Comm:
         self.h = h
         self.nranks, self.rank = nranks, rank
 
+    def collective_counts(self):
+        """(allgather, broadcast, allreduce) NCCL calls issued through this communicator."""
+        out = (ctypes.c_longlong * 3)()
+        check(lib().slb_comm_collective_counts(self.h, out))
+        return {"allgather": out[0], "broadcast": out[1], "allreduce": out[2]}
+
     def close(self):
         if self.h:
             lib().slb_comm_destroy(self.h)

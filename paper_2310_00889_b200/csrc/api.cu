@@ -1,10 +1,13 @@
 // api.cu -- C-ABI entry points for the stand-alone steps of the operator apply, plus the
 // error/status plumbing shared by the library.  See include/slb.h for the contract.
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <array>
 #include <memory>
 #include <map>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 #include "common.cuh"
@@ -12,7 +15,7 @@
 namespace slb {
 
 static thread_local std::string g_err;
-unsigned long long g_launch_count = 0;
+std::atomic<unsigned long long> g_launch_count{0};
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -34,24 +37,41 @@ slb_status check_sticky(const char* what) {
     return SLB_OK;
 }
 
+// Function-local static initialisers: thread-safe one-time initialisation (C++11).
 int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static const int n = [] {
+        int dev = 0, v = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
     return n;
 }
 
 unsigned long long* coincident_counter() {
-    static unsigned long long* p = nullptr;
-    if (!p) {
-        if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-        cudaMemset(p, 0, sizeof(unsigned long long));
-    }
+    static unsigned long long* const p = [] {
+        unsigned long long* q = nullptr;
+        if (cudaMalloc(&q, sizeof(unsigned long long)) != cudaSuccess) return (unsigned long long*)nullptr;
+        cudaMemset(q, 0, sizeof(unsigned long long));
+        cudaDeviceSynchronize();
+        return q;
+    }();
     return p;
+}
+
+// Opt a kernel in to the device's full dynamic shared memory once (the attribute is process-wide;
+// setting it to the maximum once, under a lock, means no launch can lower it under another).
+slb_status smem_optin(const void* fn) {
+    static std::mutex mu;
+    static std::set<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(fn)) return SLB_OK;
+    int dev = 0, mx = 0;
+    SLB_CUDA(cudaGetDevice(&dev));
+    SLB_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    SLB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    done.insert(fn);
+    return SLB_OK;
 }
 
 }  // namespace slb

@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
+#include <mutex>
 #include <string>
 #include "../../include/slb.h"
 
@@ -126,7 +128,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 #endif  // __CUDACC__
 
 // Kernel launch bookkeeping for launch accounting.
-extern unsigned long long g_launch_count;
+extern std::atomic<unsigned long long> g_launch_count;
+
+// Raise a kernel's dynamic shared-memory limit to the device maximum, once per kernel (thread-safe).
+slb_status smem_optin(const void* fn);
 
 int num_sms();
 
@@ -161,6 +166,17 @@ slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, 
                            cudaEvent_t fork, cudaEvent_t* join, int64_t* launches);
 slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s);
 int far_const_bufs(int64_t M);   // streams / partial arrays for M sources
+// Scoped host lock + device event chain serialising all users of the constant bank (farconst.cu).
+class ConstBankLock {
+  public:
+    ConstBankLock();
+    ~ConstBankLock();
+    slb_status acquire(cudaStream_t s);   // s waits for the previous user's last tile
+    slb_status release(cudaStream_t s);   // record: the next user waits for s's work so far
+  private:
+    std::unique_lock<std::mutex> lk_;
+    int dev_ = 0;
+};
 int far_const_tile(int64_t M);   // sources per constant-bank tile
 slb_status far_const_prepare();
 

@@ -16,6 +16,7 @@
 // tails.  The whole sequence is captured once into a CUDA graph per operator and replayed per apply.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 #include "common.cuh"
 
@@ -244,6 +245,35 @@ slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, doub
     pack_rec_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, geo, dyn, rec);
     ++g_launch_count;
     return check_launch("pack_rec_kernel");
+}
+
+// ---- library-wide serialisation of the constant bank (distinct operators are safe
+// to apply concurrently).  c_rec is one per device for the whole process; every issue of the tile
+// sequence (graph launch or direct) holds this lock, waits on the device's bank event (recorded by
+// the previous user, a no-op before the first) and re-records it after its last tile, so the tile
+// copies of two operators can never interleave on the device.
+namespace {
+constexpr int kMaxDevs = 64;
+std::mutex g_bank_mu;
+cudaEvent_t g_bank_ev[kMaxDevs] = {};
+}
+
+ConstBankLock::ConstBankLock() : lk_(g_bank_mu) {}
+ConstBankLock::~ConstBankLock() = default;
+
+slb_status ConstBankLock::acquire(cudaStream_t s) {
+    int dev = 0;
+    SLB_CUDA(cudaGetDevice(&dev));
+    SLB_REQUIRE(dev >= 0 && dev < kMaxDevs, SLB_ERR_UNSUPPORTED, "device ordinal beyond the bank table");
+    if (!g_bank_ev[dev]) SLB_CUDA(cudaEventCreateWithFlags(&g_bank_ev[dev], cudaEventDisableTiming));
+    dev_ = dev;
+    SLB_CUDA(cudaStreamWaitEvent(s, g_bank_ev[dev], 0));
+    return SLB_OK;
+}
+
+slb_status ConstBankLock::release(cudaStream_t s) {
+    SLB_CUDA(cudaEventRecord(g_bank_ev[dev_], s));
+    return SLB_OK;
 }
 
 int far_const_bufs(int64_t M) { return const_bufs_for(M); }

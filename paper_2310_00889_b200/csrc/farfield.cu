@@ -10,7 +10,7 @@
 // memory ring filled by TMA bulk copies (cp.async.bulk + mbarrier complete_tx), issued by a
 // single elected thread.  Every thread reads each source record as a broadcast (no bank
 // conflicts).  1/r comes from MUFU.RSQ64H plus one cubic correction (5 FP64 instructions).
-// The per-pair algebra is factored so the Stokes pair costs 28 FP64-pipe instructions
+// The per-pair algebra is factored so the Stokes pair costs 27 FP64-pipe instructions
 // (vs 39 algorithmic flops, FMA = 2):
 //   u += g/|r| + r (r.g)/|r|^3 [1 + (r.a)/|r|^2],   g = e w sigma, a = (3/(4 pi e)) n, e = eta/(8 pi)
 // Summation order per target is fixed by (chunk, split), which depend only on M, so results
@@ -318,11 +318,9 @@ static slb_status launch_far(const FarPlan& plan, int64_t T, const double* x, co
                              cudaStream_t s) {
     constexpr int TPC = ((kThreads / 32) / SPLIT) * 32 * J;
     const size_t smem = (size_t)2 * kTile * (kGeo + kDyn) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        SLB_CUDA(cudaFuncSetAttribute(far_kernel<KIND, J, SPLIT, MINB, UNR>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+    {
+        slb_status st_ = smem_optin((const void*)far_kernel<KIND, J, SPLIT, MINB, UNR>);
+        if (st_ != SLB_OK) return st_;
     }
     dim3 grid((unsigned)((T + TPC - 1) / TPC), (unsigned)plan.n_chunks);
     far_kernel<KIND, J, SPLIT, MINB, UNR><<<grid, kThreads, smem, s>>>(T, x, geo, dyn, plan.M, plan.chunk,

@@ -75,9 +75,10 @@ struct Gm {
         multidot_kernel<<<grid, kDotThreads, 0, s>>>(n, k, V, ld, w, partial);
         sum_partials_kernel<<<(k + 63) / 64, 64, 0, s>>>(k, nblk, partial, dots_d);
         g_launch_count += 2;
-        if (op->comm && op->comm->nranks > 1) {
+        if (op->comm) {                       // every communicator, one rank included (the path is exercised)
             NcclApi& A = nccl();
             SLB_NCCL(A.AllReduce(dots_d, dots_d, (size_t)k, ncclDouble, ncclSum, op->comm->comm, s));
+            op->comm->n_allreduce++;
         }
         SLB_CUDA(cudaMemcpyAsync(out, dots_d, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
         SLB_CUDA(cudaStreamSynchronize(s));

@@ -136,8 +136,7 @@ static slb_status near_stream_launch(int mode, int64_t T, int tdim, int cols, co
     const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
 #define NEAR_LAUNCH(TD, MODE)                                                                               \
     do {                                                                                                    \
-        SLB_CUDA(cudaFuncSetAttribute(near_stream_kernel<TD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                      (int)smem));                                                          \
+        { slb_status st_ = smem_optin((const void*)near_stream_kernel<TD, MODE>); if (st_ != SLB_OK) return st_; } \
         near_stream_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(T, cols2, row_ptr, panel_idx, blocks,  \
                                                                          sigma_c, partials, n_chunks, n_on, c_id, \
                                                                          sig_local, Lsig, u, G);            \
@@ -291,8 +290,7 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
     const unsigned grid = (unsigned)std::max<int64_t>(1, (T + (int64_t)G * kNearWarps - 1) / ((int64_t)G * kNearWarps));
 #define RAG_LAUNCH(TD, MODE)                                                                                  \
     do {                                                                                                      \
-        SLB_CUDA(cudaFuncSetAttribute(near_stream_ragged_kernel<TD, MODE>,                                    \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));               \
+        { slb_status st_ = smem_optin((const void*)near_stream_ragged_kernel<TD, MODE>); if (st_ != SLB_OK) return st_; } \
         near_stream_ragged_kernel<TD, MODE><<<grid, kNearWarps * 32, smem, s>>>(                              \
             T, S, row_ptr, panel_idx, blocks, sigma_c, partials, n_chunks, n_on, c_id, sig_local, Lsig, u, G,  \
             rag.cn0, rag.boff, tdim, ucols / 2, rag.bmeta);                                                   \
@@ -309,6 +307,11 @@ static slb_status near_ragged_launch(int mode, int64_t T, int tdim, const int64_
 
 slb_status near_apply_launch(int64_t T, int tdim, int cols, const int64_t* row_ptr, const int32_t* panel_idx,
                              const double* blocks, const double* sigma_c, double* u, cudaStream_t s) {
+    // same width rule as finalize_launch: blocks wider than 600 double2 (and every block the whole-block
+    // ring cannot hold, e.g. Stokes 12 x 32 or 16 x 64 panels) stream through the chunked kernel
+    if (tdim * cols / 2 > 600)
+        return near_ragged_launch(0, T, tdim, row_ptr, panel_idx, blocks, sigma_c, nullptr, 0, 0, 0.0, nullptr,
+                                  nullptr, u, 4, s, RagNear(), cols);
     return near_stream_launch(0, T, tdim, cols, row_ptr, panel_idx, blocks, sigma_c, nullptr, 0, 0, 0.0, nullptr,
                               nullptr, u, 4, s);
 }
@@ -431,7 +434,7 @@ slb_status fold_launch(FarKind kind, int64_t T, const double* x_trg, const int64
     while (rch > 1 && smem_of(rch) > 227 * 1024) rch = (rch + 1) / 2;
     const size_t smem = smem_of(rch);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "fold: grid too large for shared memory");
-    SLB_CUDA(cudaFuncSetAttribute(fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    { slb_status st_ = smem_optin((const void*)fold_kernel); if (st_ != SLB_OK) return st_; }
     fold_kernel<<<(unsigned)T, 128, smem, s>>>((int)kind, T, x_trg, row_ptr, panel_idx, ip, y_fine, n_fine,
                                               w_fine, eta_fine, eta, blocks, pbucket, bucket, fn0, boff, rch);
     ++g_launch_count;

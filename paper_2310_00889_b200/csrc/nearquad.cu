@@ -1030,8 +1030,8 @@ static slb_status nearquad_run(slb_kernel kernel, int64_t n_trg, const double* x
                     "nearquad: rule order too large for the panel grid");
         smem_max = std::max(smem_max, L.smem);
     }
-    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
-    SLB_CUDA(cudaFuncSetAttribute(nearquad_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+    { slb_status st_ = smem_optin((const void*)nearquad_kernel<256>); if (st_ != SLB_OK) return st_; }
+    { slb_status st_ = smem_optin((const void*)nearquad_kernel<512>); if (st_ != SLB_OK) return st_; }
     int* st = nullptr;
     SLB_CUDA(cudaMallocAsync(&st, sizeof(int), s));
     SLB_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));

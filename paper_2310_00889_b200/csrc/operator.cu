@@ -21,18 +21,27 @@ using namespace slb;
 
 // In-place all-gather of per-panel data: rank r owns elements [E(ranges[r]), E(ranges[r+1])) with
 // E(p) = p * per_panel (uniform) or off[p] * unit (ragged panels, off = node offsets).
+// Runs for EVERY communicator, a one-rank one included (then NCCL's gather is an identity, but the
+// offsets, counts and calls are the multi-rank ones).  SLB_FORCE_GROUPED_GATHER=1 (tests) takes the
+// unequal-shard path (grouped in-place broadcasts) even when the shards are equal.
+static bool force_grouped_gather() {
+    static const bool v = [] { const char* e = getenv("SLB_FORCE_GROUPED_GATHER"); return e && e[0] == '1'; }();
+    return v;
+}
+
 static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cudaStream_t s,
                             const std::vector<int64_t>* off = nullptr, int64_t unit = 1) {
     slb_comm* c = op->comm;
-    if (!c || c->nranks == 1) return SLB_OK;
+    if (!c) return SLB_OK;
     NcclApi& A = nccl();
     auto E = [&](int64_t p) { return off ? (*off)[p] * unit : p * per_panel; };
-    bool equal = true;
+    bool equal = !force_grouped_gather();
     for (int r = 1; r < c->nranks; ++r)
         if (E(op->ranges[r + 1]) - E(op->ranges[r]) != E(op->ranges[1]) - E(op->ranges[0])) equal = false;
     if (equal) {
         size_t cnt = (size_t)(E(op->ranges[1]) - E(op->ranges[0]));
         SLB_NCCL(A.AllGather(buf + E(op->ranges[c->rank]), buf, cnt, ncclDouble, c->comm, s));
+        c->n_allgather++;
     } else {
         SLB_NCCL(A.GroupStart());
         for (int r = 0; r < c->nranks; ++r) {
@@ -40,6 +49,7 @@ static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cu
             if (cnt == 0) continue;
             double* p = buf + E(op->ranges[r]);
             SLB_NCCL(A.Broadcast(p, p, cnt, ncclDouble, r, c->comm, s));
+            c->n_broadcast++;
         }
         SLB_NCCL(A.GroupEnd());
     }
@@ -92,6 +102,14 @@ slb_status slb_comm_create(const unsigned char id[128], int nranks, int rank, sl
         return SLB_ERR_NCCL;
     }
     *out = c;
+    return SLB_OK;
+}
+
+slb_status slb_comm_collective_counts(const slb_comm* c, long long out[3]) {
+    SLB_REQUIRE(c && out, SLB_ERR_INVALID_ARG, "null argument");
+    out[0] = c->n_allgather.load();
+    out[1] = c->n_broadcast.load();
+    out[2] = c->n_allreduce.load();
     return SLB_OK;
 }
 
@@ -263,14 +281,15 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     } while (0)
     // rank panel ranges
     op->ranges.assign(R + 1, 0);
-    if (R == 1) {
+    if (!comm) {
         op->ranges[1] = d->n_panels_global;
-    } else {
+    } else {                                      // every communicator (one rank included) gathers the ranges
         int64_t* dr = nullptr;
         OPCUDA(cudaMalloc(&dr, sizeof(int64_t) * 2 * R));
         int64_t mine[2] = {d->panel_begin, d->panel_end};
         OPCUDA(cudaMemcpy(dr + 2 * comm->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
         ncclResult_t r = nccl().AllGather(dr + 2 * comm->rank, dr, 2, ncclInt64, comm->comm, s);
+        comm->n_allgather++;
         std::vector<int64_t> all(2 * R);
         cudaError_t e = cudaMemcpy(all.data(), dr, sizeof(int64_t) * 2 * R, cudaMemcpyDeviceToHost);
         cudaFree(dr);
@@ -474,6 +493,9 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     if (op->use_const) {
         st = pack_rec_launch(op->M, op->geo, op->dyn, op->rec, s);
         if (st != SLB_OK) return st;
+        ConstBankLock bank;                        // the __constant__ bank is one per device (slb.h)
+        st = bank.acquire(s);
+        if (st != SLB_OK) return st;
         if (op->graph) {
             SLB_CUDA(cudaGraphLaunch(op->graph, s));
             g_launch_count += (unsigned long long)op->const_launches;
@@ -484,6 +506,8 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
             if (st != SLB_OK) return st;
             g_launch_count += (unsigned long long)nl;
         }
+        st = bank.release(s);
+        if (st != SLB_OK) return st;
     } else {
         st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
         if (st != SLB_OK) return st;

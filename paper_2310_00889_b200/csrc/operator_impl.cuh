@@ -62,6 +62,8 @@ inline NcclApi& nccl() {
 struct slb_comm {
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
+    // collectives issued through this communicator (slb_comm_collective_counts)
+    std::atomic<long long> n_allgather{0}, n_broadcast{0}, n_allreduce{0};
 };
 
 struct slb_operator {

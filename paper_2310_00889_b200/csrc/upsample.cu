@@ -178,8 +178,10 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     }
     const size_t smem = smem_of(orows, gmats);
     SLB_REQUIRE(smem <= 227 * 1024, SLB_ERR_UNSUPPORTED, "upsample: grid too large for shared memory");
-    if (smem > 48 * 1024)
-        SLB_CUDA(cudaFuncSetAttribute(upsample_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) {
+        slb_status st_ = smem_optin((const void*)upsample_dmma_kernel);
+        if (st_ != SLB_OK) return st_;
+    }
     // one panel per CTA and pass; enough CTAs for every SM to hold several
     const unsigned grid = (unsigned)std::min<int64_t>(n_panels, (int64_t)num_sms() * 16);
     upsample_dmma_kernel<<<grid, kUpWarps * 32, smem, s>>>((int)kind, nc, n_panels, ip, sigma_coarse, sigma_fine, sc,

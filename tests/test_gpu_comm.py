@@ -1,57 +1,62 @@
-"""The NCCL path of slb_matvec on one GPU.
+"""The NCCL data plane of slb_matvec / slb_gmres, executed on one GPU.
 
-A one-rank communicator runs the same code as the multi-GPU operator: libslb dlopens NCCL,
-the 128-byte id travels through torch.distributed, slb_operator_create all-gathers the panel
-ranges and every apply runs the in-place ncclAllGather of the fine (and coarse) density.  With
-one rank the gather is an identity, so the result must equal the communicator-free operator
-bit for bit.  (Two ranks cannot share one GPU under NCCL; the multi-rank partition and layout
-are covered on CPU by test_multirank_gloo.py.)
+A one-rank communicator runs every collective the multi-GPU operator runs -- no `nranks == 1`
+short-circuit remains in libslb: the create-time ncclAllGather of the rank panel ranges, the two
+in-place ncclAllGathers per apply (fine source records, coarse density), the grouped in-place
+ncclBroadcasts that replace them for unequal shards (forced here with SLB_FORCE_GROUPED_GATHER=1),
+and the ncclAllReduce of the GMRES dot products.  With one rank each collective is an identity,
+so results must equal the communicator-free operator bit for bit.  Evidence that the calls really
+went through NCCL: libslb's own per-communicator call counts, and NCCL's INFO log of the
+collectives (NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=COLL), which names each AllGather / Broadcast /
+AllReduce.  (Two NCCL ranks cannot share one GPU; the multi-rank partition and layout arithmetic
+is covered on CPU by test_multirank_gloo.py.)
 """
+import json
 import os
-import socket
+import subprocess
+import sys
 
-import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("name,kw", [("c1", {}), ("c4", dict(n_loops=3, panels=6))])
-def test_single_rank_nccl_operator_matches_plain(name, kw):
+def _run(tmp_path, grouped):
+    log = tmp_path / f"nccl_{'grouped' if grouped else 'equal'}.%h.%p.log"
+    env = dict(os.environ, NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="COLL", NCCL_DEBUG_FILE=str(log),
+               SLB_FORCE_GROUPED_GATHER="1" if grouped else "0")
+    r = subprocess.run([sys.executable, os.path.join(HERE, "nccl_one_rank.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")][-1]
+    res = json.loads(line[len("RESULT "):])
+    text = "".join(p.read_text(errors="replace") for p in tmp_path.glob(f"nccl_{'grouped' if grouped else 'equal'}.*"))
+    return res, text
+
+
+@pytest.mark.parametrize("grouped", [False, True], ids=["allgather", "grouped_broadcast"])
+def test_one_rank_nccl_collectives_bitwise(tmp_path, grouped):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import torch.distributed as dist
-    from harness import DeviceProblem
-    from paper_2310_00889_b200 import Comm
-    from synth import make_config
-
-    pr = make_config(name, **kw)
-    plain = DeviceProblem(pr)
-    u0 = plain.matvec().clone()
-    plain.close()
-
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(_free_port())
-    dist.init_process_group("gloo", rank=0, world_size=1)
-    try:
-        comm = Comm(1, 0)
-        dp = DeviceProblem(pr, comm=comm)
-        u1 = dp.matvec().clone()
-        u2 = dp.matvec().clone()          # a second apply reuses the gathered buffers
-        torch.cuda.synchronize()
-        dp.close()
-        comm.close()
-    finally:
-        dist.destroy_process_group()
-    assert torch.equal(u0, u1)
-    assert torch.equal(u1, u2)
-    assert np.isfinite(u1.cpu().numpy()).all()
+    res, log = _run(tmp_path, grouped)
+    for name, r in res["cases"].items():
+        assert r["equal_first"] and r["equal_second"] and r["finite"], (name, r)
+        # create: the panel-range gather (always an AllGather)
+        assert r["create"]["allgather"] == 1, (name, r)
+        # two applies: fine records + coarse density per apply
+        if grouped:
+            assert r["two_applies"]["broadcast"] == 4 and r["two_applies"]["allgather"] == 0, (name, r)
+        else:
+            assert r["two_applies"]["allgather"] == 4 and r["two_applies"]["broadcast"] == 0, (name, r)
+        if "gmres" in r:
+            g = r["gmres"]
+            assert g["equal"], (name, g)
+            assert g["collectives"]["allreduce"] >= g["iters"][1] > 0, (name, g)
+    # NCCL's own log of the calls
+    assert "AllGather" in log, log[-2000:]
+    assert "AllReduce" in log, log[-2000:]
+    if grouped:
+        assert "Broadcast" in log, log[-2000:]

@@ -327,3 +327,23 @@ def test_zero_density_gives_zero(S):
     u = dp.matvec(cu(np.zeros_like(pr.sigma))).cpu().numpy()
     dp.close()
     assert np.all(u == 0.0)
+
+
+@pytest.mark.parametrize("nn", [12 * 32, 16 * 64])
+def test_nearcorr_apply_wide_stokes_blocks(S, nn):
+    """Wide Stokes blocks (12 x 32 and 16 x 64 panels: 27-74 KB per block) stream through the chunked
+    ring in the stand-alone slb_nearcorr_apply (they used to return UNSUPPORTED)."""
+    rng = np.random.default_rng(12)
+    T, P = 37, 5
+    cnt = rng.integers(0, 4, size=T)
+    row_ptr = np.zeros(T + 1, np.int64)
+    np.cumsum(cnt, out=row_ptr[1:])
+    pidx = np.concatenate([np.sort(rng.choice(P, c, replace=False)) for c in cnt]).astype(np.int32)
+    nnz = int(row_ptr[-1])
+    B = rng.standard_normal(nnz * 3 * nn * 3)
+    sig = rng.standard_normal(P * nn * 3)
+    u0 = rng.standard_normal(T * 3)
+    u = cu(u0)
+    S.slb_nearcorr_apply(cu(row_ptr, torch.int64), cu(pidx, torch.int32), cu(B), cu(sig), u, 3, 3, nn)
+    ref = O.nearcorr_apply(T, 3, 3, nn, row_ptr, pidx, B, sig, u0)
+    assert rel(u.cpu().numpy(), ref) <= TOL

@@ -252,6 +252,54 @@ def test_p10_bruteforce_adaptive_quadrature():
         assert abs(u[t] - tot) <= 1e-12 * max(1.0, abs(tot)), (t, u[t], tot)
 
 
+def test_p10s_bruteforce_adaptive_quadrature_stokes():
+    """P10 for the Stokes eta S + D far sum (R1 sign) with a NON-rigid band-limited 3-vector density,
+    against nested adaptive Gauss-Kronrod (scipy quad_vec) over the exact surface; every component of
+    S and D enters (a dropped rr^T term, a transposed D or a wrong eta placement fails)."""
+    from scipy.integrate import quad_vec
+    P, ns, nt = 4, 10, 16
+    eta = 0.8
+    b = torus_body(1.0, 0.25, (-0.1, 0.15, 0.05), random_rotation(np.random.default_rng(13)))
+    gc = discretize(b, P, ns, nt)
+    gf = discretize(b, P, 2 * ns, 2 * nt)
+    pc = [np.array([0.3, -1.0, 0.5, 0.25, -0.6, 0.1]), np.array([-0.7, 0.2, 0.9, -0.3, 0.05, 0.02]),
+          np.array([0.1, 0.4, -0.8, 0.6, -0.2, -0.04])]
+    tc = [(0.5, -0.3, 0.2), (-0.4, 0.6, 0.1), (0.25, 0.35, -0.45)]
+
+    def sig(s, th):
+        s, th = np.asarray(s), np.asarray(th)
+        return np.stack([np.polynomial.polynomial.polyval(s, pc[c]) *
+                         (1 + tc[c][0] * np.cos(th) + tc[c][1] * np.sin(2 * th) + tc[c][2] * np.cos(3 * th))
+                         for c in range(3)], -1)
+
+    sc = sig(gc.s, gc.th)
+    sf = O.upsample(sc.reshape(-1), P, ns, nt, 2 * ns, 2 * nt, 3)
+    X = np.array([[-0.1, 0.15, 0.05], [2.3, -0.5, 0.6]])
+    u = O.farfield(2, X, gf.y, gf.n, gf.w, sf, eta=np.full(gf.w.size, eta))
+    H = 1e-30
+
+    def integrand(s, th, x):
+        y = b.surface(np.array([s]), np.array([th]))[0]
+        ys = b.surface(np.array([s + 1j * H]), np.array([th + 0j]))[0].imag / H
+        yt = b.surface(np.array([s + 0j]), np.array([th + 1j * H]))[0].imag / H
+        cr = np.cross(yt, ys)
+        J = np.linalg.norm(cr)
+        nn = cr / J
+        r = x - y
+        rr = np.linalg.norm(r)
+        S = (np.eye(3) / rr + np.outer(r, r) / rr ** 3) / (8 * np.pi)          # Eq. e:stokes-sl, P:L538
+        D = 3.0 / FOUR_PI * (r @ nn) * np.outer(r, r) / rr ** 5                 # P:L551, sign R1
+        return (eta * S + D) @ sig(s, th) * J
+
+    for t in range(len(X)):
+        tot = np.zeros(3)
+        for k in range(P):
+            inner = lambda s: quad_vec(lambda th: integrand(s, th, X[t]), 0, 2 * np.pi,
+                                       epsabs=1e-15, epsrel=1e-14)[0]
+            tot += quad_vec(inner, k / P, (k + 1) / P, epsabs=1e-15, epsrel=1e-14)[0]
+        assert np.abs(u[t] - tot).max() <= 1e-12 * max(1.0, np.abs(tot).max()), (t, u[t], tot)
+
+
 # ---------------------------------------------------------------- P11 near apply == dense
 def test_p11_near_apply_equals_dense():
     pr = make_config("c1")
