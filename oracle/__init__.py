@@ -10,6 +10,8 @@ Parity status per function:
   or_gauss_legendre, or_lagrange_matrix, or_trig_matrix, or_upsample  -- pinned (P7, exactness)
   or_farfield (Laplace DL, Stokes eta S + D)                            -- pinned (P1-P6, P9, P10, P12)
   or_projector                                                          -- pinned (P13)
+  or_nearquad_block / or_nearquad (N1 special-quadrature blocks)       -- pinned (jump relations, Prop. 1,
+      S[n] = 0, Green's representation, Table t:conv-biest bound, identity term; test_oracle_pins "N1")
   or_apply_rows (full operator)                                         -- pinned via its parts + P11;
       the synthetic B-block VALUES are "parity unpinned" (no paper value exists).
 """
@@ -20,6 +22,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "slb_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "slb_quad_oracle.c")]
 _SO = os.path.join(_HERE, "libslb_oracle.so")
 _lib = None
 
@@ -27,8 +30,8 @@ CFLAGS = ["-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-fno-fast
 
 
 def build(force=False):
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, _SRC, "-lm"])
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(f) for f in _SRCS):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, *_SRCS, "-lm"])
     return _SO
 
 
@@ -71,6 +74,10 @@ def lib():
         L.or_apply_rows.argtypes = [ctypes.POINTER(OrProblem), P, P, P, ctypes.c_long, P, P, P, P]
         L.or_nearcorr_apply.argtypes = [ctypes.c_long, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         P, P, P, P, P]
+        L.or_nearquad_block.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P, ctypes.c_double,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_double, P]
+        L.or_nearquad.argtypes = [ctypes.c_int, ctypes.c_long, P, P, P, P, ctypes.c_int, ctypes.c_int, P, P,
+                                  ctypes.c_double, P]
         L.or_num_threads.restype = ctypes.c_int
         L.or_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -182,6 +189,33 @@ def nearcorr_apply(T, tdim, sdim, nodes_per_panel, row_ptr, panel_idx, blocks, s
     lib().or_nearcorr_apply(T, tdim, sdim, nodes_per_panel, _p(row_ptr), _p(panel_idx),
                             _p(blocks), _p(sigma_c), _p(u))
     return u
+
+
+def nearquad_block(kernel, x, y_panel, eta=0.0, node=None, tol=1e-13):
+    """(N1) Special-quadrature block of one element by nested adaptive Gauss-Kronrod (slb_quad_oracle.c).
+    kernel: slb_kernel id (1 Laplace D + eta S_L, 2 Stokes eta S + D, 3 Stokes eta S, 4 Laplace eta S_L);
+    y_panel [ns][nt][3]; node = (i0, j0) if x is that node of the element (singular), else None.
+    Returns B [tdim][ns*nt*sdim]."""
+    y = _c(y_panel)
+    ns, nt = y.shape[0], y.shape[1]
+    d = 3 if kernel in (2, 3) else 1
+    B = np.empty((d, ns * nt * d))
+    i0, j0 = node if node is not None else (-1, -1)
+    lib().or_nearquad_block(kernel, _p(_c(x)), ns, nt, _p(y), float(eta), int(i0), int(j0), float(tol), _p(B))
+    return B
+
+
+def nearquad(kernel, x_trg, row_ptr, panel_idx, ns, nt, y_coarse, trg_node=None, eta_panel=None, tol=1e-13):
+    """(N1) All CSR pairs, same arguments as slb_nearcorr_quad (uniform orders).  Returns blocks [nnz][tdim][cols]."""
+    x, rp, pi = _c(x_trg), _c(row_ptr, np.int64), _c(panel_idx, np.int32)
+    yc = _c(y_coarse)
+    tn = None if trg_node is None else _c(trg_node, np.int64)
+    ep = None if eta_panel is None else _c(eta_panel)
+    d = 3 if kernel in (2, 3) else 1
+    out = np.empty((int(rp[-1]), d, ns * nt * d))
+    lib().or_nearquad(kernel, x.shape[0], _p(x), _p(tn), _p(rp), _p(pi), ns, nt, _p(yc), _p(ep), float(tol),
+                      _p(out))
+    return out
 
 
 class Oracle:

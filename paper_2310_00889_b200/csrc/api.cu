@@ -49,14 +49,19 @@ int num_sms() {
 }
 
 unsigned long long* coincident_counter() {
-    static unsigned long long* const p = [] {
-        unsigned long long* q = nullptr;
-        if (cudaMalloc(&q, sizeof(unsigned long long)) != cudaSuccess) return (unsigned long long*)nullptr;
-        cudaMemset(q, 0, sizeof(unsigned long long));
-        cudaDeviceSynchronize();
-        return q;
-    }();
-    return p;
+    // allocated on first use outside any stream capture (slb_operator_create calls it before it
+    // captures); a failed attempt is not cached
+    static std::mutex mu;
+    static std::atomic<unsigned long long*> p{nullptr};
+    unsigned long long* v = p.load();
+    if (v) return v;
+    std::lock_guard<std::mutex> lk(mu);
+    if (p.load()) return p.load();
+    unsigned long long* q = nullptr;
+    if (cudaMalloc(&q, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaMemset(q, 0, sizeof(unsigned long long)) != cudaSuccess) { cudaFree(q); return nullptr; }
+    p.store(q);
+    return q;
 }
 
 // Opt a kernel in to the device's full dynamic shared memory once (the attribute is process-wide;
@@ -69,7 +74,9 @@ slb_status smem_optin(const void* fn) {
     int dev = 0, mx = 0;
     SLB_CUDA(cudaGetDevice(&dev));
     SLB_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    SLB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    cudaFuncAttributes fa;
+    SLB_CUDA(cudaFuncGetAttributes(&fa, fn));          // dynamic limit = opt-in maximum - static shared
+    SLB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes));
     done.insert(fn);
     return SLB_OK;
 }

@@ -50,6 +50,7 @@ constexpr int kMaxInterp = 3600;   // doubles: ms*ns + mt*nt
 struct InterpParams {
     int ns, nt, ms, mt;
     const double* vg;              // device copy when the matrices exceed kMaxInterp, else nullptr
+    const double* mats_d;          // device copy (P_s then F_th) whenever make_interp was given `owned`
     double v[kMaxInterp];          // P_s [ms][ns] followed by F [mt][nt]
 };
 // Fills ip.  If the matrices do not fit the parameter budget and `owned` is given, they are copied
@@ -197,7 +198,13 @@ slb_status pack_dyn(FarKind kind, int64_t M, const double* sc, const double* sig
 slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int ncomp,
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
                            double* dyn, cudaStream_t s, const int32_t* plist = nullptr,
-                           const int64_t* c_off = nullptr, const int64_t* f_off = nullptr);
+                           const int64_t* c_off = nullptr, const int64_t* f_off = nullptr,
+                           double* copy_out = nullptr);
+
+// true when upsample_launch takes the streaming warp-per-panel kernel for this grid (which can also
+// write the staged coarse density to copy_out, for any plist)
+bool upsample_streams(FarKind kind, const InterpParams& ip, int nc, bool records, const double* sigma_coarse,
+                      const double* sc);
 
 // ---- near (nearcorr.cu) ----
 slb_status near_apply_launch(int64_t n_trg, int tdim, int cols, const int64_t* row_ptr,

@@ -77,16 +77,19 @@ bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip, double** owne
     if (ns < 1 || ms < 1 || nt < 2 || mt < 2 || (nt & 1) || ns > 64 || ms > 64) return false;
     ip->ns = ns; ip->nt = nt; ip->ms = ms; ip->mt = mt;
     ip->vg = nullptr;
+    ip->mats_d = nullptr;
     double xs[64], ws[64], xf[64], wf[64];
     gl_nodes(ns, xs, ws);
     gl_nodes(ms, xf, wf);
     const int n = ms * ns + mt * nt;
-    if (n <= kMaxInterp) {
+    const bool fits = n <= kMaxInterp;
+    if (fits) {
         bary_matrix(ns, xs, ms, xf, ip->v);
         trig_matrix(nt, mt, ip->v + ms * ns);
-        return true;
     }
-    if (!owned) return false;
+    if (!owned) return fits;
+    // device copy (always, when the caller can own one): the streaming upsample stages the matrices
+    // from global memory; kernels that take them by value use it only when they exceed ip->v
     std::vector<double> h(n);
     bary_matrix(ns, xs, ms, xf, h.data());
     trig_matrix(nt, mt, h.data() + ms * ns);
@@ -97,7 +100,8 @@ bool make_interp(int ns, int nt, int ms, int mt, InterpParams* ip, double** owne
         return false;
     }
     *owned = d;
-    ip->vg = d;
+    ip->mats_d = d;
+    if (!fits) ip->vg = d;
     return true;
 }
 

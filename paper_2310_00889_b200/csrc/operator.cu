@@ -140,6 +140,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     SLB_REQUIRE(d->y_fine && d->n_fine && d->w_fine, SLB_ERR_INVALID_ARG, "null fine geometry");
     SLB_REQUIRE(d->n_trg_local == 0 || (d->x_trg && d->row_ptr), SLB_ERR_INVALID_ARG, "null targets/CSR");
     SLB_REQUIRE(check_sticky("slb_operator_create") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    SLB_REQUIRE(coincident_counter(), SLB_ERR_CUDA, "coincident counter allocation failed");   // before any capture
 
     slb_operator* op = new slb_operator;
     op->d = *d;
@@ -460,8 +461,14 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
     slb_status st;
     SLB_CUDA(cudaEventRecord(op->ev[0], s));
-    // local sigma' inside the global coarse buffer
+    // local sigma' inside the global coarse buffer.  One GPU without the projector: the caller's sigma IS
+    // sigma' and the finalize reads it in place (no copy).  With a communicator the upsample writes the
+    // staged density into the global buffer as it reads it (fused copy), the projector writes sigma' there.
     double* sig_p = op->coarse + (op->ragged ? op->cn0[d.panel_begin] * op->sdim : d.panel_begin * op->cols);
+    const double* up_src = sig_p;      // what the upsample reads
+    const double* near_sig = op->coarse;
+    const double* id_sig = sig_p;
+    double* copy_out = nullptr;
     const double* Lsig = nullptr;
     if (d.n_bodies_local > 0) {
         st = proj_launch(d.n_bodies_local, op->nb0, d.y_coarse, d.w_coarse, op->bodyc, sigma_local, op->coef, sig_p,
@@ -469,19 +476,38 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
         if (st != SLB_OK) return st;
         Lsig = op->Lsig;
     } else if (op->N_loc > 0) {
-        SLB_CUDA(cudaMemcpyAsync(sig_p, sigma_local, sizeof(double) * op->N_loc * op->sdim, cudaMemcpyDeviceToDevice, s));
+        up_src = sigma_local;
+        if (!op->comm) {
+            near_sig = sigma_local;
+            id_sig = sigma_local;
+        } else {
+            bool fused = true;
+            if (op->ragged) {
+                for (auto& b : op->buckets)
+                    if (b.n_loc && !upsample_streams(op->kind, b.ip, op->sdim, true, sigma_local, op->sc)) fused = false;
+            } else {
+                fused = upsample_streams(op->kind, op->ip, op->sdim, true, sigma_local, op->sc);
+            }
+            if (fused) {
+                copy_out = sig_p;
+            } else {
+                SLB_CUDA(cudaMemcpyAsync(sig_p, sigma_local, sizeof(double) * op->N_loc * op->sdim,
+                                         cudaMemcpyDeviceToDevice, s));
+                up_src = sig_p;
+            }
+        }
     }
     if (op->ragged) {
         double* dyn_loc = op->dyn + op->fn0[d.panel_begin] * 4;
         for (auto& b : op->buckets) {
             if (!b.n_loc) continue;
-            st = upsample_launch(op->kind, b.n_loc, b.ip, op->sdim, sig_p, nullptr, op->sc, dyn_loc, s, b.plist_d,
-                                 op->lc0_d, op->lf0_d);
+            st = upsample_launch(op->kind, b.n_loc, b.ip, op->sdim, up_src, nullptr, op->sc, dyn_loc, s, b.plist_d,
+                                 op->lc0_d, op->lf0_d, copy_out);
             if (st != SLB_OK) return st;
         }
     } else {
-        st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, sig_p, nullptr, op->sc,
-                             op->dyn + d.panel_begin * op->Mn * 4, s);
+        st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, up_src, nullptr, op->sc,
+                             op->dyn + d.panel_begin * op->Mn * 4, s, nullptr, nullptr, nullptr, copy_out);
         if (st != SLB_OK) return st;
     }
     SLB_CUDA(cudaEventRecord(op->ev[1], s));
@@ -521,7 +547,7 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
         rag.bmeta = op->bmeta_d;
     }
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
-                         d.blocks, op->coarse, d.n_on_local, d.c_identity, sig_p, Lsig, u_local, op->near_G, s, rag);
+                         d.blocks, near_sig, d.n_on_local, d.c_identity, id_sig, Lsig, u_local, op->near_G, s, rag);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[4], s));
     op->timed = true;

@@ -12,6 +12,7 @@
 // for Stokes, w sigma_f n/(4 pi) for Laplace), so sigma_f never round-trips through HBM.
 // HBM-bound (AI ~3.4 flop/B separable); << 1% of the apply.
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace slb {
@@ -155,11 +156,230 @@ upsample_dmma_kernel(int kind, int nc, int64_t n_panels, const __grid_constant__
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// upsample_warp_kernel: the streaming form (round 2).  One WARP per panel, no CTA barriers in the
+// panel loop; each warp double-buffers its panels: lane 0 issues TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx) of the NEXT panel's coarse density and fine-node scales while the warp
+// contracts the current one, so HBM latency is hidden behind the DMMA work.
+//   step 1 (rows (i,c) stacked):  T1_c[i][b] = sum_j sigma[i][j][c] F[b][j]     M = N_s nc, K = N_th, N = M_th
+//   step 2 (per c, shared A):     O_c[a][b]  = sum_i P_s[a][i] T1_c[i][b]        M = M_s,   K = N_s,  N = M_th
+// Step 2 keeps the nc components of one output tile in registers, so a lane holds ALL components of
+// two adjacent fine nodes (a0+g, b0+2tq..+1) and writes their 32-byte source records straight from
+// the accumulators (8 rows x 256 contiguous bytes per warp store) -- no output staging in shared
+// memory.  Optionally the staged coarse density is also written to `copy_out` (the global coarse
+// buffer of a sharded operator), fusing the copy into the read.  P_s and F_th are staged per CTA
+// from a global copy (coalesced), never from the kernel-parameter bank.
+constexpr int kUpW = 8;   // warps per CTA (upper bound; fewer when the per-warp buffers are large)
+
+struct UpWarpLayout {
+    int nsp, ntp, msp, mtp, rows8, ldp, ldf, ldt;
+    int nin2, nout, scl;       // doubles: coarse panel (even), fine nodes, scale doubles per node
+    size_t cta_d, warp_d;      // doubles: per-CTA matrices, per-warp buffers
+};
+
+__host__ __device__ inline UpWarpLayout up_layout(int ns, int nt, int ms, int mt, int nc, int scl) {
+    UpWarpLayout L;
+    L.nsp = (ns + 3) / 4 * 4;
+    L.ntp = (nt + 3) / 4 * 4;
+    L.msp = (ms + 7) / 8 * 8;
+    L.mtp = (mt + 7) / 8 * 8;
+    L.rows8 = (ns * nc + 7) / 8 * 8;
+    L.ldp = ld_g(L.nsp);
+    L.ldf = ld_g(L.ntp);
+    L.ldt = ld_t(L.mtp);
+    L.nin2 = (ns * nt * nc + 1) & ~1;
+    L.nout = ms * mt;
+    L.scl = scl;
+    L.cta_d = (size_t)L.msp * L.ldp + (size_t)L.mtp * L.ldf;
+    // raw[2][nin2] + scale[2][nout*scl] + T1[nc][nsp][ldt]
+    L.warp_d = 2 * (size_t)L.nin2 + 2 * (size_t)L.nout * scl + (size_t)nc * L.nsp * L.ldt;
+    return L;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kUpW * 32)
+upsample_warp_kernel(int kind, int64_t n_panels, int ns, int nt, int ms, int mt, const double* __restrict__ mats,
+                     const double* __restrict__ sc_in, double* __restrict__ sf_out,
+                     const double* __restrict__ scale, double* __restrict__ dyn, double* __restrict__ copy_out,
+                     const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
+                     const int64_t* __restrict__ f_off) {
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[kUpW * 2];
+    const int scl = scale ? (far_scalar(kind) ? 4 : 1) : 0;
+    const UpWarpLayout L = up_layout(ns, nt, ms, mt, NC, scl);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double* Ps = sm;                                   // [msp][ldp]
+    double* F = Ps + L.msp * L.ldp;                    // [mtp][ldf]
+    double* wb = sm + L.cta_d + (size_t)warp * L.warp_d;
+    double* raw = wb;                                  // [2][nin2]
+    double* scs = raw + 2 * L.nin2;                    // [2][nout*scl]
+    double* T1 = scs + 2 * (size_t)L.nout * scl;       // [NC][nsp][ldt]
+    uint64_t* bar = bars + 2 * warp;
+    for (int q = threadIdx.x; q < L.msp * L.ldp; q += blockDim.x) {
+        const int a = q / L.ldp, i = q % L.ldp;
+        Ps[q] = (a < ms && i < ns) ? mats[a * ns + i] : 0.0;
+    }
+    for (int q = threadIdx.x; q < L.mtp * L.ldf; q += blockDim.x) {
+        const int b = q / L.ldf, j = q % L.ldf;
+        F[q] = (b < mt && j < nt) ? mats[ms * ns + b * nt + j] : 0.0;
+    }
+    for (int q = lane; q < NC * L.nsp * L.ldt; q += 32) T1[q] = 0.0;   // K padding rows stay zero
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int nin = ns * nt * NC;
+    const int64_t gw = (int64_t)blockIdx.x * nw + warp, stride = (int64_t)gridDim.x * nw;
+    auto issue = [&](int64_t pl, int buf) {            // lane 0: TMA the panel's inputs into buffer buf
+        const int64_t p = plist ? (int64_t)plist[pl] : pl;
+        const int64_t m0 = f_off ? f_off[p] : p * (int64_t)L.nout;
+        const double* src = sc_in + (c_off ? c_off[p] * NC : p * (int64_t)nin);
+        const uint32_t b0 = (uint32_t)(nin * 8), b1 = (uint32_t)(L.nout * scl * 8);
+        mbar_expect_tx(&bar[buf], b0 + b1);
+        bulk_g2s(raw + buf * L.nin2, src, b0, &bar[buf]);
+        if (scl) bulk_g2s(scs + (size_t)buf * L.nout * scl, scale + m0 * scl, b1, &bar[buf]);
+    };
+    if (lane == 0 && gw < n_panels) issue(gw, 0);
+    const int g = lane >> 2, tq = lane & 3;
+    const int rows = ns * NC;
+    int it = 0;
+    for (int64_t pl = gw; pl < n_panels; pl += stride, ++it) {
+        const int buf = it & 1;
+        const int64_t p = plist ? (int64_t)plist[pl] : pl;
+        const int64_t m0 = f_off ? f_off[p] : p * (int64_t)L.nout;
+        mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
+        // the other buffer was consumed by the previous iteration (its last reads are ordered before
+        // this __syncwarp): refill it with the next panel
+        __syncwarp();
+        if (lane == 0 && pl + stride < n_panels) {
+            fence_proxy_async_smem();
+            issue(pl + stride, buf ^ 1);
+        }
+        const double* R = raw + buf * L.nin2;
+        const double* SC = scs + (size_t)buf * L.nout * scl;
+        if (copy_out) {
+            double* dst = copy_out + (c_off ? c_off[p] * NC : p * (int64_t)nin);
+            for (int q = lane; q < nin; q += 32) dst[q] = R[q];
+        }
+        // step 1: T1_c[i][b], rows r = i*NC + c
+        for (int r0 = 0; r0 < L.rows8; r0 += 8) {
+            const int r = r0 + g;
+            const int rb = (r < rows) ? (r / NC) * nt * NC + (r % NC) : -1;
+            for (int n0 = 0; n0 < L.mtp; n0 += 8) {
+                double d0 = 0.0, d1 = 0.0;
+                for (int k0 = 0; k0 < L.ntp; k0 += 4) {
+                    const int j = k0 + tq;
+                    const double av = (rb >= 0 && j < nt) ? R[rb + j * NC] : 0.0;
+                    dmma_8x8x4(d0, d1, av, F[(n0 + g) * L.ldf + k0 + tq]);
+                }
+                if (r < rows) {
+                    double* T = T1 + ((r % NC) * L.nsp + r / NC) * L.ldt + n0 + 2 * tq;
+                    T[0] = d0;
+                    T[1] = d1;
+                }
+            }
+        }
+        __syncwarp();
+        // step 2 + epilogue
+        for (int a0 = 0; a0 < L.msp; a0 += 8) {
+            for (int n0 = 0; n0 < L.mtp; n0 += 8) {
+                double d0[NC], d1[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) d0[c] = d1[c] = 0.0;
+                for (int k0 = 0; k0 < L.nsp; k0 += 4) {
+                    const double av = Ps[(a0 + g) * L.ldp + k0 + tq];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        dmma_8x8x4(d0[c], d1[c], av, T1[(c * L.nsp + k0 + tq) * L.ldt + n0 + g]);
+                }
+                const int a = a0 + g, b = n0 + 2 * tq;
+                if (a >= ms || b >= mt) continue;
+                const int e = a * mt + b;                  // node e and e + 1 (b + 1 < mt: mt even)
+                const int64_t m = m0 + e;
+                if (dyn) {
+                    double2* D2 = reinterpret_cast<double2*>(dyn) + 2 * m;
+                    if (NC == 1) {
+                        const double* s0 = SC + 4 * e;
+                        D2[0] = make_double2(s0[0] * d0[0], s0[1] * d0[0]);
+                        D2[1] = make_double2(s0[2] * d0[0], s0[3] * d0[0]);
+                        D2[2] = make_double2(s0[4] * d1[0], s0[5] * d1[0]);
+                        D2[3] = make_double2(s0[6] * d1[0], s0[7] * d1[0]);
+                    } else {
+                        const double s0 = SC[e], s1 = SC[e + 1];
+                        D2[0] = make_double2(s0 * d0[0], s0 * d0[1]);
+                        D2[1] = make_double2(s0 * d0[NC - 1], 0.0);
+                        D2[2] = make_double2(s1 * d1[0], s1 * d1[1]);
+                        D2[3] = make_double2(s1 * d1[NC - 1], 0.0);
+                    }
+                } else {
+                    double* o = sf_out + m * NC;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        o[c] = d0[c];
+                        o[NC + c] = d1[c];
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Per-warp buffers of the streaming kernel (doubles), or 0 when it does not apply (large grids).
+static size_t up_warp_bytes(const InterpParams& ip, int nc, bool scaled, bool scalar, int* warps) {
+    const UpWarpLayout L = up_layout(ip.ns, ip.nt, ip.ms, ip.mt, nc, scaled ? (scalar ? 4 : 1) : 0);
+    const size_t cta = L.cta_d * 8, wb = L.warp_d * 8;
+    int w = kUpW;
+    while (w > 1 && cta + w * wb > 200 * 1024) --w;
+    if (cta + w * wb > 200 * 1024 || w < 4) return 0;
+    *warps = w;
+    return cta + w * wb;
+}
+
+static bool upsample_legacy() {
+    static const bool v = [] { const char* e = getenv("SLB_UPSAMPLE_LEGACY"); return e && e[0] == '1'; }();
+    return v;
+}
+
+bool upsample_streams(FarKind kind, const InterpParams& ip, int nc, bool records, const double* sigma_coarse,
+                      const double* sc) {
+    int warps = 0;
+    const bool aligned = ((uintptr_t)sigma_coarse % 16 == 0) && (!sc || (uintptr_t)sc % 16 == 0);
+    return !upsample_legacy() && ip.mats_d && aligned && up_warp_bytes(ip, nc, records, far_scalar(kind), &warps) > 0;
+}
+
 slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int nc,
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
                            double* dyn, cudaStream_t s, const int32_t* plist, const int64_t* c_off,
-                           const int64_t* f_off) {
+                           const int64_t* f_off, double* copy_out) {
     if (n_panels <= 0) return SLB_OK;
+    int warps = 0;
+    const size_t wsm = up_warp_bytes(ip, nc, dyn != nullptr, far_scalar(kind), &warps);
+    if (upsample_streams(kind, ip, nc, dyn != nullptr, sigma_coarse, sc)) {
+        { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<1>); if (st_ != SLB_OK) return st_; }
+        { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<3>); if (st_ != SLB_OK) return st_; }
+        // a warp per panel up to the resident limit; beyond it the warps loop (and prefetch)
+        const unsigned grid = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((n_panels + warps - 1) / warps, (int64_t)num_sms() * (200 * 1024 / wsm)));
+        if (nc == 1)
+            upsample_warp_kernel<1><<<grid, warps * 32, wsm, s>>>((int)kind, n_panels, ip.ns, ip.nt, ip.ms, ip.mt,
+                                                                  ip.mats_d, sigma_coarse, sigma_fine, sc, dyn,
+                                                                  copy_out, plist, c_off, f_off);
+        else
+            upsample_warp_kernel<3><<<grid, warps * 32, wsm, s>>>((int)kind, n_panels, ip.ns, ip.nt, ip.ms, ip.mt,
+                                                                  ip.mats_d, sigma_coarse, sigma_fine, sc, dyn,
+                                                                  copy_out, plist, c_off, f_off);
+        ++g_launch_count;
+        return check_launch("upsample_warp_kernel");
+    }
+    if (copy_out) {
+        // legacy kernel: separate copy of the coarse density (contiguous for uniform panels / plist == NULL)
+        SLB_REQUIRE(!plist, SLB_ERR_UNSUPPORTED, "fused coarse copy needs the streaming upsample");
+        const int64_t nin = (int64_t)ip.ns * ip.nt * nc;
+        SLB_CUDA(cudaMemcpyAsync(copy_out, sigma_coarse, sizeof(double) * nin * n_panels, cudaMemcpyDeviceToDevice, s));
+    }
     auto rup_h = [](int v, int m) { return (v + m - 1) / m * m; };
     const int nsp = rup_h(ip.ns, 4), ntp = rup_h(ip.nt, 4), msp = rup_h(ip.ms, 8), mtp = rup_h(ip.mt, 8);
     const int ncol2p = rup_h(ip.mt * nc, 8);
