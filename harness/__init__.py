@@ -83,7 +83,7 @@ class DeviceProblem:
             pi_d = torch.from_numpy(np.ascontiguousarray(pidx, dtype=np.int32)).to(dev)
             qk = (3 if pr.kernel == 2 else 4) if single_layer else pr.kernel
             slb_nearcorr_quad(qk, self.x_trg, rp_d, pi_d, pr.Ns, pr.Nt, f64(pr.y_c),
-                              self.blocks, trg_node=trg_node, eta_panel=None if single_layer else eta_panel, order=quad.get("order", 12),
+                              self.blocks, trg_node=trg_node, eta_panel=None if single_layer else eta_panel, order=quad.get("order", 0),
                               beta=quad.get("beta", 0.6), panel_nt=pr.nt_of_panel() if pr.ragged else None,
                               panel_ns=pr.ns_of_panel() if pr.ragged else None)
         self.y_f, self.n_f, self.w_f = f64(pr.y_f), f64(pr.n_f), f64(pr.w_f)

@@ -71,76 +71,106 @@ static void qpanel_init(qpanel* P, int ns, int nt, const double* yc) {
         }
 }
 
-/* Lagrange basis and derivative, direct product formulas */
-static void lagrange(const qpanel* P, double t, double* l, double* dl) {
+/* Lagrange basis and derivative, direct product formulas.  Evaluated in long double: the geometry built
+ * from them feeds (r.n) = O(|r|^2) of the double layer near the surface, whose absolute accuracy the
+ * pins and the parity tests need beyond what eps-level basis values give. */
+typedef long double qreal;
+
+static void lagrange_ld(const qpanel* P, qreal t, qreal* l, qreal* dl) {
     int n = P->ns;
     for (int i = 0; i < n; ++i) {
-        double p = 1.0;
+        qreal p = 1.0L;
         for (int k = 0; k < n; ++k)
-            if (k != i) p *= (t - P->tg[k]) / (P->tg[i] - P->tg[k]);
+            if (k != i) p *= (t - (qreal)P->tg[k]) / ((qreal)P->tg[i] - (qreal)P->tg[k]);
         l[i] = p;
-        double d = 0.0;
+        qreal d = 0.0L;
         for (int m = 0; m < n; ++m) {
             if (m == i) continue;
-            double q = 1.0 / (P->tg[i] - P->tg[m]);
+            qreal q = 1.0L / ((qreal)P->tg[i] - (qreal)P->tg[m]);
             for (int k = 0; k < n; ++k)
-                if (k != i && k != m) q *= (t - P->tg[k]) / (P->tg[i] - P->tg[k]);
+                if (k != i && k != m) q *= (t - (qreal)P->tg[k]) / ((qreal)P->tg[i] - (qreal)P->tg[k]);
             d += q;
         }
         dl[i] = d;
     }
 }
 
-/* trig cardinal functions C_j(th) and C_j'(th) from the Fourier-sum definition (R3):
- * cos l(th - th_j) = cos(l th) cos(l th_j) + sin(l th) sin(l th_j) */
-static void cardinal(const qpanel* P, double th, double* C, double* dC) {
+static void lagrange(const qpanel* P, double t, double* l, double* dl) {
+    qreal L[Q_MAXN], D[Q_MAXN];
+    lagrange_ld(P, t, L, D);
+    for (int i = 0; i < P->ns; ++i) { l[i] = (double)L[i]; dl[i] = (double)D[i]; }
+}
+
+/* trig cardinal functions C_j(th) and C_j'(th) from the Fourier-sum definition (R3), long double:
+ * cos l(th - th_j), sin l(th - th_j) evaluated directly at the difference */
+static void cardinal_ld(const qpanel* P, qreal th, qreal* C, qreal* dC) {
     int N = P->nt;
-    double cl[Q_MAXN / 2 + 1], sl[Q_MAXN / 2 + 1];
-    for (int l = 0; l <= N / 2; ++l) {
-        cl[l] = cos(l * th);
-        sl[l] = sin(l * th);
-    }
     for (int j = 0; j < N; ++j) {
-        double v = 1.0, d = 0.0;
-        for (int l = 1; l < N / 2; ++l) {
-            double c = cl[l] * P->ec[l][j] + sl[l] * P->es[l][j];     /* cos l(th - th_j) */
-            double s = sl[l] * P->ec[l][j] - cl[l] * P->es[l][j];     /* sin l(th - th_j) */
-            v += 2.0 * c;
-            d -= 2.0 * l * s;
+        qreal phi = th - 2.0L * 3.141592653589793238462643383279502884L * j / N;
+        qreal c1 = cosl(phi), s1 = sinl(phi), cl = 1.0L, sl = 0.0L;
+        qreal v = 1.0L, d = 0.0L;
+        for (int l = 1; l < N / 2; ++l) {          /* cos, sin of l phi by the angle-addition recurrence */
+            qreal cn = cl * c1 - sl * s1;
+            sl = sl * c1 + cl * s1;
+            cl = cn;
+            v += 2.0L * cl;
+            d -= 2.0L * l * sl;
         }
-        int h = N / 2;
-        double c = cl[h] * P->ec[h][j] + sl[h] * P->es[h][j];
-        double s = sl[h] * P->ec[h][j] - cl[h] * P->es[h][j];
-        v += c;
-        d -= h * s;
+        v += cosl(0.5L * N * phi);
+        d -= 0.5L * N * sinl(0.5L * N * phi);
         C[j] = v / N;
         dC[j] = d / N;
     }
 }
 
+static void cardinal(const qpanel* P, double th, double* C, double* dC) {
+    qreal c[Q_MAXN], d[Q_MAXN];
+    cardinal_ld(P, th, c, d);
+    for (int j = 0; j < P->nt; ++j) { C[j] = (double)c[j]; dC[j] = (double)d[j]; }
+}
+
 typedef struct {
     double l[Q_MAXN], dl[Q_MAXN], C[Q_MAXN], dC[Q_MAXN];
     double y[3], yt[3], yh[3], n[3], J;
+    double rel[3];                /* y - xref (eval_point_x), long-double accumulated */
 } qpoint;
 
-static void eval_point(const qpanel* P, double t, double th, qpoint* q) {
-    lagrange(P, t, q->l, q->dl);
-    cardinal(P, th, q->C, q->dC);
-    for (int a = 0; a < 3; ++a) { q->y[a] = 0.0; q->yt[a] = 0.0; q->yh[a] = 0.0; }
+/* Surface point and tangents.  xref: evaluate them from the node positions relative to xref (y_ij - xref;
+ * the interpolant reproduces constants, so y - xref, y_t, y_th are the same functions), which keeps their
+ * rounding error at eps |y_ij - xref| ~ eps L instead of eps |y| -- the normal of a near-singular
+ * double-layer integrand enters through (r.n) = O(|r|^2) and needs that.  xref = NULL: absolute. */
+static void eval_point_x(const qpanel* P, const double* xref, double t, double th, qpoint* q) {
+    qreal L[Q_MAXN], DL[Q_MAXN], C[Q_MAXN], DC[Q_MAXN];
+    lagrange_ld(P, t, L, DL);
+    cardinal_ld(P, th, C, DC);
+    const double z[3] = {0.0, 0.0, 0.0};
+    const double* o = xref ? xref : z;
+    qreal y[3] = {0, 0, 0}, yt[3] = {0, 0, 0}, yh[3] = {0, 0, 0};
     for (int i = 0; i < P->ns; ++i)
         for (int j = 0; j < P->nt; ++j) {
             const double* v = P->yc + 3 * (i * P->nt + j);
             for (int a = 0; a < 3; ++a) {
-                q->y[a] += v[a] * q->l[i] * q->C[j];
-                q->yt[a] += v[a] * q->dl[i] * q->C[j];
-                q->yh[a] += v[a] * q->l[i] * q->dC[j];
+                const qreal dv = (qreal)v[a] - (qreal)o[a];
+                y[a] += dv * L[i] * C[j];
+                yt[a] += dv * DL[i] * C[j];
+                yh[a] += dv * L[i] * DC[j];
             }
         }
-    double c[3] = {q->yh[1] * q->yt[2] - q->yh[2] * q->yt[1], q->yh[2] * q->yt[0] - q->yh[0] * q->yt[2],
-                   q->yh[0] * q->yt[1] - q->yh[1] * q->yt[0]};
-    q->J = sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-    for (int a = 0; a < 3; ++a) q->n[a] = c[a] / q->J;
+    for (int i = 0; i < P->ns; ++i) { q->l[i] = (double)L[i]; q->dl[i] = (double)DL[i]; }
+    for (int j = 0; j < P->nt; ++j) { q->C[j] = (double)C[j]; q->dC[j] = (double)DC[j]; }
+    for (int a = 0; a < 3; ++a) {
+        q->y[a] = (double)(y[a] + (qreal)o[a]);
+        q->yt[a] = (double)yt[a];
+        q->yh[a] = (double)yh[a];
+        q->rel[a] = (double)y[a];                 /* y - xref */
+    }
+    qreal c[3] = {yh[1] * yt[2] - yh[2] * yt[1], yh[2] * yt[0] - yh[0] * yt[2], yh[0] * yt[1] - yh[1] * yt[0]};
+    qreal J = sqrtl(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    q->J = (double)J;
+    for (int a = 0; a < 3; ++a) q->n[a] = (double)(c[a] / J);
 }
+
+static void eval_point(const qpanel* P, double t, double th, qpoint* q) { eval_point_x(P, NULL, t, th, q); }
 
 /* ------------------------------------------------------------------ */
 /* kernels by slb_kernel id: 1 Laplace D (+ eta S_L), 2 Stokes eta S + D, 3 Stokes S, 4 Laplace S_L */
@@ -174,8 +204,8 @@ static const double WG[4] = {0.129484966168869693270611432679082, 0.279705391489
 typedef void (*qfun)(void* ctx, double x, double* out);
 
 /* one GK15 panel: res = K15 (nv values); returns the QUADPACK-style error estimate
- * E min(1, (200 E / A)^1.5), E = max_c |K15_c - G7_c|, A = max_c h sum_k wk |f_c(x_k)|;
- * *abs_out = A. */
+ * max_c E_c min(1, (200 E_c / A_c)^1.5), E_c = |K15_c - G7_c|, A_c = h sum_k wk |f_c(x_k)|;
+ * *abs_out = max_c A_c. */
 static double gk15(qfun f, void* ctx, int nv, double a, double b, double* res, double* tmp, double* abs_out) {
     double c = 0.5 * (a + b), h = 0.5 * (b - a);
     double* g = tmp + nv;
@@ -193,26 +223,30 @@ static double gk15(qfun f, void* ctx, int nv, double a, double b, double* res, d
             }
         }
     }
+    /* the QUADPACK heuristic E min(1, (200 E / A)^1.5) per component (E, A of the same component),
+     * then the maximum over components */
     double e = 0.0, A = 0.0;
     for (int v = 0; v < nv; ++v) {
         res[v] *= h;
         g[v] *= h;
         double d = fabs(res[v] - g[v]);
+        double av = fabs(h) * ab[v];
+        if (av > 0.0 && d > 0.0) {
+            double q = pow(200.0 * d / av, 1.5);
+            if (q < 1.0) d *= q;
+        }
+        d -= 50.0 * 2.2e-16 * av;          /* what remains above this component's rounding floor */
         if (d > e) e = d;
-        if (fabs(h) * ab[v] > A) A = fabs(h) * ab[v];
+        if (av > A) A = av;
     }
     *abs_out = A;
-    if (A > 0.0 && e > 0.0) {
-        double q = pow(200.0 * e / A, 1.5);
-        if (q < 1.0) e *= q;
-    }
     return e;
 }
 
 /* Global adaptive integration (QUADPACK qag strategy) of f over [bp[0], bp[nb]] starting from
  * the panels of bp: bisect the panel with the largest error estimate until the summed estimate
- * is <= tol * S (S = max_c integral of |f_c| over the initial panels), or the panel's estimate
- * is at the rounding floor (50 eps A), or 4000 panels.  The result is summed in panel order
+ * is <= tol * S (S = max_c |integral_c| estimated on the initial panels), a panel's estimate being
+ * what is left above each component's rounding floor (50 eps int |f_c|), or 4000 panels.  The result is summed in panel order
  * (deterministic).  out[nv] written. */
 typedef struct { double a, b, err, A; int live; } qpan;
 
@@ -222,28 +256,34 @@ static void adapt(qfun f, void* ctx, int nv, const double* bp, int nb, double to
     double* R = (double*)malloc(sizeof(double) * (size_t)nv * cap);     /* per-panel results */
     double* tmp = (double*)malloc(sizeof(double) * nv * 3);
     int np = 0;
-    double S = 0.0, E = 0.0;
+    double E = 0.0;
+    double* net = (double*)calloc((size_t)nv, sizeof(double));
     for (int q = 0; q < nb && np < cap; ++q) {
         if (!(bp[q + 1] > bp[q])) continue;
         pan[np].a = bp[q];
         pan[np].b = bp[q + 1];
         pan[np].err = gk15(f, ctx, nv, bp[q], bp[q + 1], R + (size_t)np * nv, tmp, &pan[np].A);
         pan[np].live = 1;
-        S += pan[np].A;
-        E += pan[np].err;
+        for (int v = 0; v < nv; ++v) net[v] += R[(size_t)np * nv + v];
+        if (pan[np].err > 0.0) E += pan[np].err;
         ++np;
     }
+    /* scale: the largest |integral| (max-norm of the result), not the integral of |f| */
+    double S = 0.0;
+    for (int v = 0; v < nv; ++v) if (fabs(net[v]) > S) S = fabs(net[v]);
+    free(net);
+    if (S == 0.0) S = 1e-300;
     while (E > tol * S && np < cap) {
         int w = -1;
         for (int q = 0; q < np; ++q)
             if (pan[q].live && (w < 0 || pan[q].err > pan[w].err)) w = q;
         if (w < 0) break;
-        if (pan[w].err <= 50.0 * 2.2e-16 * pan[w].A || (pan[w].b - pan[w].a) < 1e-15 * (bp[nb] - bp[0])) {
+        if (pan[w].err <= 0.0 || (pan[w].b - pan[w].a) < 1e-15 * (bp[nb] - bp[0])) {
             pan[w].live = 0;             /* at the rounding floor: keep it, stop refining it */
             continue;
         }
         double a = pan[w].a, b = pan[w].b, m = 0.5 * (a + b);
-        E -= pan[w].err;
+        E -= fmax(pan[w].err, 0.0);
         /* left half replaces w, right half appended; order restored by sorting on a at the end */
         pan[w].b = m;
         pan[w].err = gk15(f, ctx, nv, a, m, R + (size_t)w * nv, tmp, &pan[w].A);
@@ -251,7 +291,7 @@ static void adapt(qfun f, void* ctx, int nv, const double* bp, int nb, double to
         pan[np].b = b;
         pan[np].live = 1;
         pan[np].err = gk15(f, ctx, nv, m, b, R + (size_t)np * nv, tmp, &pan[np].A);
-        E += pan[w].err + pan[np].err;
+        E += fmax(pan[w].err, 0.0) + fmax(pan[np].err, 0.0);
         ++np;
     }
     /* sum in ascending a (deterministic order independent of the refinement history) */
@@ -309,8 +349,9 @@ typedef struct {
 static void f_inner(void* vc, double th, double* out) {
     qctx* c = (qctx*)vc;
     qpoint q;
-    eval_point(c->P, c->t_cur, th, &q);
-    double r[3] = {c->x[0] - q.y[0], c->x[1] - q.y[1], c->x[2] - q.y[2]};
+    eval_point_x(c->P, c->x, c->t_cur, th, &q);
+    /* r = x - y from the node positions relative to x, accumulated in long double */
+    double r[3] = {-q.rel[0], -q.rel[1], -q.rel[2]};
     double K[9];
     kernel_eval(c->kernel, r, q.n, c->eta, K);
     int d = c->d, N = c->P->nt;
@@ -383,7 +424,7 @@ static void f_duffy_inner(void* vc, double v, double* out) {
     double dh = c->tri == 0 ? c->B * u * v : c->B * u;
     double t = c->t0 + dt, th = c->th0 + dh;
     qpoint q;
-    eval_point(c->P, t, th, &q);
+    eval_point_x(c->P, c->x, t, th, &q);
     double r[3];
     r_singular(c, dt, dh, q.C, r);
     double K[9];

@@ -23,7 +23,8 @@ def sources():
 
 
 def _headers():
-    return glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "slb.h")]
+    return (glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG, "csrc", "*.inc")) +
+            [os.path.join(ROOT, "include", "slb.h")])
 
 
 def _obj(src):

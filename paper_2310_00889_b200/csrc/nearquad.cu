@@ -963,6 +963,14 @@ nearquad_kernel(int kind, int64_t T, const double* __restrict__ x_trg, const int
 
 using namespace slb;
 
+namespace slb {
+slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_trg, const int64_t* trg_node,
+                              const int64_t* row_ptr, const int32_t* panel_idx, int ns_max, int nt_max,
+                              const double* y_coarse, const double* eta_panel, double* blocks, cudaStream_t s,
+                              const int32_t* pnt, const int64_t* cn0, const int64_t* boff, const int32_t* pns,
+                              int ns_uniform, int nt_uniform);
+}
+
 // One launch per panel size class (ragged panels: the shared-memory layout is sized by the class's
 // largest panel, so small panels keep several CTAs per SM -- c3v's 16 x 64 gap panels would otherwise
 // force one CTA per SM on every target).  classes: (ns_max, nt_max) per class; pclass [P] or NULL.
@@ -1097,7 +1105,8 @@ static slb_status nearquad_check(slb_kernel kernel, int64_t n_trg, int ns, int o
                 SLB_ERR_INVALID_ARG, "bad kernel");
     SLB_REQUIRE(n_trg >= 0 && ns >= 2, SLB_ERR_INVALID_ARG, "bad sizes");
     SLB_REQUIRE(ns <= kMaxNsQ, SLB_ERR_UNSUPPORTED, "panel grid too large for nearquad");
-    SLB_REQUIRE(order >= 4 && order <= kMaxQ && beta > 0.0, SLB_ERR_INVALID_ARG, "need 4 <= order <= 24, beta > 0");
+    SLB_REQUIRE(order == 0 || (order >= 4 && order <= kMaxQ && beta > 0.0), SLB_ERR_INVALID_ARG,
+                "need order 0 (the paper's rule) or 4 <= order <= 24 with beta > 0");
     SLB_REQUIRE(n_trg <= 2147483647LL, SLB_ERR_UNSUPPORTED, "too many targets");
     return SLB_OK;
 }
@@ -1113,6 +1122,9 @@ extern "C" slb_status slb_nearcorr_quad(slb_kernel kernel, int64_t n_trg, const 
     if (n_trg == 0) return SLB_OK;
     SLB_REQUIRE(x_trg && row_ptr && panel_idx && y_coarse && blocks, SLB_ERR_INVALID_ARG, "null pointer");
     SLB_REQUIRE(kernel != SLB_STOKES_SLDL || eta_panel, SLB_ERR_INVALID_ARG, "Stokes SL+DL needs eta_panel");
+    if (order == 0)
+        return nearquad_modal_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, nt, y_coarse, eta_panel, blocks,
+                                  s, nullptr, nullptr, nullptr, nullptr, ns, nt);
     return nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, ns, nt, y_coarse, eta_panel, order, beta,
                         blocks, s, nullptr, nullptr, nullptr, nullptr);
 }
@@ -1182,8 +1194,11 @@ extern "C" slb_status slb_nearcorr_quad_ragged(slb_kernel kernel, int64_t n_trg,
         set_error("slb_nearcorr_quad_ragged: copying the panel tables failed");
         return SLB_ERR_CUDA;
     }
-    slb_status r = nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse, eta_panel,
-                                order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d, classes, pc_d);
+    slb_status r = order == 0
+                       ? nearquad_modal_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse,
+                                            eta_panel, blocks, s, pnt_d, c0_d, bo_d, pns_d, nsmax, ntmax)
+                       : nearquad_run(kernel, n_trg, x_trg, trg_node, row_ptr, panel_idx, nsmax, ntmax, y_coarse, eta_panel,
+                                      order, beta, blocks, s, pnt_d, c0_d, bo_d, pns_d, classes, pc_d);
     cudaStreamSynchronize(s);
     cleanup();
     return r;

@@ -77,7 +77,7 @@ def test_exterior_dirichlet_cfie(kernel, rho):
     # Stokes needs the finer mesh to reach 1e-10 at targets 0.2 rho off the surface (study:
     # tools/bvp_study.py, profiles/r01_next/bvp_study.log); Laplace reaches 3e-12 on the coarse one
     P, Nt = (24, 12 if rho == 0.1 else 8) if kernel == 1 else (48, 16 if rho == 0.1 else 12)
-    quad = dict(order=14, beta=0.6)
+    quad = dict(order=0)
     eta = 1.0 / (2 * rho * np.log(1 / rho))
     X = exterior_targets(R, rho)
     pr = make_torus_problem(R=R, rho=rho, panels=P, Nt=Nt, kernel=kernel, eta=eta)

@@ -56,7 +56,7 @@ def golden():
     return rows
 
 
-def greens_rep_error(P, nt, order=14, beta=0.6):
+def greens_rep_error(P, nt, order=0, beta=0.6):
     from harness import DeviceProblem
     quad = dict(order=order, beta=beta)
     pr = make_torus_problem(R=1.0, rho=0.25, panels=P, Ns=10, Nt=nt, kernel=1)

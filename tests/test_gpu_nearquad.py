@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 import oracle as O  # noqa: E402
 from synth import make_torus_problem, torus_body  # noqa: E402
 
-QUAD = dict(order=14, beta=0.6)
+QUAD = dict(order=0)   # the paper's rule (modal angular sums, Bernstein s-panels, singular log rule)
 
 
 def cu(a, dt=None):
@@ -264,9 +264,10 @@ def test_nearcorr_quad_edge_cases():
     rp1 = cu(np.array([0, 1]), torch.int64)
     pi1 = cu(np.array([0]), torch.int32)
     b1 = torch.empty(pr.Ns * pr.Nt, dtype=torch.float64, device="cuda")
-    try:
-        S.slb_nearcorr_quad(1, xt, rp1, pi1, pr.Ns, pr.Nt, y, b1, order=14)
-    except SlbError as e:
-        assert "cell budget" in str(e) or "UNSUPPORTED" in str(e), e
-    else:
-        assert torch.isfinite(b1).all()
+    for order in (0, 14):
+        try:
+            S.slb_nearcorr_quad(1, xt, rp1, pi1, pr.Ns, pr.Nt, y, b1, order=order)
+        except SlbError as e:
+            assert "budget" in str(e) or "UNSUPPORTED" in str(e), e
+        else:
+            assert torch.isfinite(b1).all()

@@ -127,7 +127,8 @@ def test_gmres_ragged_manufactured(S):
 
 
 # ------------------------------------------------------------------ with special-quadrature blocks (N1)
-def test_ragged_quad_blocks_equal_orders_match_uniform(S):
+@pytest.mark.parametrize("order", [0, 10], ids=["paper_modal", "adaptive2d"])
+def test_ragged_quad_blocks_equal_orders_match_uniform(S, order):
     """slb_nearcorr_quad_ragged with all orders equal reproduces the uniform blocks bit for bit"""
     import paper_2310_00889_b200 as P
     pr = make_torus_problem(panels=8, kernel=2)
@@ -137,8 +138,8 @@ def test_ragged_quad_blocks_equal_orders_match_uniform(S):
     eta = cu(pr.eta_body[pr.body_of_panel])
     b1 = torch.empty(pr.nnz * pr.block_len, dtype=torch.float64, device="cuda")
     b2 = torch.empty_like(b1)
-    P.slb_nearcorr_quad(2, x, rp, pi, pr.Ns, pr.Nt, cu(pr.y_c), b1, trg_node=tn, eta_panel=eta, order=10)
-    P.slb_nearcorr_quad(2, x, rp, pi, pr.Ns, pr.Nt, cu(pr.y_c), b2, trg_node=tn, eta_panel=eta, order=10,
+    P.slb_nearcorr_quad(2, x, rp, pi, pr.Ns, pr.Nt, cu(pr.y_c), b1, trg_node=tn, eta_panel=eta, order=order)
+    P.slb_nearcorr_quad(2, x, rp, pi, pr.Ns, pr.Nt, cu(pr.y_c), b2, trg_node=tn, eta_panel=eta, order=order,
                         panel_nt=np.full(pr.P, pr.Nt))
     assert torch.equal(b1, b2)
 
@@ -151,7 +152,7 @@ def test_ragged_gauss_law_with_special_blocks(S):
     X, inside = near_surface_targets(seed=6)
     nts = np.array([12, 16, 20, 16] * 4, np.int32)
     pr = make_torus_problem(panels=16, extra_targets=X, nt_panels=nts)
-    dp = DeviceProblem(pr, quad=dict(order=14, beta=0.6))
+    dp = DeviceProblem(pr, quad=dict(order=0))
     u = dp.matvec(cu(np.ones((pr.N, 1)))).cpu().numpy()[:, 0]
     dp.close()
     assert np.abs(u[:pr.n_on]).max() < 1e-9
@@ -165,7 +166,7 @@ def test_ragged_ring_sedimentation(S):
     from harness import DeviceProblem
     rho, P = 1e-2, 24
     nts = np.array([8, 12] * (P // 2), np.int32)
-    quad = dict(order=14, beta=0.6)
+    quad = dict(order=0)
     pr = make_torus_problem(rho=rho, panels=P, kernel=2, nt_panels=nts)
     nu = completion_density(pr.y_c, pr.w_c, np.zeros(3), np.array([0.0, 0.0, -1.0]), np.zeros(3))
     Knu = []

@@ -51,7 +51,7 @@ def completion_density(y, w, center, F, Tq):
     return ab[:3] + np.cross(ab[3:], d)
 
 
-def sedimentation_speed(rho, panels, Ns=10, Nt=12, order=14, beta=0.6, tol=1e-14):
+def sedimentation_speed(rho, panels, Ns=10, Nt=12, order=0, beta=0.6, tol=1e-14):
     import oracle as O
     from harness import DeviceProblem
     from synth import make_torus_problem
@@ -115,7 +115,7 @@ def test_mobility_solve_ring_sedimentation(rho, panels, nt):
         pytest.skip("no CUDA device")
     from synth import make_torus_problem
     pr = make_torus_problem(rho=rho, panels=panels, Nt=nt, kernel=2)
-    mob, sl = _mobility_ops(pr, dict(order=14, beta=0.6))
+    mob, sl = _mobility_ops(pr, dict(order=0))
     rig, sig, it, rr = mob.op.mobility_solve(sl.op, [[0, 0, -1.0, 0, 0, 0]], tol=1e-14)
     mob.close(); sl.close()
     U = -rig[0, 2]
@@ -133,7 +133,7 @@ def test_mobility_solve_two_bodies_matches_assembled():
     import oracle as O
     from harness import DeviceProblem
     from synth import make_config
-    quad = dict(order=12, beta=0.6)
+    quad = dict(order=0)
     pr = make_config("c3", panels=10)                  # two tori, gap r/20, per-body eta
     rng = np.random.default_rng(3)
     ft = rng.standard_normal((2, 6))
@@ -183,7 +183,7 @@ def test_ring_sedimentation_graded_ragged_mesh():
     br = np.concatenate([[0.0], np.cumsum(np.concatenate([h, h[::-1]]))])
     br /= br[-1]
     nts = np.array([12, 8] * (P // 2), np.int32)
-    quad = dict(order=14, beta=0.6)
+    quad = dict(order=0)
     mk = lambda **kw: make_torus_problem(rho=rho, panels=P, kernel=2, nt_panels=nts, breaks=br, **kw)
     pr = mk()
     nu = completion_density(pr.y_c, pr.w_c, np.zeros(3), np.array([0.0, 0.0, -1.0]), np.zeros(3))
