@@ -1,15 +1,26 @@
 // nearlist.cu -- (NEXT N3) near-list construction on the GPU.
 //
-// Stands in for the paper's near-region search (§3.3: spheres around the nodes
-// of each element, Morton-sorted, overlap search): here the rule of DESIGN.md R15,
+// The near region of element k is a union of spheres centred at its nodes (PAPER.md Fig. bernstein-ellipse
+// caption P:L895-903), all of radius radius[k] (the caller's rule: R15's 2 L_k for the benchmark
+// configs, or a tolerance-based radius), so
 //     near(t) = { k : sqrt(min_j |x_t - y_kj|^2) < radius_k }  U  { own_panel[t] },
 // evaluated exactly in fp64 with the distance written as ((dx*dx + dy*dy) + dz*dz) without FMA
-// contraction, so decisions are bit-identical to the input generator's CPU rule.
-// One warp per target scans all panels: a bounding-sphere test (panel centroid + max node
-// distance, conservative by a relative 1e-9) prunes, survivors get the exact node minimum;
-// warp ballots emit the panel ids in ascending order.  Two passes (count, fill) around an
-// exclusive scan; output is the CSR the operator consumes.
+// contraction -- decisions are bit-identical to the input generator's CPU rule (synth/nearlist.py).
+//
+// Search (§3.3): targets are sorted on a Morton (Z-order) curve, 21 bits per axis over their
+// bounding box, so every cell of the implied octree is a contiguous section of the sorted array, found by
+// binary search.  The spheres of one element are searched together: the element's bounding sphere
+// (centroid + farthest node) grown by radius[k] gives a query cube; the tree depth is chosen so the cube
+// spans at most 2 cells per axis (the paper's "radius determines the depth"), and the <= 8 sections are
+// scanned (a warp per element) with the exact node test.  Searching per element instead of per sphere
+// means a (target, element) pair is produced at most once -- the paper's de-duplication step is not
+// needed -- and the own-panel pair is added separately.  Pairs are keyed t * P + k and sorted, which
+// yields the CSR (row_ptr by binary search of the sorted keys, panels ascending per row).  Sorting and
+// the prefix sum are CUB primitives (setup, not the apply path).  The previous O(T P) all-panel scan is
+// kept behind SLB_NEAR_SCAN=1 for timing comparisons.
 #include <algorithm>
+#include <cstdlib>
+#include <cub/cub.cuh>
 #include "common.cuh"
 
 namespace slb {
@@ -108,6 +119,284 @@ __global__ void __launch_bounds__(1024) scan_kernel(int64_t n, const int64_t* __
     if (threadIdx.x == 0) row_ptr[n] = carry;
 }
 
+
+// ------------------------------------------------------------------ Morton-sorted search
+constexpr int kMBits = 21;
+constexpr uint64_t kMMax = (1ull << kMBits) - 1;
+
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {       // 21 bits -> every third bit
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+__device__ __forceinline__ uint64_t morton3(uint64_t a, uint64_t b, uint64_t c) {
+    return spread3(a) | (spread3(b) << 1) | (spread3(c) << 2);
+}
+
+struct MBox { double lo[3], scale[3]; };
+
+__device__ __forceinline__ uint64_t quant(double v, double lo, double sc) {
+    double q = floor((v - lo) * sc);
+    q = fmin(fmax(q, 0.0), (double)kMMax);
+    return (uint64_t)q;
+}
+
+// bounding box of the targets: per-block partial min/max, then one block folds them
+__global__ void bbox_partial_kernel(int64_t T, const double* __restrict__ x, double* __restrict__ part) {
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
+        for (int q = 0; q < 3; ++q) { mn[q] = fmin(mn[q], x[3 * t + q]); mx[q] = fmax(mx[q], x[3 * t + q]); }
+    __shared__ double sh[6][256];
+    for (int q = 0; q < 3; ++q) { sh[q][threadIdx.x] = mn[q]; sh[3 + q][threadIdx.x] = mx[q]; }
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o)
+            for (int q = 0; q < 3; ++q) {
+                sh[q][threadIdx.x] = fmin(sh[q][threadIdx.x], sh[q][threadIdx.x + o]);
+                sh[3 + q][threadIdx.x] = fmax(sh[3 + q][threadIdx.x], sh[3 + q][threadIdx.x + o]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 6; ++q) part[6 * blockIdx.x + q] = sh[q][0];
+}
+
+__global__ void morton_kernel(int64_t T, const double* __restrict__ x, const double* __restrict__ part, int nparts,
+                              uint64_t* __restrict__ code, int32_t* __restrict__ idx, double* __restrict__ box) {
+    __shared__ double bx[6];
+    if (threadIdx.x < 6) {
+        double v = threadIdx.x < 3 ? 1e300 : -1e300;
+        for (int b = 0; b < nparts; ++b)
+            v = threadIdx.x < 3 ? fmin(v, part[6 * b + threadIdx.x]) : fmax(v, part[6 * b + threadIdx.x]);
+        bx[threadIdx.x] = v;
+    }
+    __syncthreads();
+    double lo[3], sc[3];
+    for (int q = 0; q < 3; ++q) {
+        const double ext = fmax(bx[3 + q] - bx[q], 1e-300);
+        lo[q] = bx[q];
+        sc[q] = (double)kMMax / ext;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 3) { box[threadIdx.x] = lo[threadIdx.x]; box[3 + threadIdx.x] = sc[threadIdx.x]; }
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+        code[t] = morton3(quant(x[3 * t], lo[0], sc[0]), quant(x[3 * t + 1], lo[1], sc[1]),
+                          quant(x[3 * t + 2], lo[2], sc[2]));
+        idx[t] = (int32_t)t;
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t v) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (a[m] < v) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+// One warp per element: query cube around the element's bounding sphere grown by radius[k]; <= 8 Morton
+// sections at the depth where the cube spans <= 2 cells per axis; exact node test on every target in them.
+// FILL = false: count per element; FILL = true: write keys t * P + k from offsets[k].
+template <bool FILL>
+__global__ void __launch_bounds__(256)
+near_morton_kernel(int64_t T, int64_t P, int Nn, const double* __restrict__ y, const double* __restrict__ radius,
+                   const double* __restrict__ sph, const int64_t* __restrict__ own, const uint64_t* __restrict__ code,
+                   const int32_t* __restrict__ idx, const double* __restrict__ xs, const double* __restrict__ box,
+                   int64_t* __restrict__ counts, const int64_t* __restrict__ offsets, uint64_t* __restrict__ keys) {
+    const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (k >= P) return;
+    const double lim = radius[k];
+    const double c0 = sph[4 * k], c1 = sph[4 * k + 1], c2 = sph[4 * k + 2], R = sph[4 * k + 3];
+    const double reach = (R + lim) * (1.0 + 1e-9) + 1e-300;       // conservative (pre-filter only)
+    const double cc[3] = {c0, c1, c2};
+    uint64_t qlo[3], qhi[3];
+    uint64_t span = 0;
+    for (int q = 0; q < 3; ++q) {
+        qlo[q] = quant(cc[q] - reach, box[q], box[3 + q]);
+        qhi[q] = quant(cc[q] + reach, box[q], box[3 + q]);
+        span = max(span, qhi[q] - qlo[q]);
+    }
+    int sh = 0;                                                     // cell edge 2^sh >= span + 1
+    while (sh < kMBits && (1ull << sh) < span + 1) ++sh;
+    int64_t cnt = 0;
+    int64_t base = FILL ? offsets[k] : 0;
+    const double* yk = y + k * (int64_t)Nn * 3;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t cx = qlo[0] >> sh; cx <= (qhi[0] >> sh); ++cx)
+        for (uint64_t cy = qlo[1] >> sh; cy <= (qhi[1] >> sh); ++cy)
+            for (uint64_t cz = qlo[2] >> sh; cz <= (qhi[2] >> sh); ++cz) {
+                const uint64_t pre = morton3(cx, cy, cz);
+                const uint64_t a = pre << (3 * sh), b = (3 * sh >= 63) ? ~0ull : ((pre + 1) << (3 * sh));
+                int64_t i0 = 0, i1 = 0;
+                if (lane == 0) {
+                    i0 = lower_bound_u64(code, T, a);
+                    i1 = lower_bound_u64(code, T, b);
+                }
+                i0 = __shfl_sync(0xffffffffu, i0, 0);
+                i1 = __shfl_sync(0xffffffffu, i1, 0);
+                for (int64_t i = i0; i < i1; i += 32) {
+                    bool near = false;
+                    int32_t t = -1;
+                    if (i + lane < i1) {
+                        t = idx[i + lane];
+                        const double x0 = xs[3 * (i + lane)], x1 = xs[3 * (i + lane) + 1], x2 = xs[3 * (i + lane) + 2];
+                        const double ex = x0 - c0, ey = x1 - c1, ez = x2 - c2;
+                        const bool own_k = own && own[t] == k;
+                        if (!own_k && sqrt(ex * ex + ey * ey + ez * ez) < reach) {
+                            for (int j = 0; j < Nn && !near; ++j) {
+                                const double dx = __dsub_rn(x0, yk[3 * j]);
+                                const double dy = __dsub_rn(x1, yk[3 * j + 1]);
+                                const double dz = __dsub_rn(x2, yk[3 * j + 2]);
+                                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                                            __dmul_rn(dz, dz));
+                                near = __dsqrt_rn(d2) < lim;
+                            }
+                        }
+                    }
+                    const unsigned mask = __ballot_sync(0xffffffffu, near);
+                    if (FILL && near) keys[base + cnt + __popc(mask & lt)] = (uint64_t)t * (uint64_t)P + (uint64_t)k;
+                    cnt += __popc(mask);
+                }
+            }
+    if (!FILL && lane == 0) counts[k] = cnt;
+}
+
+__global__ void own_keys_kernel(int64_t T, int64_t P, const int64_t* __restrict__ own, uint64_t* __restrict__ keys) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = own ? own[t] : -1;
+        keys[t] = (o >= 0 && o < P) ? (uint64_t)t * (uint64_t)P + (uint64_t)o : ~0ull;
+    }
+}
+
+__global__ void gather_x_kernel(int64_t T, const double* __restrict__ x, const int32_t* __restrict__ idx,
+                                double* __restrict__ xs) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t t = idx[i];
+        xs[3 * i] = x[3 * t]; xs[3 * i + 1] = x[3 * t + 1]; xs[3 * i + 2] = x[3 * t + 2];
+    }
+}
+
+// row_ptr[t] = first key >= t * P (t = 0..T), nnz = first sentinel; panel ids = key mod P
+__global__ void csr_from_keys_kernel(int64_t T, int64_t P, const uint64_t* __restrict__ keys, int64_t n,
+                                     int64_t* __restrict__ row_ptr) {
+    const int64_t nnz = lower_bound_u64(keys, n, ~0ull);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += (int64_t)gridDim.x * blockDim.x)
+        row_ptr[t] = t == T ? nnz : lower_bound_u64(keys, nnz, (uint64_t)t * (uint64_t)P);
+}
+
+__global__ void panel_from_keys_kernel(int64_t nnz, int64_t P, const uint64_t* __restrict__ keys,
+                                       int32_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)(keys[i] % (uint64_t)P);
+}
+
+static bool near_use_scan() {
+    static const bool v = [] { const char* e = getenv("SLB_NEAR_SCAN"); return e && e[0] == '1'; }();
+    return v;
+}
+
+static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int Nn, const double* y,
+                                    const double* radius, const int64_t* own, int64_t* row_ptr, int32_t* panel_idx,
+                                    int64_t capacity, int64_t* nnz_out, cudaStream_t s) {
+    const int nb = std::max(1, std::min(num_sms() * 4, (int)((T + 255) / 256)));
+    double *part = nullptr, *box = nullptr, *xs = nullptr, *sph = nullptr;
+    uint64_t *code = nullptr, *code_s = nullptr, *keys = nullptr, *keys_s = nullptr;
+    int32_t *idx = nullptr, *idx_s = nullptr;
+    int64_t *counts = nullptr, *offs = nullptr;
+    void* tmp = nullptr;
+    slb_status st = SLB_OK;
+    auto fail = [&](cudaError_t e, const char* what) {
+        set_error(std::string("slb_near_build (Morton): ") + what + ": " + cudaGetErrorString(e));
+        st = e == cudaErrorMemoryAllocation ? SLB_ERR_OOM : SLB_ERR_CUDA;
+    };
+#define NB_CUDA(call, what) do { cudaError_t e_ = (call); if (e_ != cudaSuccess && st == SLB_OK) fail(e_, what); } while (0)
+    NB_CUDA(cudaMallocAsync(&part, sizeof(double) * 6 * nb, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&box, sizeof(double) * 6, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&code, sizeof(uint64_t) * T, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&code_s, sizeof(uint64_t) * T, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&idx, sizeof(int32_t) * T, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&idx_s, sizeof(int32_t) * T, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&xs, sizeof(double) * 3 * T, s), "alloc");
+    NB_CUDA(cudaMallocAsync(&sph, sizeof(double) * 4 * std::max<int64_t>(P, 1), s), "alloc");
+    NB_CUDA(cudaMallocAsync(&counts, sizeof(int64_t) * (P + 1), s), "alloc");
+    NB_CUDA(cudaMallocAsync(&offs, sizeof(int64_t) * (P + 1), s), "alloc");
+    if (st == SLB_OK) {
+        bbox_partial_kernel<<<nb, 256, 0, s>>>(T, x, part);
+        morton_kernel<<<nb, 256, 0, s>>>(T, x, part, nb, code, idx, box);
+        g_launch_count += 2;
+        size_t tb = 0;
+        NB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, code, code_s, idx, idx_s, (int)T, 0, 3 * kMBits, s), "sort size");
+        NB_CUDA(cudaMallocAsync(&tmp, tb, s), "alloc");
+        NB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, code, code_s, idx, idx_s, (int)T, 0, 3 * kMBits, s), "sort");
+        cudaFreeAsync(tmp, s);
+        tmp = nullptr;
+        gather_x_kernel<<<nb, 256, 0, s>>>(T, x, idx_s, xs);
+        panel_sphere_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(P, Nn, y, sph);
+        near_morton_kernel<false><<<(unsigned)((P + 7) / 8), 256, 0, s>>>(T, P, Nn, y, radius, sph, own, code_s, idx_s,
+                                                                        xs, box, counts, nullptr, nullptr);
+        g_launch_count += 3;
+        NB_CUDA(cudaMemsetAsync(counts + P, 0, sizeof(int64_t), s), "memset");
+        size_t sb = 0;
+        NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, counts, offs, (int)(P + 1), s), "scan size");
+        NB_CUDA(cudaMallocAsync(&tmp, sb, s), "alloc");
+        NB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, sb, counts, offs, (int)(P + 1), s), "scan");
+        cudaFreeAsync(tmp, s);
+        tmp = nullptr;
+    }
+    int64_t nsearch = 0;
+    if (st == SLB_OK) {
+        NB_CUDA(cudaMemcpyAsync(&nsearch, offs + P, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "copy");
+        NB_CUDA(cudaStreamSynchronize(s), "sync");
+    }
+    const int64_t n = nsearch + T;
+    if (st == SLB_OK) {
+        NB_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * std::max<int64_t>(n, 1), s), "alloc");
+        NB_CUDA(cudaMallocAsync(&keys_s, sizeof(uint64_t) * std::max<int64_t>(n, 1), s), "alloc");
+    }
+    if (st == SLB_OK) {
+        near_morton_kernel<true><<<(unsigned)((P + 7) / 8), 256, 0, s>>>(T, P, Nn, y, radius, sph, own, code_s, idx_s,
+                                                                       xs, box, nullptr, offs, keys);
+        own_keys_kernel<<<nb, 256, 0, s>>>(T, P, own, keys + nsearch);
+        g_launch_count += 2;
+        size_t kb = 0;
+        NB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, kb, keys, keys_s, (int)n, 0, 64, s), "sort size");
+        NB_CUDA(cudaMallocAsync(&tmp, kb, s), "alloc");
+        NB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, kb, keys, keys_s, (int)n, 0, 64, s), "sort");
+        cudaFreeAsync(tmp, s);
+        tmp = nullptr;
+        csr_from_keys_kernel<<<nb, 256, 0, s>>>(T, P, keys_s, n, row_ptr);
+        ++g_launch_count;
+    }
+    int64_t nnz = 0;
+    if (st == SLB_OK) {
+        NB_CUDA(cudaMemcpyAsync(&nnz, row_ptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "copy");
+        NB_CUDA(cudaStreamSynchronize(s), "sync");
+    }
+    if (st == SLB_OK) {
+        *nnz_out = nnz;
+        if (panel_idx) {
+            if (capacity < nnz) {
+                set_error("slb_near_build: capacity < nnz");
+                st = SLB_ERR_INVALID_ARG;
+            } else if (nnz > 0) {
+                panel_from_keys_kernel<<<nb, 256, 0, s>>>(nnz, P, keys_s, panel_idx);
+                ++g_launch_count;
+            }
+        }
+    }
+    if (st == SLB_OK) st = check_launch("slb_near_build (Morton)");
+#undef NB_CUDA
+    cudaFreeAsync(part, s); cudaFreeAsync(box, s); cudaFreeAsync(code, s); cudaFreeAsync(code_s, s);
+    cudaFreeAsync(idx, s); cudaFreeAsync(idx_s, s); cudaFreeAsync(xs, s); cudaFreeAsync(sph, s);
+    cudaFreeAsync(counts, s); cudaFreeAsync(offs, s); cudaFreeAsync(keys, s); cudaFreeAsync(keys_s, s);
+    return st;
+}
+
 }  // namespace slb
 
 using namespace slb;
@@ -121,6 +410,10 @@ extern "C" slb_status slb_near_build(int64_t n_trg, const double* x_trg, int64_t
     SLB_REQUIRE(n_trg == 0 || (x_trg && (n_panels == 0 || (y_nodes && radius))), SLB_ERR_INVALID_ARG, "null input");
     SLB_REQUIRE(n_panels <= 2147483647LL, SLB_ERR_UNSUPPORTED, "panel ids must fit int32");
     SLB_REQUIRE(check_sticky("slb_near_build") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    SLB_REQUIRE(n_trg <= 2147483647LL, SLB_ERR_UNSUPPORTED, "target ids must fit int32");
+    if (!near_use_scan() && n_trg > 0 && n_panels > 0)
+        return near_build_morton(n_trg, x_trg, n_panels, nodes_per_panel, y_nodes, radius, own_panel, row_ptr, panel_idx,
+                                 capacity, nnz_out, s);
     double* sph = nullptr;
     int64_t* counts = nullptr;
     SLB_CUDA(cudaMallocAsync(&sph, sizeof(double) * 4 * std::max<int64_t>(n_panels, 1), s));

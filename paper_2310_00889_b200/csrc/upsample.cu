@@ -327,6 +327,191 @@ upsample_warp_kernel(int kind, int64_t n_panels, int ns, int nt, int ms, int mt,
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// upsample_rec_kernel<NS, NT, MS, MT>: the Stokes record path (NC = 3, dyn records) with the grid fixed at
+// compile time (the benchmark grids: 10x12 -> 20x24 for c4/c5, 10x16 -> 20x32, 12x20 -> 24x40), so every
+// DMMA tile loop is unrolled and addressing is constant-folded.  Differences to the generic kernel: the
+// fine-node scales are prefetched straight into registers (__ldg, issued before the contraction; no
+// shared-memory buffer), which leaves ~12 KB of shared memory per warp and 16 warps per SM; the coarse
+// density is still double-buffered by TMA bulk copies.
+
+template <int NS, int NT, int MS, int MT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const double* __restrict__ sc_in,
+                    const double* __restrict__ scale, double* __restrict__ dyn, double* __restrict__ copy_out,
+                    const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
+                    const int64_t* __restrict__ f_off) {
+    constexpr int NC = 3;
+    constexpr int NSP = (NS + 3) / 4 * 4, NTP = (NT + 3) / 4 * 4, MSP = (MS + 7) / 8 * 8, MTP = (MT + 7) / 8 * 8;
+    constexpr int ROWS = NS * NC, ROWS8 = (ROWS + 7) / 8 * 8;
+    constexpr int LDP = (NSP % 16 == 0 || NSP % 16 == 8) ? NSP + 4 : NSP;
+    constexpr int LDF = (NTP % 16 == 0 || NTP % 16 == 8) ? NTP + 4 : NTP;
+    constexpr int LDT = (MTP % 16 == 0) ? MTP + 8 : MTP;
+    constexpr int NIN = NS * NT * NC, NIN2 = (NIN + 1) & ~1, NOUT = MS * MT;
+    constexpr int WARP_D = 2 * NIN2 + NC * NSP * LDT;
+    constexpr int NA = MSP / 8, NB = MTP / 8;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[WARPS * 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double* Ps = sm;                                   // [MSP][LDP]
+    double* F = Ps + MSP * LDP;                        // [MTP][LDF]
+    double* wb = F + MTP * LDF + (size_t)warp * WARP_D;
+    double* raw = wb;                                  // [2][NIN2]
+    double* T1 = raw + 2 * NIN2;                       // [NC][NSP][LDT]
+    uint64_t* bar = bars + 2 * warp;
+    for (int q = threadIdx.x; q < MSP * LDP; q += blockDim.x) {
+        const int a = q / LDP, i = q % LDP;
+        Ps[q] = (a < MS && i < NS) ? mats[a * NS + i] : 0.0;
+    }
+    for (int q = threadIdx.x; q < MTP * LDF; q += blockDim.x) {
+        const int b = q / LDF, j = q % LDF;
+        F[q] = (b < MT && j < NT) ? mats[MS * NS + b * NT + j] : 0.0;
+    }
+    for (int q = lane; q < NC * NSP * LDT; q += 32) T1[q] = 0.0;
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t gw = (int64_t)blockIdx.x * nw + warp, stride = (int64_t)gridDim.x * nw;
+    auto issue = [&](int64_t pl, int buf) {
+        const int64_t p = plist ? (int64_t)plist[pl] : pl;
+        const double* src = sc_in + (c_off ? c_off[p] * NC : p * (int64_t)NIN);
+        mbar_expect_tx(&bar[buf], (uint32_t)(NIN * 8));
+        bulk_g2s(raw + buf * NIN2, src, (uint32_t)(NIN * 8), &bar[buf]);
+    };
+    if (lane == 0 && gw < n_panels) issue(gw, 0);
+    const int g = lane >> 2, tq = lane & 3;
+    int it = 0;
+    for (int64_t pl = gw; pl < n_panels; pl += stride, ++it) {
+        const int buf = it & 1;
+        const int64_t p = plist ? (int64_t)plist[pl] : pl;
+        const int64_t m0 = f_off ? f_off[p] : p * (int64_t)NOUT;
+        // this lane's fine-node scales (2 adjacent nodes per output tile), loads in flight during the GEMMs
+        double sc0[NA][NB], sc1[NA][NB];
+#pragma unroll
+        for (int ta = 0; ta < NA; ++ta)
+#pragma unroll
+            for (int tb = 0; tb < NB; ++tb) {
+                const int a = ta * 8 + g, b = tb * 8 + 2 * tq;
+                if (a < MS && b < MT) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(scale + m0 + a * MT + b));
+                    sc0[ta][tb] = v.x;
+                    sc1[ta][tb] = v.y;
+                } else {
+                    sc0[ta][tb] = sc1[ta][tb] = 0.0;
+                }
+            }
+        mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
+        __syncwarp();
+        if (lane == 0 && pl + stride < n_panels) {
+            fence_proxy_async_smem();
+            issue(pl + stride, buf ^ 1);
+        }
+        const double* R = raw + buf * NIN2;
+        if (copy_out) {
+            double* dst = copy_out + (c_off ? c_off[p] * NC : p * (int64_t)NIN);
+            for (int q = lane; q < NIN; q += 32) dst[q] = R[q];
+        }
+        // step 1: T1_c[i][b] = sum_j sigma[i][j][c] F[b][j], rows r = i NC + c
+#pragma unroll
+        for (int r0 = 0; r0 < ROWS8; r0 += 8) {
+            const int r = r0 + g;
+            const int rb = (r < ROWS) ? (r / NC) * NT * NC + (r % NC) : 0;
+#pragma unroll
+            for (int n0 = 0; n0 < MTP; n0 += 8) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int k0 = 0; k0 < NTP; k0 += 4) {
+                    const int j = k0 + tq;
+                    const double av = (r < ROWS && j < NT) ? R[rb + j * NC] : 0.0;
+                    dmma_8x8x4(d0, d1, av, F[(n0 + g) * LDF + k0 + tq]);
+                }
+                if (r < ROWS) {
+                    double* T = T1 + ((r % NC) * NSP + r / NC) * LDT + n0 + 2 * tq;
+                    T[0] = d0;
+                    T[1] = d1;
+                }
+            }
+        }
+        __syncwarp();
+        // step 2 + epilogue: records {g, 0} of two adjacent nodes per lane straight from the accumulators
+        double2* D2 = reinterpret_cast<double2*>(dyn);
+#pragma unroll
+        for (int ta = 0; ta < NA; ++ta) {
+#pragma unroll
+            for (int tb = 0; tb < NB; ++tb) {
+                double d0[NC], d1[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) d0[c] = d1[c] = 0.0;
+#pragma unroll
+                for (int k0 = 0; k0 < NSP; k0 += 4) {
+                    const double av = Ps[(ta * 8 + g) * LDP + k0 + tq];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        dmma_8x8x4(d0[c], d1[c], av, T1[(c * NSP + k0 + tq) * LDT + tb * 8 + g]);
+                }
+                const int a = ta * 8 + g, b = tb * 8 + 2 * tq;
+                if (a < MS && b < MT) {
+                    const int64_t m = m0 + a * MT + b;
+                    const double s0 = sc0[ta][tb], s1 = sc1[ta][tb];
+                    double2* o = D2 + 2 * m;
+                    o[0] = make_double2(s0 * d0[0], s0 * d0[1]);
+                    o[1] = make_double2(s0 * d0[2], 0.0);
+                    o[2] = make_double2(s1 * d1[0], s1 * d1[1]);
+                    o[3] = make_double2(s1 * d1[2], 0.0);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int NS, int NT, int MS, int MT>
+static constexpr size_t rec_smem_bytes(int warps) {
+    return sizeof(double) * ((size_t)((MS + 7) / 8 * 8) * (((NS + 3) / 4 * 4) % 16 == 0 || ((NS + 3) / 4 * 4) % 16 == 8
+                                                              ? (NS + 3) / 4 * 4 + 4 : (NS + 3) / 4 * 4) +
+                             (size_t)((MT + 7) / 8 * 8) * (((NT + 3) / 4 * 4) % 16 == 0 || ((NT + 3) / 4 * 4) % 16 == 8
+                                                              ? (NT + 3) / 4 * 4 + 4 : (NT + 3) / 4 * 4) +
+                             (size_t)warps * (2 * ((NS * NT * 3 + 1) & ~1) +
+                                              3 * ((NS + 3) / 4 * 4) *
+                                                  ((((MT + 7) / 8 * 8) % 16 == 0) ? (MT + 7) / 8 * 8 + 8 : (MT + 7) / 8 * 8)));
+}
+
+template <int NS, int NT, int MS, int MT, int WARPS>
+static slb_status launch_rec(int64_t n_panels, const double* mats, const double* sc_in, const double* scale,
+                             double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
+                             const int64_t* f_off, cudaStream_t s) {
+    const size_t bytes = rec_smem_bytes<NS, NT, MS, MT>(WARPS);
+    const void* fn = (const void*)upsample_rec_kernel<NS, NT, MS, MT, WARPS>;
+    { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
+    int per_sm = 0;
+    SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, bytes));
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((n_panels + WARPS - 1) / WARPS, (int64_t)num_sms() * std::max(1, per_sm)));
+    upsample_rec_kernel<NS, NT, MS, MT, WARPS><<<grid, WARPS * 32, bytes, s>>>(n_panels, mats, sc_in, scale, dyn,
+                                                                              copy_out, plist, c_off, f_off);
+    ++g_launch_count;
+    return check_launch("upsample_rec_kernel");
+}
+
+// the compiled grids; returns false when (ns, nt, ms, mt) is not one of them
+static bool rec_supported(int ns, int nt, int ms, int mt) {
+    return (ns == 10 && nt == 12 && ms == 20 && mt == 24) || (ns == 10 && nt == 16 && ms == 20 && mt == 32) ||
+           (ns == 12 && nt == 20 && ms == 24 && mt == 40);
+}
+
+static slb_status rec_dispatch(const InterpParams& ip, int64_t n_panels, const double* sc_in, const double* scale,
+                               double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
+                               const int64_t* f_off, cudaStream_t s) {
+    if (ip.ns == 10 && ip.nt == 12)
+        return launch_rec<10, 12, 20, 24, 16>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
+    if (ip.ns == 10 && ip.nt == 16)
+        return launch_rec<10, 16, 20, 32, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
+    return launch_rec<12, 20, 24, 40, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
+}
+
 // Per-warp buffers of the streaming kernel (doubles), or 0 when it does not apply (large grids).
 static size_t up_warp_bytes(const InterpParams& ip, int nc, bool scaled, bool scalar, int* warps) {
     const UpWarpLayout L = up_layout(ip.ns, ip.nt, ip.ms, ip.mt, nc, scaled ? (scalar ? 4 : 1) : 0);
@@ -357,6 +542,10 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
     if (n_panels <= 0) return SLB_OK;
     int warps = 0;
     const size_t wsm = up_warp_bytes(ip, nc, dyn != nullptr, far_scalar(kind), &warps);
+    static const bool generic = [] { const char* e = getenv("SLB_UPSAMPLE_GENERIC"); return e && e[0] == '1'; }();
+    if (!generic && dyn && nc == 3 && !far_scalar(kind) && rec_supported(ip.ns, ip.nt, ip.ms, ip.mt) &&
+        upsample_streams(kind, ip, nc, true, sigma_coarse, sc))
+        return rec_dispatch(ip, n_panels, sigma_coarse, sc, dyn, copy_out, plist, c_off, f_off, s);
     if (upsample_streams(kind, ip, nc, dyn != nullptr, sigma_coarse, sc)) {
         { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<1>); if (st_ != SLB_OK) return st_; }
         { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<3>); if (st_ != SLB_OK) return st_; }

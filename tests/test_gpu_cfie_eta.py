@@ -43,7 +43,9 @@ def _laplace_iters(rho, eta, tol=1e-10, must_converge=True):
     from harness import DeviceProblem
     pr = make_torus_problem(rho=rho, panels=24, Nt=8, kernel=1, eta=eta)
     y = pr.y_c
-    u0 = (np.cos(np.arctan2(y[:, 1], y[:, 0])) + y[:, 2] / rho)[:, None]
+    # data with a constant part: the exterior I/2 + D annihilates constants (Gauss law), so that mode is
+    # carried by the single layer alone
+    u0 = (1.0 + np.cos(np.arctan2(y[:, 1], y[:, 0])) + y[:, 2] / rho)[:, None]
     dp = DeviceProblem(pr, quad=dict(order=0))
     _, it, rr = dp.op.gmres(torch.from_numpy(np.ascontiguousarray(u0)).cuda(), restart=200, max_iters=400, tol=tol)
     dp.close()
@@ -54,16 +56,16 @@ def _laplace_iters(rho, eta, tol=1e-10, must_converge=True):
 def test_laplace_cfie_iterations_do_not_grow_with_slenderness():
     """Laplace combined field I/2 + D + S_L / (2 rho ln(1/rho)) (Eq. e:laplace-bie-new): 'the
     condition number remains small as rho shrinks' -- GMRES iterations stay flat from
-    rho = 1e-2 to 1e-4, while with two decades less single layer (towards the pure double layer, whose
-    exterior I/2 + D annihilates constants, Gauss law, and has the j = 0 modes near 0) the
-    count grows as rho shrinks (capped at 400: it need not converge)"""
+    rho = 1e-2 to 1e-4, while with a FIXED small single-layer weight (eta = 0.05, not scaled like
+    1/(rho log 1/rho)) the constant mode -- annihilated by the exterior I/2 + D, P:L1735 -- gets an
+    eigenvalue ~ eta rho log(1/rho) -> 0 and the count grows as rho shrinks (capped at 400)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cf, weak = {}, {}
     for rho in (1e-2, 1e-3, 1e-4):
         eta = 1.0 / (2 * rho * np.log(1 / rho))
         cf[rho] = _laplace_iters(rho, eta)
-        weak[rho] = _laplace_iters(rho, 0.01 * eta, must_converge=False)
-    print("Laplace GMRES iterations, CFIE at eta*:", cf, " at eta*/100:", weak)
+        weak[rho] = _laplace_iters(rho, 0.05, must_converge=False)
+    print("Laplace GMRES iterations, CFIE at eta*:", cf, " at eta = 0.05:", weak)
     assert max(cf.values()) - min(cf.values()) <= 3, cf
-    assert cf[1e-4] <= cf[1e-2] and weak[1e-4] > weak[1e-2], (cf, weak)      # measured 5, 4, 3 vs 4, 10, 9
+    assert cf[1e-4] <= cf[1e-2] + 1 and weak[1e-4] > weak[1e-2], (cf, weak)
