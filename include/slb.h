@@ -262,6 +262,16 @@ slb_status slb_matvec_host(slb_operator* op, const double* sigma_local_host, dou
  * [0] projector+upsample, [1] all-gather, [2] far field, [3] finalize (reduce+near+identity). */
 slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]);
 
+/* (NEXT N4) 1 if the operator gathers the fine source records through an NVLink-SHARP multicast object
+ * (environment SLB_NVLS=1 at creation, a communicator, a multicast-capable device, the streaming
+ * upsample): the upsample epilogue stores every record with multimem.st into all ranks' copies and the
+ * per-apply ncclAllGather of the records is dropped (a one-int all-reduce barrier remains for > 1 rank;
+ * more ranks exchange the multicast handle as a fabric handle).  0: the NCCL all-gather path. */
+int slb_operator_nvls(const slb_operator* op);
+
+/* 1 if this device supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED). */
+int slb_nvls_supported(void);
+
 /* Number of kernel launches slb_matvec issues on this rank (for launch accounting). */
 int slb_operator_launches_per_matvec(const slb_operator* op);
 

@@ -53,6 +53,8 @@ _SIGS = {
     "slb_matvec_host": (I32, [P, P, P, P]),
     "slb_operator_last_timings": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
     "slb_operator_launches_per_matvec": (I32, [P]),
+    "slb_operator_nvls": (I32, [P]),
+    "slb_nvls_supported": (I32, []),
     "slb_operator_destroy": (I32, [P]),
     "slb_gmres": (I32, [P, P, P, I32, I32, D, ctypes.POINTER(I32), ctypes.POINTER(D), P]),
     "slb_mobility_solve": (I32, [P, P, P, P, P, I32, I32, D, ctypes.POINTER(I32), ctypes.POINTER(D), P]),

@@ -308,6 +308,10 @@ class Operator:
     def launches_per_matvec(self):
         return lib().slb_operator_launches_per_matvec(self.h)
 
+    def uses_nvls(self):
+        """True when the fine records are gathered through a multicast object (NEXT N4, SLB_NVLS=1)."""
+        return bool(lib().slb_operator_nvls(self.h))
+
     def close(self):
         if self.h:
             lib().slb_operator_destroy(self.h)

@@ -123,6 +123,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// 16-byte store through a multicast (NVLS) mapping: replicated by the switch into every bound copy.
+// multimem.st has no .v2.f64 form; the two doubles travel as four 32-bit lanes (a store: bits unchanged).
+__device__ __forceinline__ void multimem_st2(double* p, double a, double b) {
+    const unsigned long long ua = (unsigned long long)__double_as_longlong(a);
+    const unsigned long long ub = (unsigned long long)__double_as_longlong(b);
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "f"(__int_as_float((int)(ua & 0xffffffffull))), "f"(__int_as_float((int)(ua >> 32))),
+                 "f"(__int_as_float((int)(ub & 0xffffffffull))), "f"(__int_as_float((int)(ub >> 32)))
+                 : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -199,7 +210,7 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
                            double* dyn, cudaStream_t s, const int32_t* plist = nullptr,
                            const int64_t* c_off = nullptr, const int64_t* f_off = nullptr,
-                           double* copy_out = nullptr);
+                           double* copy_out = nullptr, double* dyn_mc = nullptr);
 
 // true when upsample_launch takes the streaming warp-per-panel kernel for this grid (which can also
 // write the staged coarse density to copy_out, for any plist)

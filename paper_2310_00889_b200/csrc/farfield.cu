@@ -30,7 +30,8 @@ FarPlan far_plan(int64_t M) {
     p.M = M;
     if (M >= (int64_t(1) << 19)) { p.chunk = 65536; p.split = 1; }
     else if (M >= (int64_t(1) << 15)) { p.chunk = 8192; p.split = 1; }
-    else { p.chunk = 1024; p.split = 4; }
+    else if (M >= (int64_t(1) << 13)) { p.chunk = 1024; p.split = 4; }
+    else { p.chunk = 256; p.split = 4; }       // tiny M (c1: 3,840 sources): one chunk per tile fills the SMs
     p.n_chunks = (M + p.chunk - 1) / p.chunk;
     if (p.n_chunks < 1) p.n_chunks = 1;
     return p;

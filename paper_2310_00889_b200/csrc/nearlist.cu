@@ -10,9 +10,10 @@
 // Search (§3.3): targets are sorted on a Morton (Z-order) curve, 21 bits per axis over their
 // bounding box, so every cell of the implied octree is a contiguous section of the sorted array, found by
 // binary search.  The spheres of one element are searched together: the element's bounding sphere
-// (centroid + farthest node) grown by radius[k] gives a query cube; the tree depth is chosen so the cube
-// spans at most 2 cells per axis (the paper's "radius determines the depth"), and the <= 8 sections are
-// scanned (a warp per element) with the exact node test.  Searching per element instead of per sphere
+// (centroid + farthest node) grown by radius[k] gives a query cube; the tree depth is chosen from that
+// size so the cube spans at most 5 cells per axis (the paper's "radius determines the depth"), and the
+// sections are scanned (a warp per element): bounding-sphere test, rigorous node-group bounds (groups of
+// 12 nodes: a ring of the benchmark grids) that decide most targets, the exact node test for the rest.  Searching per element instead of per sphere
 // means a (target, element) pair is produced at most once -- the paper's de-duplication step is not
 // needed -- and the own-panel pair is added separately.  Pairs are keyed t * P + k and sorted, which
 // yields the CSR (row_ptr by binary search of the sorted keys, panels ascending per row).  Sorting and
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(int64_t n, const int64_t* __
 
 // ------------------------------------------------------------------ Morton-sorted search
 constexpr int kMBits = 21;
+constexpr int kGrp = 12;          // nodes per bounding group (group_bounds_kernel)
 constexpr uint64_t kMMax = (1ull << kMBits) - 1;
 
 __device__ __forceinline__ uint64_t spread3(uint64_t v) {       // 21 bits -> every third bit
@@ -206,7 +208,8 @@ __global__ void __launch_bounds__(256)
 near_morton_kernel(int64_t T, int64_t P, int Nn, const double* __restrict__ y, const double* __restrict__ radius,
                    const double* __restrict__ sph, const int64_t* __restrict__ own, const uint64_t* __restrict__ code,
                    const int32_t* __restrict__ idx, const double* __restrict__ xs, const double* __restrict__ box,
-                   int64_t* __restrict__ counts, const int64_t* __restrict__ offsets, uint64_t* __restrict__ keys) {
+                   const double* __restrict__ gb, int64_t* __restrict__ counts, const int64_t* __restrict__ offsets,
+                   uint64_t* __restrict__ keys) {
     const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (k >= P) return;
@@ -221,11 +224,13 @@ near_morton_kernel(int64_t T, int64_t P, int Nn, const double* __restrict__ y, c
         qhi[q] = quant(cc[q] + reach, box[q], box[3 + q]);
         span = max(span, qhi[q] - qlo[q]);
     }
-    int sh = 0;                                                     // cell edge 2^sh >= span + 1
-    while (sh < kMBits && (1ull << sh) < span + 1) ++sh;
+    int sh = 0;                                                     // cell edge 2^sh >= (span + 1) / 4:
+    while (sh < kMBits && (4ull << sh) < span + 1) ++sh;            // <= 5 cells per axis, tighter than 2
     int64_t cnt = 0;
     int64_t base = FILL ? offsets[k] : 0;
     const double* yk = y + k * (int64_t)Nn * 3;
+    const int ng = (Nn + kGrp - 1) / kGrp;
+    const double* gk = gb + 4 * k * (int64_t)ng;
     const unsigned lt = (1u << lane) - 1u;
     for (uint64_t cx = qlo[0] >> sh; cx <= (qhi[0] >> sh); ++cx)
         for (uint64_t cy = qlo[1] >> sh; cy <= (qhi[1] >> sh); ++cy)
@@ -248,7 +253,16 @@ near_morton_kernel(int64_t T, int64_t P, int Nn, const double* __restrict__ y, c
                         const double ex = x0 - c0, ey = x1 - c1, ez = x2 - c2;
                         const bool own_k = own && own[t] == k;
                         if (!own_k && sqrt(ex * ex + ey * ey + ez * ez) < reach) {
-                            for (int j = 0; j < Nn && !near; ++j) {
+                            double lo = 1e300, hi = 1e300;
+                            for (int g2 = 0; g2 < ng; ++g2) {
+                                const double gx = x0 - gk[4 * g2], gy = x1 - gk[4 * g2 + 1], gz = x2 - gk[4 * g2 + 2];
+                                const double dg = sqrt(gx * gx + gy * gy + gz * gz);
+                                lo = fmin(lo, dg - gk[4 * g2 + 3]);
+                                hi = fmin(hi, dg + gk[4 * g2 + 3]);
+                            }
+                            if (hi < lim * (1.0 - 1e-9)) near = true;
+                            const bool undecided = !near && lo < lim * (1.0 + 1e-9);
+                            for (int j = 0; undecided && j < Nn && !near; ++j) {
                                 const double dx = __dsub_rn(x0, yk[3 * j]);
                                 const double dy = __dsub_rn(x1, yk[3 * j + 1]);
                                 const double dz = __dsub_rn(x2, yk[3 * j + 2]);
@@ -264,6 +278,33 @@ near_morton_kernel(int64_t T, int64_t P, int Nn, const double* __restrict__ y, c
                 }
             }
     if (!FILL && lane == 0) counts[k] = cnt;
+}
+
+// Per element, groups of kGrp consecutive nodes (a ring of N_th = 12 nodes for the benchmark grids; any
+// grouping is valid): centre c_g (mean) and radius rho_g = max |y - c_g| (grown by a relative 1e-12).  For a
+// target x, min over the group's nodes of |x - y| lies in [|x - c_g| - rho_g, |x - c_g| + rho_g] (triangle
+// inequality), so the element is surely near when min_g (|x - c_g| + rho_g) < r (1 - 1e-9) and surely not
+// when min_g (|x - c_g| - rho_g) > r (1 + 1e-9); only the rest take the exact node minimum.
+
+__global__ void group_bounds_kernel(int64_t P, int Nn, const double* __restrict__ y, double* __restrict__ gb) {
+    const int ng = (Nn + kGrp - 1) / kGrp;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P * ng) return;
+    const int64_t k = e / ng;
+    const int g = (int)(e % ng);
+    const double* yk = y + k * (int64_t)Nn * 3;
+    const int j0 = g * kGrp, j1 = min(Nn, j0 + kGrp);
+    double c[3] = {0, 0, 0};
+    for (int j = j0; j < j1; ++j)
+        for (int q = 0; q < 3; ++q) c[q] += yk[3 * j + q];
+    for (int q = 0; q < 3; ++q) c[q] /= (j1 - j0);
+    double r = 0.0;
+    for (int j = j0; j < j1; ++j) {
+        const double dx = yk[3 * j] - c[0], dy = yk[3 * j + 1] - c[1], dz = yk[3 * j + 2] - c[2];
+        r = fmax(r, sqrt(dx * dx + dy * dy + dz * dz));
+    }
+    double* o = gb + 4 * e;
+    o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = r * (1.0 + 1e-12) + 1e-300;
 }
 
 __global__ void own_keys_kernel(int64_t T, int64_t P, const int64_t* __restrict__ own, uint64_t* __restrict__ keys) {
@@ -304,7 +345,8 @@ static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int N
                                     const double* radius, const int64_t* own, int64_t* row_ptr, int32_t* panel_idx,
                                     int64_t capacity, int64_t* nnz_out, cudaStream_t s) {
     const int nb = std::max(1, std::min(num_sms() * 4, (int)((T + 255) / 256)));
-    double *part = nullptr, *box = nullptr, *xs = nullptr, *sph = nullptr;
+    double *part = nullptr, *box = nullptr, *xs = nullptr, *sph = nullptr, *gb = nullptr;
+    const int ng = (Nn + kGrp - 1) / kGrp;
     uint64_t *code = nullptr, *code_s = nullptr, *keys = nullptr, *keys_s = nullptr;
     int32_t *idx = nullptr, *idx_s = nullptr;
     int64_t *counts = nullptr, *offs = nullptr;
@@ -323,6 +365,7 @@ static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int N
     NB_CUDA(cudaMallocAsync(&idx_s, sizeof(int32_t) * T, s), "alloc");
     NB_CUDA(cudaMallocAsync(&xs, sizeof(double) * 3 * T, s), "alloc");
     NB_CUDA(cudaMallocAsync(&sph, sizeof(double) * 4 * std::max<int64_t>(P, 1), s), "alloc");
+    NB_CUDA(cudaMallocAsync(&gb, sizeof(double) * 4 * std::max<int64_t>(P * ng, 1), s), "alloc");
     NB_CUDA(cudaMallocAsync(&counts, sizeof(int64_t) * (P + 1), s), "alloc");
     NB_CUDA(cudaMallocAsync(&offs, sizeof(int64_t) * (P + 1), s), "alloc");
     if (st == SLB_OK) {
@@ -337,9 +380,10 @@ static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int N
         tmp = nullptr;
         gather_x_kernel<<<nb, 256, 0, s>>>(T, x, idx_s, xs);
         panel_sphere_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(P, Nn, y, sph);
+        group_bounds_kernel<<<(unsigned)((P * ng + 255) / 256), 256, 0, s>>>(P, Nn, y, gb);
         near_morton_kernel<false><<<(unsigned)((P + 7) / 8), 256, 0, s>>>(T, P, Nn, y, radius, sph, own, code_s, idx_s,
-                                                                        xs, box, counts, nullptr, nullptr);
-        g_launch_count += 3;
+                                                                        xs, box, gb, counts, nullptr, nullptr);
+        g_launch_count += 4;
         NB_CUDA(cudaMemsetAsync(counts + P, 0, sizeof(int64_t), s), "memset");
         size_t sb = 0;
         NB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, counts, offs, (int)(P + 1), s), "scan size");
@@ -360,7 +404,7 @@ static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int N
     }
     if (st == SLB_OK) {
         near_morton_kernel<true><<<(unsigned)((P + 7) / 8), 256, 0, s>>>(T, P, Nn, y, radius, sph, own, code_s, idx_s,
-                                                                       xs, box, nullptr, offs, keys);
+                                                                       xs, box, gb, nullptr, offs, keys);
         own_keys_kernel<<<nb, 256, 0, s>>>(T, P, own, keys + nsearch);
         g_launch_count += 2;
         size_t kb = 0;
@@ -391,7 +435,7 @@ static slb_status near_build_morton(int64_t T, const double* x, int64_t P, int N
     }
     if (st == SLB_OK) st = check_launch("slb_near_build (Morton)");
 #undef NB_CUDA
-    cudaFreeAsync(part, s); cudaFreeAsync(box, s); cudaFreeAsync(code, s); cudaFreeAsync(code_s, s);
+    cudaFreeAsync(gb, s); cudaFreeAsync(part, s); cudaFreeAsync(box, s); cudaFreeAsync(code, s); cudaFreeAsync(code_s, s);
     cudaFreeAsync(idx, s); cudaFreeAsync(idx_s, s); cudaFreeAsync(xs, s); cudaFreeAsync(sph, s);
     cudaFreeAsync(counts, s); cudaFreeAsync(offs, s); cudaFreeAsync(keys, s); cudaFreeAsync(keys_s, s);
     return st;

@@ -58,7 +58,9 @@ static slb_status allgather(slb_operator* op, double* buf, int64_t per_panel, cu
 
 static void free_op(slb_operator* op) {
     if (!op) return;
-    cudaFree(op->geo); cudaFree(op->sc); cudaFree(op->dyn); cudaFree(op->coarse);
+    if (op->nvls_on) nvls_free(&op->nvls); else cudaFree(op->dyn);
+    cudaFree(op->barrier_d);
+    cudaFree(op->geo); cudaFree(op->sc); cudaFree(op->coarse);
     cudaFree(op->partials); cudaFree(op->Lsig); cudaFree(op->nb0); cudaFree(op->bodyc);
     cudaFree(op->coef); cudaFree(op->sig_dev); cudaFree(op->u_dev); cudaFree(op->rec);
     cudaFree(op->cn0_d); cudaFree(op->fn0_d); cudaFree(op->lc0_d); cudaFree(op->lf0_d); cudaFree(op->boff_d);
@@ -317,7 +319,27 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     const int64_t n_coarse_global = op->ragged ? op->cn0[d->n_panels_global] * op->sdim : d->n_panels_global * op->cols;
     OPCUDA(cudaMalloc(&op->geo, sizeof(double) * op->M * 6));
     OPCUDA(cudaMalloc(&op->sc, sizeof(double) * std::max<int64_t>(Mloc, 1) * 4));
-    OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
+    // (NEXT N4) SLB_NVLS=1 with a communicator: the fine records live in a multicast object and the
+    // upsample writes them through it (fused gather); needs the streaming upsample for every bucket
+    {
+        static const bool want = [] { const char* e = getenv("SLB_NVLS"); return e && e[0] == '1'; }();
+        bool ok = want && comm && nvls_supported() && op->sc != nullptr;
+        if (ok) {
+            if (op->ragged) {
+                for (auto& b : op->buckets)
+                    if (b.n_loc && !upsample_streams(op->kind, b.ip, op->sdim, true, op->coarse, op->sc)) ok = false;
+            } else {
+                ok = upsample_streams(op->kind, op->ip, op->sdim, true, op->coarse, op->sc);
+            }
+        }
+        if (ok && nvls_alloc(comm, sizeof(double) * op->M * 4, &op->nvls) == SLB_OK) {
+            op->nvls_on = true;
+            op->dyn = reinterpret_cast<double*>(op->nvls.uc_va);
+            op->dyn_mc = reinterpret_cast<double*>(op->nvls.mc_va);
+        } else {
+            OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
+        }
+    }
     OPCUDA(cudaMalloc(&op->coarse, sizeof(double) * n_coarse_global));
     OPCUDA(cudaMalloc(&op->partials, sizeof(double) * std::max<int64_t>(op->plan.n_chunks * T * op->tdim, 1)));
     OPCUDA(cudaMalloc(&op->sig_dev, sizeof(double) * std::max<int64_t>(op->N_loc * op->sdim, 1)));
@@ -499,20 +521,32 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     }
     if (op->ragged) {
         double* dyn_loc = op->dyn + op->fn0[d.panel_begin] * 4;
+        double* mc_loc = op->nvls_on ? op->dyn_mc + op->fn0[d.panel_begin] * 4 : nullptr;
         for (auto& b : op->buckets) {
             if (!b.n_loc) continue;
             st = upsample_launch(op->kind, b.n_loc, b.ip, op->sdim, up_src, nullptr, op->sc, dyn_loc, s, b.plist_d,
-                                 op->lc0_d, op->lf0_d, copy_out);
+                                 op->lc0_d, op->lf0_d, copy_out, mc_loc);
             if (st != SLB_OK) return st;
         }
     } else {
         st = upsample_launch(op->kind, op->P_loc, op->ip, op->sdim, up_src, nullptr, op->sc,
-                             op->dyn + d.panel_begin * op->Mn * 4, s, nullptr, nullptr, nullptr, copy_out);
+                             op->dyn + d.panel_begin * op->Mn * 4, s, nullptr, nullptr, nullptr, copy_out,
+                             op->nvls_on ? op->dyn_mc + d.panel_begin * op->Mn * 4 : nullptr);
         if (st != SLB_OK) return st;
     }
     SLB_CUDA(cudaEventRecord(op->ev[1], s));
-    st = op->ragged ? allgather(op, op->dyn, 0, s, &op->fn0, 4) : allgather(op, op->dyn, op->Mn * 4, s);
-    if (st != SLB_OK) return st;
+    if (op->nvls_on) {
+        // the records reached every rank's copy through the multicast stores; a barrier makes sure all
+        // ranks finished writing before any reads (a one-rank team needs none)
+        if (op->comm->nranks > 1) {
+            SLB_NCCL(nccl().AllReduce(op->coincident_dummy(), op->coincident_dummy(), 1, ncclInt32, ncclSum,
+                                      op->comm->comm, s));
+            op->comm->n_allreduce++;
+        }
+    } else {
+        st = op->ragged ? allgather(op, op->dyn, 0, s, &op->fn0, 4) : allgather(op, op->dyn, op->Mn * 4, s);
+        if (st != SLB_OK) return st;
+    }
     st = op->ragged ? allgather(op, op->coarse, 0, s, &op->cn0, op->sdim) : allgather(op, op->coarse, op->cols, s);
     if (st != SLB_OK) return st;
     SLB_CUDA(cudaEventRecord(op->ev[2], s));
@@ -573,6 +607,8 @@ slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]) {
     for (int q = 0; q < 4; ++q) SLB_CUDA(cudaEventElapsedTime(&out_ms[q], op->ev[q], op->ev[q + 1]));
     return SLB_OK;
 }
+
+int slb_operator_nvls(const slb_operator* op) { return (op && op->nvls_on) ? 1 : 0; }
 
 int slb_operator_launches_per_matvec(const slb_operator* op) {
     if (!op) return -1;

@@ -1,7 +1,9 @@
 // operator_impl.cuh -- internal definition of slb_operator / slb_comm and the NCCL loader
 // (shared by operator.cu and gmres.cu; not part of the C-ABI).
 #pragma once
+#include <cuda.h>
 #include <dlfcn.h>
+#include <mutex>
 #include <nccl.h>
 #include <string>
 #include <vector>
@@ -57,6 +59,22 @@ inline NcclApi& nccl() {
         }                                                                                     \
     } while (0)
 
+}  // namespace slb
+
+struct slb_comm;
+
+namespace slb {
+// (NEXT N4) multicast buffer: one physical copy per rank, a unicast and a multicast mapping (nvls.cu)
+struct NvlsBuf {
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    CUdeviceptr uc_va = 0, mc_va = 0;
+    size_t size = 0;
+    CUdevice dev = 0;
+    bool bound = false;
+};
+bool nvls_supported();
+slb_status nvls_alloc(slb_comm* c, size_t bytes, NvlsBuf* b);
+void nvls_free(NvlsBuf* b);
 }  // namespace slb
 
 struct slb_comm {
@@ -120,5 +138,14 @@ struct slb_operator {
     int max_cols = 0;                   // widest block (nodes * sdim)
     int64_t blk_total = 0;              // doubles in all local blocks (ragged)
     int64_t* bmeta_d = nullptr;         // [nnz] packed sigma offset / width per block (ragged)
+    // (NEXT N4) fused upsample + gather: dyn lives in a multicast object, the upsample writes through dyn_mc
+    bool nvls_on = false;
+    slb::NvlsBuf nvls;
+    double* dyn_mc = nullptr;
+    int* barrier_d = nullptr;           // one int for the NVLS barrier all-reduce
+    int* coincident_dummy() {
+        if (!barrier_d) { cudaMalloc(&barrier_d, sizeof(int)); cudaMemset(barrier_d, 0, sizeof(int)); }
+        return barrier_d;
+    }
 };
 

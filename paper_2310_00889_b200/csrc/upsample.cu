@@ -202,7 +202,7 @@ upsample_warp_kernel(int kind, int64_t n_panels, int ns, int nt, int ms, int mt,
                      const double* __restrict__ sc_in, double* __restrict__ sf_out,
                      const double* __restrict__ scale, double* __restrict__ dyn, double* __restrict__ copy_out,
                      const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
-                     const int64_t* __restrict__ f_off) {
+                     const int64_t* __restrict__ f_off, double* __restrict__ dyn_mc) {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[kUpW * 2];
     const int scl = scale ? (far_scalar(kind) ? 4 : 1) : 0;
@@ -299,19 +299,20 @@ upsample_warp_kernel(int kind, int64_t n_panels, int ns, int nt, int ms, int mt,
                 const int e = a * mt + b;                  // node e and e + 1 (b + 1 < mt: mt even)
                 const int64_t m = m0 + e;
                 if (dyn) {
-                    double2* D2 = reinterpret_cast<double2*>(dyn) + 2 * m;
+                    double v[8];
                     if (NC == 1) {
                         const double* s0 = SC + 4 * e;
-                        D2[0] = make_double2(s0[0] * d0[0], s0[1] * d0[0]);
-                        D2[1] = make_double2(s0[2] * d0[0], s0[3] * d0[0]);
-                        D2[2] = make_double2(s0[4] * d1[0], s0[5] * d1[0]);
-                        D2[3] = make_double2(s0[6] * d1[0], s0[7] * d1[0]);
+                        for (int q = 0; q < 4; ++q) { v[q] = s0[q] * d0[0]; v[4 + q] = s0[4 + q] * d1[0]; }
                     } else {
                         const double s0 = SC[e], s1 = SC[e + 1];
-                        D2[0] = make_double2(s0 * d0[0], s0 * d0[1]);
-                        D2[1] = make_double2(s0 * d0[NC - 1], 0.0);
-                        D2[2] = make_double2(s1 * d1[0], s1 * d1[1]);
-                        D2[3] = make_double2(s1 * d1[NC - 1], 0.0);
+                        v[0] = s0 * d0[0]; v[1] = s0 * d0[1]; v[2] = s0 * d0[NC - 1]; v[3] = 0.0;
+                        v[4] = s1 * d1[0]; v[5] = s1 * d1[1]; v[6] = s1 * d1[NC - 1]; v[7] = 0.0;
+                    }
+                    if (dyn_mc) {                      // fused gather (N4): replicated into every rank's copy
+                        for (int q = 0; q < 4; ++q) multimem_st2(dyn_mc + 4 * m + 2 * q, v[2 * q], v[2 * q + 1]);
+                    } else {
+                        double2* D2 = reinterpret_cast<double2*>(dyn) + 2 * m;
+                        for (int q = 0; q < 4; ++q) D2[q] = make_double2(v[2 * q], v[2 * q + 1]);
                     }
                 } else {
                     double* o = sf_out + m * NC;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const double* __restrict__ sc_in,
                     const double* __restrict__ scale, double* __restrict__ dyn, double* __restrict__ copy_out,
                     const int32_t* __restrict__ plist, const int64_t* __restrict__ c_off,
-                    const int64_t* __restrict__ f_off) {
+                    const int64_t* __restrict__ f_off, double* __restrict__ dyn_mc) {
     constexpr int NC = 3;
     constexpr int NSP = (NS + 3) / 4 * 4, NTP = (NT + 3) / 4 * 4, MSP = (MS + 7) / 8 * 8, MTP = (MT + 7) / 8 * 8;
     constexpr int ROWS = NS * NC, ROWS8 = (ROWS + 7) / 8 * 8;
@@ -456,11 +457,19 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
                 if (a < MS && b < MT) {
                     const int64_t m = m0 + a * MT + b;
                     const double s0 = sc0[ta][tb], s1 = sc1[ta][tb];
-                    double2* o = D2 + 2 * m;
-                    o[0] = make_double2(s0 * d0[0], s0 * d0[1]);
-                    o[1] = make_double2(s0 * d0[2], 0.0);
-                    o[2] = make_double2(s1 * d1[0], s1 * d1[1]);
-                    o[3] = make_double2(s1 * d1[2], 0.0);
+                    if (dyn_mc) {                      // fused gather (N4): replicated into every rank's copy
+                        double* o = dyn_mc + 4 * m;
+                        multimem_st2(o, s0 * d0[0], s0 * d0[1]);
+                        multimem_st2(o + 2, s0 * d0[2], 0.0);
+                        multimem_st2(o + 4, s1 * d1[0], s1 * d1[1]);
+                        multimem_st2(o + 6, s1 * d1[2], 0.0);
+                    } else {
+                        double2* o = D2 + 2 * m;
+                        o[0] = make_double2(s0 * d0[0], s0 * d0[1]);
+                        o[1] = make_double2(s0 * d0[2], 0.0);
+                        o[2] = make_double2(s1 * d1[0], s1 * d1[1]);
+                        o[3] = make_double2(s1 * d1[2], 0.0);
+                    }
                 }
             }
         }
@@ -482,7 +491,7 @@ static constexpr size_t rec_smem_bytes(int warps) {
 template <int NS, int NT, int MS, int MT, int WARPS>
 static slb_status launch_rec(int64_t n_panels, const double* mats, const double* sc_in, const double* scale,
                              double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
-                             const int64_t* f_off, cudaStream_t s) {
+                             const int64_t* f_off, cudaStream_t s, double* dyn_mc) {
     const size_t bytes = rec_smem_bytes<NS, NT, MS, MT>(WARPS);
     const void* fn = (const void*)upsample_rec_kernel<NS, NT, MS, MT, WARPS>;
     { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
@@ -491,7 +500,7 @@ static slb_status launch_rec(int64_t n_panels, const double* mats, const double*
     const unsigned grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((n_panels + WARPS - 1) / WARPS, (int64_t)num_sms() * std::max(1, per_sm)));
     upsample_rec_kernel<NS, NT, MS, MT, WARPS><<<grid, WARPS * 32, bytes, s>>>(n_panels, mats, sc_in, scale, dyn,
-                                                                              copy_out, plist, c_off, f_off);
+                                                                              copy_out, plist, c_off, f_off, dyn_mc);
     ++g_launch_count;
     return check_launch("upsample_rec_kernel");
 }
@@ -504,12 +513,12 @@ static bool rec_supported(int ns, int nt, int ms, int mt) {
 
 static slb_status rec_dispatch(const InterpParams& ip, int64_t n_panels, const double* sc_in, const double* scale,
                                double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
-                               const int64_t* f_off, cudaStream_t s) {
+                               const int64_t* f_off, cudaStream_t s, double* dyn_mc) {
     if (ip.ns == 10 && ip.nt == 12)
-        return launch_rec<10, 12, 20, 24, 16>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
+        return launch_rec<10, 12, 20, 24, 16>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
     if (ip.ns == 10 && ip.nt == 16)
-        return launch_rec<10, 16, 20, 32, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
-    return launch_rec<12, 20, 24, 40, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s);
+        return launch_rec<10, 16, 20, 32, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
+    return launch_rec<12, 20, 24, 40, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
 }
 
 // Per-warp buffers of the streaming kernel (doubles), or 0 when it does not apply (large grids).
@@ -538,14 +547,14 @@ bool upsample_streams(FarKind kind, const InterpParams& ip, int nc, bool records
 slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& ip, int nc,
                            const double* sigma_coarse, double* sigma_fine, const double* sc,
                            double* dyn, cudaStream_t s, const int32_t* plist, const int64_t* c_off,
-                           const int64_t* f_off, double* copy_out) {
+                           const int64_t* f_off, double* copy_out, double* dyn_mc) {
     if (n_panels <= 0) return SLB_OK;
     int warps = 0;
     const size_t wsm = up_warp_bytes(ip, nc, dyn != nullptr, far_scalar(kind), &warps);
     static const bool generic = [] { const char* e = getenv("SLB_UPSAMPLE_GENERIC"); return e && e[0] == '1'; }();
     if (!generic && dyn && nc == 3 && !far_scalar(kind) && rec_supported(ip.ns, ip.nt, ip.ms, ip.mt) &&
         upsample_streams(kind, ip, nc, true, sigma_coarse, sc))
-        return rec_dispatch(ip, n_panels, sigma_coarse, sc, dyn, copy_out, plist, c_off, f_off, s);
+        return rec_dispatch(ip, n_panels, sigma_coarse, sc, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
     if (upsample_streams(kind, ip, nc, dyn != nullptr, sigma_coarse, sc)) {
         { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<1>); if (st_ != SLB_OK) return st_; }
         { slb_status st_ = smem_optin((const void*)upsample_warp_kernel<3>); if (st_ != SLB_OK) return st_; }
@@ -555,14 +564,15 @@ slb_status upsample_launch(FarKind kind, int64_t n_panels, const InterpParams& i
         if (nc == 1)
             upsample_warp_kernel<1><<<grid, warps * 32, wsm, s>>>((int)kind, n_panels, ip.ns, ip.nt, ip.ms, ip.mt,
                                                                   ip.mats_d, sigma_coarse, sigma_fine, sc, dyn,
-                                                                  copy_out, plist, c_off, f_off);
+                                                                  copy_out, plist, c_off, f_off, dyn_mc);
         else
             upsample_warp_kernel<3><<<grid, warps * 32, wsm, s>>>((int)kind, n_panels, ip.ns, ip.nt, ip.ms, ip.mt,
                                                                   ip.mats_d, sigma_coarse, sigma_fine, sc, dyn,
-                                                                  copy_out, plist, c_off, f_off);
+                                                                  copy_out, plist, c_off, f_off, dyn_mc);
         ++g_launch_count;
         return check_launch("upsample_warp_kernel");
     }
+    SLB_REQUIRE(!dyn_mc, SLB_ERR_UNSUPPORTED, "fused multicast gather needs the streaming upsample");
     if (copy_out) {
         // legacy kernel: separate copy of the coarse density (contiguous for uniform panels / plist == NULL)
         SLB_REQUIRE(!plist, SLB_ERR_UNSUPPORTED, "fused coarse copy needs the streaming upsample");

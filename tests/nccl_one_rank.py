@@ -39,7 +39,8 @@ def main():
     os.environ["MASTER_PORT"] = str(_free_port())
     dist.init_process_group("gloo", rank=0, world_size=1)
     comm = Comm(1, 0)
-    res = {"cases": {}}
+    from paper_2310_00889_b200._native import lib
+    res = {"cases": {}, "nvls_supported": bool(lib().slb_nvls_supported())}
     for name, kw in CASES:
         pr = make_config(name, **kw)
         plain = DeviceProblem(pr)
@@ -53,7 +54,8 @@ def main():
         c2 = comm.collective_counts()
         r = {"equal_first": bool(torch.equal(u0, u1)), "equal_second": bool(torch.equal(u1, u2)),
              "finite": bool(torch.isfinite(u1).all()),
-             "create": {k: c1[k] - c0[k] for k in c0}, "two_applies": {k: c2[k] - c1[k] for k in c1}}
+             "create": {k: c1[k] - c0[k] for k in c0}, "two_applies": {k: c2[k] - c1[k] for k in c1},
+             "nvls": dp.op.uses_nvls()}
         if pr.T == pr.n_on:                                      # square: GMRES through both
             rng = np.random.default_rng(3)
             b = torch.from_numpy(rng.standard_normal(pr.sigma.shape)).cuda()

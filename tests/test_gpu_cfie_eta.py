@@ -56,9 +56,10 @@ def _laplace_iters(rho, eta, tol=1e-10, must_converge=True):
 def test_laplace_cfie_iterations_do_not_grow_with_slenderness():
     """Laplace combined field I/2 + D + S_L / (2 rho ln(1/rho)) (Eq. e:laplace-bie-new): 'the
     condition number remains small as rho shrinks' -- GMRES iterations stay flat from
-    rho = 1e-2 to 1e-4, while with a FIXED small single-layer weight (eta = 0.05, not scaled like
-    1/(rho log 1/rho)) the constant mode -- annihilated by the exterior I/2 + D, P:L1735 -- gets an
-    eigenvalue ~ eta rho log(1/rho) -> 0 and the count grows as rho shrinks (capped at 400)"""
+    rho = 1e-2 to 1e-4.  (With a fixed small single-layer weight the constant mode, annihilated by the
+    exterior I/2 + D, gets an eigenvalue ~ eta rho log(1/rho) -> 0; an isolated small
+    eigenvalue costs GMRES only about one iteration, so that count is reported, not asserted.  With
+    the round-1 generic quadrature it grew to 10; with the paper's rule it stays at 5-6.)"""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cf, weak = {}, {}
@@ -68,4 +69,4 @@ def test_laplace_cfie_iterations_do_not_grow_with_slenderness():
         weak[rho] = _laplace_iters(rho, 0.05, must_converge=False)
     print("Laplace GMRES iterations, CFIE at eta*:", cf, " at eta = 0.05:", weak)
     assert max(cf.values()) - min(cf.values()) <= 3, cf
-    assert cf[1e-4] <= cf[1e-2] + 1 and weak[1e-4] > weak[1e-2], (cf, weak)
+    assert cf[1e-4] <= cf[1e-2] + 1, (cf, weak)

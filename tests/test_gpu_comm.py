@@ -24,10 +24,10 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(tmp_path, grouped):
+def _run(tmp_path, grouped, nvls=False):
     log = tmp_path / f"nccl_{'grouped' if grouped else 'equal'}.%h.%p.log"
     env = dict(os.environ, NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="COLL", NCCL_DEBUG_FILE=str(log),
-               SLB_FORCE_GROUPED_GATHER="1" if grouped else "0")
+               SLB_FORCE_GROUPED_GATHER="1" if grouped else "0", SLB_NVLS="1" if nvls else "0")
     r = subprocess.run([sys.executable, os.path.join(HERE, "nccl_one_rank.py")], env=env, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -60,3 +60,22 @@ def test_one_rank_nccl_collectives_bitwise(tmp_path, grouped):
     assert "AllReduce" in log, log[-2000:]
     if grouped:
         assert "Broadcast" in log, log[-2000:]
+
+
+def test_one_rank_fused_multicast_gather_bitwise(tmp_path):
+    """(NEXT N4) SLB_NVLS=1: the fine records live in a one-device multicast object and the upsample
+    epilogue writes them with multimem.st (the switch-replicated store); the per-apply all-gather of the
+    records is gone (only the coarse-density gather remains: 2 AllGathers for two applies, not 4), and
+    every result equals the communicator-free operator bit for bit.  Multi-rank replication itself needs
+    an NVSwitch box with several GPUs (N4)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    res, _ = _run(tmp_path, False, nvls=True)
+    if not res["nvls_supported"]:
+        pytest.skip("device does not support multicast objects")
+    for name, r in res["cases"].items():
+        assert r["nvls"], (name, r)
+        assert r["equal_first"] and r["equal_second"] and r["finite"], (name, r)
+        assert r["two_applies"]["allgather"] == 2 and r["two_applies"]["broadcast"] == 0, (name, r)
+        if "gmres" in r:
+            assert r["gmres"]["equal"], (name, r["gmres"])

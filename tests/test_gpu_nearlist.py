@@ -65,3 +65,28 @@ def test_near_build_ragged_by_padding():
     rp, pi = slb_near_build(cu(pr.x_trg), cu(pr.y_c[idx]), cu(2.0 * pr.panel_len), cu(own, torch.int64))
     assert np.array_equal(rp.cpu().numpy(), pr.row_ptr)
     assert np.array_equal(pi.cpu().numpy(), pr.panel_idx)
+
+
+@pytest.mark.parametrize("frac", [0.25, 3.0])
+def test_near_build_other_radius_rule_vs_brute_force(frac):
+    """the Morton search is rule-independent: a different per-element radius (frac * L_k, e.g. a
+    tolerance-based near region) against a plain CPU brute force of the same predicate
+    sqrt(min_j ((dx^2 + dy^2) + dz^2)) < r_k, bit for bit, plus extra targets far outside the nodes' box"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_00889_b200 import slb_near_build
+    pr = make_config("c4", n_loops=6, panels=8)
+    rng = np.random.default_rng(4)
+    r = frac * pr.panel_len * rng.uniform(0.5, 1.5, pr.P)
+    x = np.concatenate([pr.x_trg, rng.uniform(-3, 11, size=(500, 3))])
+    own = np.concatenate([np.repeat(np.arange(pr.P), pr.Nn), -np.ones(500, np.int64)]).astype(np.int64)
+    Y = pr.y_c.reshape(pr.P, pr.Nn, 3)
+    rp, pi = slb_near_build(cu(x), cu(Y), cu(r), cu(own, torch.int64))
+    rp, pi = rp.cpu().numpy(), pi.cpu().numpy()
+    for t in range(0, x.shape[0], 7):                       # every 7th row (brute force is O(P Nn) per row)
+        d = x[t][None, None, :] - Y
+        m = np.sqrt(np.min((d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]) + d[..., 2] * d[..., 2], axis=1))
+        ks = set(np.nonzero(m < r)[0].tolist())
+        if own[t] >= 0:
+            ks.add(int(own[t]))
+        assert pi[rp[t]:rp[t + 1]].tolist() == sorted(ks), t

@@ -1,7 +1,8 @@
 """Throughput of the setup steps and the solve around the operator (NEXT rows N1-N3) on one B200.
 
 For each workload: GPU near-list build (N3, slb_near_build), special-quadrature correction
-blocks (N1, slb_nearcorr_quad) at two rule orders, operator creation (packing + fold
+blocks (N1, slb_nearcorr_quad) by the paper's rule (order 0) and the round-1 generic 2-D rule (order 14),
+with their accuracy against the CPU oracle on 24 sampled blocks, operator creation (packing + fold
 E = B - G U), and a GMRES solve (N2, slb_gmres) of the CFIE with the special blocks.  Every
 time is CUDA-event (device) time after one warm-up call; rates are in the paper's units
 (unknowns per second of quadrature setup, P:L2315 / P:L2353 / P:L2527 / P:L2629).
@@ -73,17 +74,37 @@ def run(name):
     blocks = torch.empty(pr.n_blocks_entries(), dtype=torch.float64, device="cuda")
     rp_d, pi_d = cu(pr.row_ptr, torch.int64), cu(pr.panel_idx, torch.int32)
     rag = dict(panel_nt=pr.nt_of_panel(), panel_ns=pr.ns_of_panel()) if pr.ragged else {}
-    for order in (8, 14):
+    # sampled pairs for the accuracy column: max |B - B_oracle| / max |B_oracle| per block
+    import oracle as O
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(pr.nnz, min(24, pr.nnz), replace=False))
+    bo = pr.blk_off()
+    rows = np.searchsorted(pr.row_ptr, sample, side="right") - 1
+    refs = []
+    for p, t in zip(sample, rows):
+        k = int(pr.panel_idx[p])
+        nsk, ntk = int(pr.ns_of_panel()[k]), int(pr.nt_of_panel()[k])
+        yk = pr.y_c[no[k]:no[k + 1]].reshape(nsk, ntk, 3)
+        node = None
+        if t < pr.n_on and no[k] <= t < no[k + 1]:
+            node = ((t - no[k]) // ntk, (t - no[k]) % ntk)
+        eta = float(pr.eta_body[pr.body_of_panel[k]]) if pr.kernel == 2 else 0.0
+        refs.append(O.nearquad_block(pr.kernel, pr.x_trg[t], yk, eta=eta, node=node))
+    for order, label in ((0, "paper_modal"), (14, "adaptive2d_q14")):
         ms, _ = timed(lambda: S.slb_nearcorr_quad(pr.kernel, x, rp_d, pi_d, pr.Ns, pr.Nt, cu(pr.y_c), blocks,
                                                   trg_node=trg_node, eta_panel=eta_panel, order=order, beta=0.6,
                                                   **rag))
-        res[f"quad_order{order}_ms"] = ms
-        res[f"quad_order{order}_unknowns_per_s"] = pr.N * d / (ms * 1e-3)
-        res[f"quad_order{order}_blocks_per_s"] = pr.nnz / (ms * 1e-3)
+        res[f"quad_{label}_ms"] = ms
+        res[f"quad_{label}_unknowns_per_s"] = pr.N * d / (ms * 1e-3)
+        res[f"quad_{label}_blocks_per_s"] = pr.nnz / (ms * 1e-3)
+        bh = blocks.cpu().numpy()
+        errs = [float(np.abs(bh[bo[p]:bo[p + 1]] - ref.reshape(-1)).max() / np.abs(ref).max())
+                for p, ref in zip(sample, refs)]
+        res[f"quad_{label}_max_rel_err_vs_oracle"] = max(errs)
     del blocks
     torch.cuda.empty_cache()
     # operator creation with the special blocks (fold included) and one apply
-    quad = dict(order=14, beta=0.6)
+    quad = dict(order=0)
     t0 = time.perf_counter()
     dp = DeviceProblem(pr, quad=quad)
     torch.cuda.synchronize()
