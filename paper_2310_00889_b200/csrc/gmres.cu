@@ -144,7 +144,7 @@ extern "C" slb_status slb_gmres(slb_operator* op, const double* rhs, double* x, 
     }
     while (true) {
         // r = b - A x  into V_0
-        GM(slb_matvec(op, x, w, s));
+        GM(matvec_direct(op, x, w, s));
         GM(g.axpby(1.0, rhs, -1.0, w, V));
         double rr;
         GM(g.dots(1, V, ld, V, &rr));
@@ -156,7 +156,7 @@ extern "C" slb_status slb_gmres(slb_operator* op, const double* rhs, double* x, 
         gv[0] = beta;
         int j = 0;
         for (; j < m && it < max_iters; ++j, ++it) {
-            GM(slb_matvec(op, V + (int64_t)j * ld, w, s));
+            GM(matvec_direct(op, V + (int64_t)j * ld, w, s));
             // CGS2
             GM(g.dots(j + 1, V, ld, w, h.data()));
             GM(g.update(j + 1, V, ld, h.data(), -1.0, w));

@@ -10,6 +10,7 @@
 //                                                                              P:L1750/1868/2009)
 // NCCL is loaded at run time (dlopen "libnccl.so.2": the copy torch already loaded is reused).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -67,6 +68,8 @@ static void free_op(slb_operator* op) {
     cudaFree(op->pbucket_d); cudaFree(op->bmeta_d);
     for (auto& b : op->buckets) { cudaFree(b.plist_d); cudaFree(b.ip_buf); }
     cudaFree(op->ip_buf);
+    for (auto& g : op->apply_graphs) cudaGraphExecDestroy(g.exec);
+    if (op->cap_stream) cudaStreamDestroy(op->cap_stream);
     for (auto& e : op->ev) if (e) cudaEventDestroy(e);
     if (op->graph) cudaGraphExecDestroy(op->graph);
     for (auto& w : op->ws) if (w) cudaStreamDestroy(w);
@@ -337,6 +340,9 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
             op->dyn = reinterpret_cast<double*>(op->nvls.uc_va);
             op->dyn_mc = reinterpret_cast<double*>(op->nvls.mc_va);
         } else {
+            if (want)          // requested explicitly: say why the NCCL all-gather path is used instead
+                fprintf(stderr, "slb: SLB_NVLS=1 but the multicast gather is unavailable (%s)\n",
+                        !comm ? "no communicator" : !ok ? "device or upsample path unsupported" : slb_last_error());
             OPCUDA(cudaMalloc(&op->dyn, sizeof(double) * op->M * 4));
         }
     }
@@ -473,16 +479,21 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
     return SLB_OK;
 }
 
-slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s) {
-    SLB_REQUIRE(op, SLB_ERR_INVALID_ARG, "null operator");
-    SLB_REQUIRE((op->N_loc == 0 || sigma_local) && (op->d.n_trg_local == 0 || u_local), SLB_ERR_INVALID_ARG,
-                "null density/output");
-    SLB_REQUIRE(check_sticky("slb_matvec") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+}  // extern "C"
+
+// The apply itself.  captured: being recorded into the operator's whole-apply graph (the stage events
+// become event-record nodes; the constant-bank tiles are recorded inline and the bank lock is taken by
+// the caller around the graph launch).
+static slb_status matvec_body(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s,
+                              bool captured) {
     const slb_operator_desc& d = op->d;
+    auto rec_ev = [&](int q) {
+        return captured ? cudaEventRecordWithFlags(op->ev[q], s, cudaEventRecordExternal) : cudaEventRecord(op->ev[q], s);
+    };
     unsigned long long* zc = coincident_counter();
     SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
     slb_status st;
-    SLB_CUDA(cudaEventRecord(op->ev[0], s));
+    SLB_CUDA(rec_ev(0));
     // local sigma' inside the global coarse buffer.  One GPU without the projector: the caller's sigma IS
     // sigma' and the finalize reads it in place (no copy).  With a communicator the upsample writes the
     // staged density into the global buffer as it reads it (fused copy), the projector writes sigma' there.
@@ -534,7 +545,7 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
                              op->nvls_on ? op->dyn_mc + d.panel_begin * op->Mn * 4 : nullptr);
         if (st != SLB_OK) return st;
     }
-    SLB_CUDA(cudaEventRecord(op->ev[1], s));
+    SLB_CUDA(rec_ev(1));
     if (op->nvls_on) {
         // the records reached every rank's copy through the multicast stores; a barrier makes sure all
         // ranks finished writing before any reads (a one-rank team needs none)
@@ -549,30 +560,38 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     }
     st = op->ragged ? allgather(op, op->coarse, 0, s, &op->cn0, op->sdim) : allgather(op, op->coarse, op->cols, s);
     if (st != SLB_OK) return st;
-    SLB_CUDA(cudaEventRecord(op->ev[2], s));
+    SLB_CUDA(rec_ev(2));
     if (op->use_const) {
         st = pack_rec_launch(op->M, op->geo, op->dyn, op->rec, s);
         if (st != SLB_OK) return st;
-        ConstBankLock bank;                        // the __constant__ bank is one per device (slb.h)
-        st = bank.acquire(s);
-        if (st != SLB_OK) return st;
-        if (op->graph) {
-            SLB_CUDA(cudaGraphLaunch(op->graph, s));
-            g_launch_count += (unsigned long long)op->const_launches;
-        } else {
+        if (captured) {                            // tiles recorded inline; the caller holds the bank lock
             int64_t nl = 0;
             st = far_const_issue(op->kind, op->M, d.n_trg_local, d.x_trg, op->rec, op->partials, zc, s, op->ws,
                                  op->fork, op->join, &nl);
             if (st != SLB_OK) return st;
             g_launch_count += (unsigned long long)nl;
+        } else {
+            ConstBankLock bank;                    // the __constant__ bank is one per device (slb.h)
+            st = bank.acquire(s);
+            if (st != SLB_OK) return st;
+            if (op->graph) {
+                SLB_CUDA(cudaGraphLaunch(op->graph, s));
+                g_launch_count += (unsigned long long)op->const_launches;
+            } else {
+                int64_t nl = 0;
+                st = far_const_issue(op->kind, op->M, d.n_trg_local, d.x_trg, op->rec, op->partials, zc, s, op->ws,
+                                     op->fork, op->join, &nl);
+                if (st != SLB_OK) return st;
+                g_launch_count += (unsigned long long)nl;
+            }
+            st = bank.release(s);
+            if (st != SLB_OK) return st;
         }
-        st = bank.release(s);
-        if (st != SLB_OK) return st;
     } else {
         st = far_partials(op->kind, op->plan, d.n_trg_local, d.x_trg, op->geo, op->dyn, op->partials, zc, s);
         if (st != SLB_OK) return st;
     }
-    SLB_CUDA(cudaEventRecord(op->ev[3], s));
+    SLB_CUDA(rec_ev(3));
     RagNear rag;
     if (op->ragged) {
         rag.cn0 = op->cn0_d;
@@ -583,7 +602,76 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
     st = finalize_launch(op->plan, d.n_trg_local, op->tdim, (int)op->cols, op->partials, d.row_ptr, d.panel_idx,
                          d.blocks, near_sig, d.n_on_local, d.c_identity, id_sig, Lsig, u_local, op->near_G, s, rag);
     if (st != SLB_OK) return st;
-    SLB_CUDA(cudaEventRecord(op->ev[4], s));
+    SLB_CUDA(rec_ev(4));
+    op->timed = true;
+    return SLB_OK;
+}
+
+static bool apply_graphs_enabled(const slb_operator* op) {
+    static const bool on = [] { const char* e = getenv("SLB_APPLY_GRAPH"); return !(e && e[0] == '0'); }();
+    return on && (!op->comm || op->comm->nranks == 1);
+}
+
+namespace slb {
+slb_status matvec_direct(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s) {
+    return matvec_body(op, sigma_local, u_local, s, false);
+}
+}  // namespace slb
+
+extern "C" {
+
+// One apply.  The whole sequence (projector, upsample, gathers, far field, finalize, stage events) is
+// recorded once per (sigma, u) pointer pair into a CUDA graph (a small LRU per operator) and replayed,
+// so consecutive kernels run back to back without host launch gaps (single-rank operators; the first
+// call with a new pair runs directly and initialises everything lazily created).
+slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s) {
+    SLB_REQUIRE(op, SLB_ERR_INVALID_ARG, "null operator");
+    SLB_REQUIRE((op->N_loc == 0 || sigma_local) && (op->d.n_trg_local == 0 || u_local), SLB_ERR_INVALID_ARG,
+                "null density/output");
+    SLB_REQUIRE(check_sticky("slb_matvec") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    SLB_REQUIRE(coincident_counter(), SLB_ERR_CUDA, "coincident counter allocation failed");
+    if (!apply_graphs_enabled(op)) return matvec_body(op, sigma_local, u_local, s, false);
+    slb_operator::ApplyGraph* hit = nullptr;
+    for (auto& g : op->apply_graphs)
+        if (g.sigma == sigma_local && g.u == u_local) hit = &g;
+    if (!hit) {
+        if (!op->seen_direct) {
+            op->seen_direct = true;
+            return matvec_body(op, sigma_local, u_local, s, false);
+        }
+        if (!op->cap_stream) SLB_CUDA(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+        const unsigned long long c0 = g_launch_count.load();
+        cudaGraph_t g = nullptr;
+        SLB_CUDA(cudaStreamBeginCapture(op->cap_stream, cudaStreamCaptureModeThreadLocal));
+        slb_status st = matvec_body(op, sigma_local, u_local, op->cap_stream, true);
+        cudaError_t e = cudaStreamEndCapture(op->cap_stream, &g);
+        const unsigned long long nl = g_launch_count.load() - c0;
+        g_launch_count -= nl;                      // recorded, not launched
+        cudaGraphExec_t ex = nullptr;
+        if (st == SLB_OK && e == cudaSuccess && g) e = cudaGraphInstantiate(&ex, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (st != SLB_OK || e != cudaSuccess || !ex) {
+            cudaGetLastError();
+            return matvec_body(op, sigma_local, u_local, s, false);   // capture not possible: direct issue
+        }
+        if (op->apply_graphs.size() >= 4) {
+            cudaGraphExecDestroy(op->apply_graphs.front().exec);
+            op->apply_graphs.erase(op->apply_graphs.begin());
+        }
+        op->apply_graphs.push_back({sigma_local, u_local, ex, nl});
+        hit = &op->apply_graphs.back();
+    }
+    if (op->use_const) {
+        ConstBankLock bank;
+        slb_status st = bank.acquire(s);
+        if (st != SLB_OK) return st;
+        SLB_CUDA(cudaGraphLaunch(hit->exec, s));
+        st = bank.release(s);
+        if (st != SLB_OK) return st;
+    } else {
+        SLB_CUDA(cudaGraphLaunch(hit->exec, s));
+    }
+    g_launch_count += hit->launches;
     op->timed = true;
     return SLB_OK;
 }

@@ -75,6 +75,7 @@ struct NvlsBuf {
 bool nvls_supported();
 slb_status nvls_alloc(slb_comm* c, size_t bytes, NvlsBuf* b);
 void nvls_free(NvlsBuf* b);
+slb_status matvec_direct(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s);
 }  // namespace slb
 
 struct slb_comm {
@@ -142,6 +143,16 @@ struct slb_operator {
     bool nvls_on = false;
     slb::NvlsBuf nvls;
     double* dyn_mc = nullptr;
+    // whole-apply CUDA graphs keyed by the (sigma, u) pointers (slb_matvec)
+    struct ApplyGraph {
+        const double* sigma;
+        double* u;
+        cudaGraphExec_t exec;
+        unsigned long long launches;
+    };
+    std::vector<ApplyGraph> apply_graphs;
+    cudaStream_t cap_stream = nullptr;
+    bool seen_direct = false;
     int* barrier_d = nullptr;           // one int for the NVLS barrier all-reduce
     int* coincident_dummy() {
         if (!barrier_d) { cudaMalloc(&barrier_d, sizeof(int)); cudaMemset(barrier_d, 0, sizeof(int)); }

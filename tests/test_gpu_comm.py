@@ -33,6 +33,7 @@ def _run(tmp_path, grouped, nvls=False):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")][-1]
     res = json.loads(line[len("RESULT "):])
+    res["stderr"] = r.stderr[-2000:]
     text = "".join(p.read_text(errors="replace") for p in tmp_path.glob(f"nccl_{'grouped' if grouped else 'equal'}.*"))
     return res, text
 
@@ -74,7 +75,7 @@ def test_one_rank_fused_multicast_gather_bitwise(tmp_path):
     if not res["nvls_supported"]:
         pytest.skip("device does not support multicast objects")
     for name, r in res["cases"].items():
-        assert r["nvls"], (name, r)
+        assert r["nvls"], (name, r, res["stderr"])
         assert r["equal_first"] and r["equal_second"] and r["finite"], (name, r)
         assert r["two_applies"]["allgather"] == 2 and r["two_applies"]["broadcast"] == 0, (name, r)
         if "gmres" in r:
