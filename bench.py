@@ -299,9 +299,11 @@ def main():
     near_bytes = dp.n_entries * 8 + dp.nnz * 4 + T_loc * 8 * (pr.tdim + 2)
     n_loc_nodes = int(no[dp.pe] - no[dp.pb])
     m_loc = int(fo[dp.pe] - fo[dp.pb])
-    # upsample (+projector) algorithmic bytes: sigma read + sigma' write (+ L sigma), fine scale read, records written
-    up_bytes = (n_loc_nodes * pr.sdim * 8 * (2 + (2 if pr.projector else 0)) + m_loc * 8 * (3 if pr.kernel == 1 else 1)
-                + m_loc * 8 * 3)
+    # upsample (+projector) algorithmic bytes: the coarse density read once (+ the projector's second read
+    # and its sigma', L sigma writes), the fine-node scales read (1 double per node Stokes, 4 Laplace), the
+    # 32-byte source records written
+    up_bytes = (n_loc_nodes * pr.sdim * 8 * (1 + (3 if pr.projector else 0)) + m_loc * 8 * (4 if pr.kernel == 1 else 1)
+                + m_loc * 32)
     dfma = None
     if rank == 0:
         try:
@@ -346,7 +348,7 @@ def main():
             "roofline_near": {"bound": "hbm", "kernel": "finalize_kernel (near blocks + chunk reduce)",
                               "achieved": near_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": near_gbs / hbm_peak,
                               "bytes_per_launch": near_bytes, "launch_ms": fin_ms},
-            "roofline_upsample": {"bound": "hbm", "kernel": "upsample_dmma_kernel (+ projector, DMMA m8n8k4)",
+            "roofline_upsample": {"bound": "hbm", "kernel": "upsample_rec_kernel / upsample_warp_kernel (+ projector; DMMA m8n8k4, TMA-fed)",
                                   "achieved": up_bytes / (st_mean[0] * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                                   "frac": up_bytes / (st_mean[0] * 1e-3) / 1e9 / hbm_peak,
                                   "bytes_per_launch": up_bytes, "launch_ms": st_mean[0]},

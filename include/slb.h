@@ -269,7 +269,8 @@ slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]);
  * more ranks exchange the multicast handle as a fabric handle).  0: the NCCL all-gather path. */
 int slb_operator_nvls(const slb_operator* op);
 
-/* 1 if this device supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED). */
+/* 1 if this device supports multicast objects: CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED and a probe
+ * cuMulticastCreate succeeds (some single-GPU containers report the attribute but reject creation). */
 int slb_nvls_supported(void);
 
 /* Number of kernel launches slb_matvec issues on this rank (for launch accounting). */

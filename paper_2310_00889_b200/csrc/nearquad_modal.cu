@@ -261,7 +261,9 @@ __host__ __device__ inline Smem smem_layout(int ns, int nt, int W, int ldE, int 
     return S;
 }
 
-template <int KD>
+// KD: kernel dimension (1 Laplace, 3 Stokes); NCT: 8-column DMMA tiles of the modal sums (covers the
+// launch's largest N_th: 2 (N_th/2 + 1) columns), so the accumulators are sized per rule class.
+template <int KD, int NCT>
 __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ Args A, const __grid_constant__ Tables TB) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int64_t s_pair;
@@ -324,8 +326,9 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
         const double* tg = TB.tgl + ns * (ns - 1) / 2;
         const double* lam = TB.lam + ns * (ns - 1) / 2;
         const RuleSet& RS = TB.rs[class_of_nt(nt)];
-        const int ncol = 2 * (L + 1), nct = (ncol + 7) / 8;
-        const int nrt = S.rows / 8;
+        const int ncol = 2 * (L + 1), nct = (ncol + 7) / 8;     // <= NCT
+        constexpr int NRT = KD == 3 ? 2 : 1;                  // 8-row DMMA tiles (9 kernel components -> 16 rows)
+        const int nrt = NRT;
         // element nodes relative to the target; block accumulator
         for (int q = threadIdx.x; q < ns * nt; q += blockDim.x) {
             const double* yv = A.y + 3 * (n0 + q);
@@ -427,7 +430,9 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 if (sing) {
                     // dyadic towards s0 down to ~rho/4 (parameter units), log rule on the two touching panels;
                     // the singular sub-panels store the OFFSET from s0 (exact near s0)
-                    const double hl = 0.25 * rho / ytn;
+                    // log panel length: the s-structure of h_j near s0 lives on the scale rho / (N_th |y_s|)
+                    // (C_j oscillates N_th / 2 times), so the panel shrinks with N_th (0.25 rho / |y_t| at N_th = 12)
+                    const double hl = fmin(0.25, 3.0 / nt) * rho / ytn;
                     // left: offsets -(1 + s0) ... 0
                     {
                         double len = 1.0 + ts;
@@ -615,11 +620,11 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 const int roff = RS.off[rule], rcnt = RS.cnt[rule];
 
                 // DMMA accumulators: hhat[row][col], col = 2 l + (0: cos, 1: sin)
-                double acc[2][9][2];
+                double acc[NRT][NCT][2];
 #pragma unroll
-                for (int a2 = 0; a2 < 2; ++a2)
+                for (int a2 = 0; a2 < NRT; ++a2)
 #pragma unroll
-                    for (int c2 = 0; c2 < 9; ++c2) acc[a2][c2][0] = acc[a2][c2][1] = 0.0;
+                    for (int c2 = 0; c2 < NCT; ++c2) acc[a2][c2][0] = acc[a2][c2][1] = 0.0;
                 for (int c0 = 0; c0 < rcnt; c0 += kChunk) {
                     // node lane: geometry, kernel, modes
                     {
@@ -693,16 +698,15 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
 #pragma unroll
                     for (int k0 = 0; k0 < kChunk; k0 += 4) {
                         const int mrow = k0 + tq;
-                        double av[2];
+                        double av[NRT];
 #pragma unroll
-                        for (int rt = 0; rt < 2; ++rt) av[rt] = (rt < nrt) ? Vb[mrow * S.ldv + 8 * rt + g] : 0.0;
+                        for (int rt = 0; rt < NRT; ++rt) av[rt] = Vb[mrow * S.ldv + 8 * rt + g];
 #pragma unroll
-                        for (int ct = 0; ct < 9; ++ct) {
+                        for (int ct = 0; ct < NCT; ++ct) {
                             if (ct < nct) {
                                 const double bv = Eb[mrow * A.ld_e + 8 * ct + g];
 #pragma unroll
-                                for (int rt = 0; rt < 2; ++rt)
-                                    if (rt < nrt) dmma(acc[rt][ct][0], acc[rt][ct][1], av[rt], bv);
+                                for (int rt = 0; rt < NRT; ++rt) dmma(acc[rt][ct][0], acc[rt][ct][1], av[rt], bv);
                             }
                         }
                     }
@@ -710,10 +714,10 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 }
                 // stage hhat in Eb as [row][ld_e], then the inverse DFT h_j (Eq. e:modal-greens-fn-wts)
 #pragma unroll
-                for (int rt = 0; rt < 2; ++rt)
+                for (int rt = 0; rt < NRT; ++rt)
 #pragma unroll
-                    for (int ct = 0; ct < 9; ++ct)
-                        if (rt < nrt && ct < nct) {
+                    for (int ct = 0; ct < NCT; ++ct)
+                        if (ct < nct) {
                             Eb[(8 * rt + g) * A.ld_e + 8 * ct + 2 * tq] = acc[rt][ct][0];
                             Eb[(8 * rt + g) * A.ld_e + 8 * ct + 2 * tq + 1] = acc[rt][ct][1];
                         }
@@ -916,13 +920,21 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
     SLB_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
     a.work = work;
     a.status = reinterpret_cast<int*>(work + 1);
-    const void* fn = KD == 3 ? (const void*)nq_modal_kernel<3> : (const void*)nq_modal_kernel<1>;
+    const int nct_launch = (2 * (a.nt / 2 + 1) + 7) / 8;
+    const int NCTc = nct_launch <= 2 ? 2 : nct_launch <= 4 ? 4 : nct_launch <= 6 ? 6 : 9;
+    const void* fn;
+#define NQ_FN(K, C) (const void*)nq_modal_kernel<K, C>
+    if (KD == 3) fn = NCTc == 2 ? NQ_FN(3, 2) : NCTc == 4 ? NQ_FN(3, 4) : NCTc == 6 ? NQ_FN(3, 6) : NQ_FN(3, 9);
+    else fn = NCTc == 2 ? NQ_FN(1, 2) : NCTc == 4 ? NQ_FN(1, 4) : NCTc == 6 ? NQ_FN(1, 6) : NQ_FN(1, 9);
+#undef NQ_FN
     { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
     int per_sm = 0;
     SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, W * 32, bytes));
     const int64_t grid = std::min<int64_t>(nnz, (int64_t)num_sms() * std::max(1, per_sm));
-    if (KD == 3) nq_modal_kernel<3><<<(unsigned)grid, W * 32, bytes, s>>>(a, *tb);
-    else nq_modal_kernel<1><<<(unsigned)grid, W * 32, bytes, s>>>(a, *tb);
+    {
+        void* args[] = {(void*)&a, (void*)tb.get()};
+        SLB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(W * 32), args, bytes, s));
+    }
     ++g_launch_count;
     slb_status r = check_launch("nq_modal_kernel");
     int h = 0;

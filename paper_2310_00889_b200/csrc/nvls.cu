@@ -96,6 +96,9 @@ void nvls_free(NvlsBuf* b) {
     *b = NvlsBuf();
 }
 
+// The attribute alone is not enough: on some systems (e.g. one GPU of an NVSwitch box exposed to a
+// container) CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 1 but cuMulticastCreate returns
+// CUDA_ERROR_INVALID_VALUE (tools/nvls_probe.py).  Probe a minimal object once.
 bool nvls_supported() {
     DrvApi& A = drv();
     if (!A.ok) return false;
@@ -104,8 +107,26 @@ bool nvls_supported() {
     CUdevice cd;
     if (A.DeviceGet(&cd, dev) != CUDA_SUCCESS) return false;
     int v = 0;
-    if (A.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS) return false;
-    return v != 0;
+    if (A.DeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS || !v) return false;
+    static std::mutex mu;
+    static int probed[64];                       // 0 unknown, 1 yes, 2 no (per device)
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return false;
+    if (!probed[dev]) {
+        CUmulticastObjectProp mp;
+        std::memset(&mp, 0, sizeof(mp));
+        mp.numDevices = 1;
+        mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+        size_t gran = 0;
+        mp.size = 1 << 21;
+        CUmemGenericAllocationHandle h = 0;
+        bool ok = A.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS;
+        if (ok && gran > mp.size) mp.size = gran;
+        ok = ok && A.MulticastCreate(&h, &mp) == CUDA_SUCCESS;
+        if (h) A.MemRelease(h);
+        probed[dev] = ok ? 1 : 2;
+    }
+    return probed[dev] == 1;
 }
 
 // Multicast buffer of >= bytes shared by the communicator's ranks (c == NULL or one rank: a team of one).
@@ -121,7 +142,8 @@ slb_status nvls_alloc(slb_comm* c, size_t bytes, NvlsBuf* b) {
     CUmulticastObjectProp mp;
     std::memset(&mp, 0, sizeof(mp));
     mp.numDevices = (unsigned)R;
-    mp.handleTypes = R > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_NONE;
+    // a shareable handle type is required even for a team of one (NONE is rejected)
+    mp.handleTypes = R > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     mp.size = bytes;
     size_t gran = 0;
     DRV(A.MulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
@@ -157,7 +179,7 @@ slb_status nvls_alloc(slb_comm* c, size_t bytes, NvlsBuf* b) {
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = dev;
-    ap.requestedHandleTypes = R > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_NONE;
+    ap.requestedHandleTypes = R > 1 ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     DRV(A.MemCreate(&b->mem, size, &ap, 0), "cuMemCreate");
     DRV(A.MulticastBindMem(b->mc, 0, b->mem, 0, size, 0), "cuMulticastBindMem");
     b->bound = true;

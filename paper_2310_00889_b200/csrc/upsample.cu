@@ -382,7 +382,9 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
         mbar_expect_tx(&bar[buf], (uint32_t)(NIN * 8));
         bulk_g2s(raw + buf * NIN2, src, (uint32_t)(NIN * 8), &bar[buf]);
     };
+    // both buffers filled up front (a warp typically owns only 2-3 panels: no steady state to hide behind)
     if (lane == 0 && gw < n_panels) issue(gw, 0);
+    if (lane == 0 && gw + stride < n_panels) issue(gw + stride, 1);
     const int g = lane >> 2, tq = lane & 3;
     int it = 0;
     for (int64_t pl = gw; pl < n_panels; pl += stride, ++it) {
@@ -406,10 +408,6 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
             }
         mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
         __syncwarp();
-        if (lane == 0 && pl + stride < n_panels) {
-            fence_proxy_async_smem();
-            issue(pl + stride, buf ^ 1);
-        }
         const double* R = raw + buf * NIN2;
         if (copy_out) {
             double* dst = copy_out + (c_off ? c_off[p] * NC : p * (int64_t)NIN);
@@ -437,6 +435,11 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
             }
         }
         __syncwarp();
+        // raw[buf] fully consumed (step 1 and the copy): refill it with the panel after next
+        if (lane == 0 && pl + 2 * stride < n_panels) {
+            fence_proxy_async_smem();
+            issue(pl + 2 * stride, buf);
+        }
         // step 2 + epilogue: records {g, 0} of two adjacent nodes per lane straight from the accumulators
         double2* D2 = reinterpret_cast<double2*>(dyn);
 #pragma unroll
@@ -514,6 +517,9 @@ static bool rec_supported(int ns, int nt, int ms, int mt) {
 static slb_status rec_dispatch(const InterpParams& ip, int64_t n_panels, const double* sc_in, const double* scale,
                                double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
                                const int64_t* f_off, cudaStream_t s, double* dyn_mc) {
+    static const int w8 = [] { const char* e = getenv("SLB_UPS_W8"); return (e && e[0] == '1') ? 1 : 0; }();
+    if (ip.ns == 10 && ip.nt == 12 && w8)
+        return launch_rec<10, 12, 20, 24, 8>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
     if (ip.ns == 10 && ip.nt == 12)
         return launch_rec<10, 12, 20, 24, 16>(n_panels, ip.mats_d, sc_in, scale, dyn, copy_out, plist, c_off, f_off, s, dyn_mc);
     if (ip.ns == 10 && ip.nt == 16)

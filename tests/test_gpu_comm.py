@@ -73,7 +73,9 @@ def test_one_rank_fused_multicast_gather_bitwise(tmp_path):
         pytest.skip("no CUDA device")
     res, _ = _run(tmp_path, False, nvls=True)
     if not res["nvls_supported"]:
-        pytest.skip("device does not support multicast objects")
+        # e.g. this pool's boxes: the attribute says supported but cuMulticastCreate returns
+        # CUDA_ERROR_INVALID_VALUE for every team size / handle type (tools/nvls_probe.py)
+        pytest.skip("multicast objects cannot be created on this device (see tools/nvls_probe.py)")
     for name, r in res["cases"].items():
         assert r["nvls"], (name, r, res["stderr"])
         assert r["equal_first"] and r["equal_second"] and r["finite"], (name, r)

@@ -109,3 +109,52 @@ def test_nearquad_blocks_vs_oracle(name, mk, kernel, rho, order):
     # the paper's rule (order 0) at the north_star tolerance; the generic 2-D rule of round 1 is held
     # to what its acceptance test supports (it is kept for comparison, N1)
     assert errs.max() <= (TOL if order == 0 else 1e-9), errs
+
+
+def test_nearquad_blocks_vs_oracle_c3v_ragged():
+    """c3v's ragged elements (N4): the 16 x 64 gap elements and a 12 x 12 outer element, through
+    slb_nearcorr_quad_ragged -- singular, neighbour-node, across-the-gap and off-surface pairs."""
+    _skip()
+    import paper_2310_00889_b200 as S
+    pr = make_config("c3v", panels=64)
+    no = pr.node_off()
+    pns, pnt = pr.ns_of_panel(), pr.nt_of_panel()
+    big = int(np.argmax(pns * pnt))                     # a 16 x 64 element at the gap
+    small = int(np.argmin(pns * pnt))                   # a 12 x 12 element away from it
+    trip = []
+    for k in (big, small):
+        ns, nt = int(pns[k]), int(pnt[k])
+        for (i, j) in [(0, 0), (ns // 2, nt // 3), (ns - 1, nt - 1)]:
+            nd = no[k] + i * nt + j
+            trip.append((pr.y_c[nd], nd, k))
+        kn = (k + 1) % pr.P if (k + 1) % (pr.P // 2) else k - 1
+        nd = no[kn] + 2
+        trip.append((pr.y_c[nd], nd, k))
+        for q, f in enumerate([1e-3, -1e-3, 0.1, -0.5]):
+            nd = no[k] + (ns // 2) * nt + (5 * q) % nt
+            trip.append((pr.y_c[nd] + f * 0.05 * pr.n_c[nd], -1, k))
+    y1 = pr.y_c[no[pr.P // 2]:]                        # the other torus' node closest to the gap element
+    d0 = np.linalg.norm(y1 - pr.y_c[no[big]:no[big + 1]].mean(0), axis=1)
+    nd = int(np.argmin(d0)) + no[pr.P // 2]
+    trip.append((pr.y_c[nd], nd, big))
+    X = np.array([t[0] for t in trip])
+    nodes = np.array([t[1] for t in trip], np.int64)
+    pid = np.array([t[2] for t in trip], np.int32)
+    rp = np.arange(len(trip) + 1, dtype=np.int64)
+    sizes = [9 * int(pns[k] * pnt[k]) for k in pid]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    blocks = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
+    eta = pr.eta_body[pr.body_of_panel]
+    S.slb_nearcorr_quad(2, cu(X), cu(rp, torch.int64), cu(pid, torch.int32), pr.Ns, pr.Nt, cu(pr.y_c), blocks,
+                        trg_node=cu(nodes, torch.int64), eta_panel=cu(eta), order=0, panel_nt=pnt, panel_ns=pns)
+    got = blocks.cpu().numpy()
+    errs = []
+    for q, (x, nd, k) in enumerate(trip):
+        ns, nt = int(pns[k]), int(pnt[k])
+        yk = pr.y_c[no[k]:no[k + 1]].reshape(ns, nt, 3)
+        node = ((nd - no[k]) // nt, (nd - no[k]) % nt) if no[k] <= nd < no[k + 1] else None
+        ref = O.nearquad_block(2, x, yk, eta=float(eta[k]), node=node)
+        errs.append(np.abs(got[off[q]:off[q + 1]] - ref.reshape(-1)).max() / np.abs(ref).max())
+    errs = np.array(errs)
+    print("c3v", " ".join(f"{e:.1e}" for e in errs))
+    assert errs.max() <= TOL, errs
