@@ -211,6 +211,38 @@ __device__ __forceinline__ void cardinal_j(int N, int j, int j0, double th0, dou
     *dC = (0.5 * N * cn * cot - 0.5 * sn / (sp * sp)) / N;
 }
 
+// Singular-pair form for a whole ring at once (j0 = the target's index, th = th_j0 + dh, |dh| < pi / N):
+// sin(N phi_j / 2) = (-1)^(j - j0) sin(N dh / 2) and cot(phi_j / 2) = (cot b_j - t) / (1 + t cot b_j), with
+// t = tan(dh / 2) and b_j = pi (j0 - j) / N, so each j costs one division and keeps full relative accuracy
+// (|dh| < pi / N keeps every phi_j, j != j0, at least pi / N from 0); j = j0 takes the Fourier sums.
+__device__ __forceinline__ void cardinal_ring_sing(int N, int j0, double dh, double sh, double ch, double t,
+                                                   const double* r0, const double* D, const double* Dp,
+                                                   double* r, double* rh, double* rs) {
+    for (int c = 0; c < 3; ++c) { r[c] = 0.0; rh[c] = 0.0; rs[c] = 0.0; }
+    for (int j = 0; j < N; ++j) {
+        double C, dC;
+        const int m = j0 - j;
+        if (m == 0) {
+            cardinal_j(N, j, j0, 0.0, dh, sh, ch, &C, &dC);
+        } else {
+            double sb, cb;
+            sincospi((double)m / N, &sb, &cb);
+            const double cotb = cb / sb;
+            const double cot = (cotb - t) / (1.0 + t * cotb);          // cot((dh + 2 pi m / N) / 2)
+            const double sg = (m & 1) ? -1.0 : 1.0;
+            const double sn = sg * sh, cn = sg * ch;
+            C = sn * cot / N;
+            dC = (0.5 * N * cn * cot - 0.5 * sn * (1.0 + cot * cot)) / N;
+        }
+        for (int c = 0; c < 3; ++c) {
+            r[c] += D[3 * j + c] * C;
+            rh[c] += D[3 * j + c] * dC;
+            rs[c] += Dp[3 * j + c] * C;
+        }
+    }
+    (void)r0;
+}
+
 // kernel matrix (rows a = target component, cols b = source component), times J omega
 template <int KD>
 __device__ __forceinline__ void kernel_vals(int kernel, const double r[3], const double n[3], double eta, double dl,
@@ -523,7 +555,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 // modes of the ring (non-singular geometry): Rh_l = (1/N) sum_j D_j e^{-i l th_j}
                 int leff = 0;
                 double th0 = 0.0, dist = 0.0, rr = 1.0;
-                if (!sing) {
+                {
                     for (int e = lane; e < (L + 1) * 6; e += 32) {
                         const int l = e / 6, c = (e % 6) >> 1, im = e & 1, wh = 0;
                         (void)wh;
@@ -547,6 +579,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         for (int e = 0; e < 6; ++e) v = fmax(v, fmax(fabs(Rh[6 * l + e]), fabs(Rp[6 * l + e])));
                         if (v > 1e-17 * mx) leff = l;
                     }
+                }
+                if (!sing) {
                     // closest angle: 64 samples, then Newton on f = |r|^2 / 2 (all lanes, redundantly)
                     auto ring = [&](double th, double* r, double* rh, double* rhh) {
                         for (int c = 0; c < 3; ++c) { r[c] = Rh[c * 2]; rh[c] = 0.0; rhh[c] = 0.0; }
@@ -633,7 +667,12 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         double r[3], rh[3], rs[3];
                         const double th = th0 + dh;
                         if (wq != 0.0) {
-                            if (!sing) {
+                            // the element's own node: relative-accuracy nodal geometry only where r is small
+                            // (close ring and |dh| < 1); elsewhere the modes are accurate to eps |r|
+                            // (within half a node spacing of th_j0: there every other j has |phi_j| > |dh|;
+                            // beyond it |r| > ~rho pi / N and the modal form is accurate to ~eps N)
+                            const bool nodal = sing && alpha < 0.5 && fabs(dh) < kPi / nt;
+                            if (!nodal) {
                                 double s1, c1;
                                 sincos(th, &s1, &c1);
                                 for (int c = 0; c < 3; ++c) { r[c] = Rh[2 * c]; rh[c] = 0.0; rs[c] = Rp[2 * c]; }
@@ -654,16 +693,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                             } else {
                                 double sh, ch;
                                 sincos(0.5 * nt * dh, &sh, &ch);
-                                for (int c = 0; c < 3; ++c) { r[c] = 0.0; rh[c] = 0.0; rs[c] = 0.0; }
-                                for (int j = 0; j < nt; ++j) {
-                                    double C, dC;
-                                    cardinal_j(nt, j, j0, th0, dh, sh, ch, &C, &dC);
-                                    for (int c = 0; c < 3; ++c) {
-                                        r[c] += Dr[3 * j + c] * C;
-                                        rh[c] += Dr[3 * j + c] * dC;
-                                        rs[c] += Dp[3 * j + c] * C;
-                                    }
-                                }
+                                cardinal_ring_sing(nt, j0, dh, sh, ch, tan(0.5 * dh), nullptr, Dr, Dp, r, rh, rs);
                             }
                             // y = x - r: y_th x y_s = r_th x r_s (outward, R8); J = |.|, n = ./J
                             const double cx = rh[1] * rs[2] - rh[2] * rs[1];
