@@ -216,7 +216,7 @@ __device__ __forceinline__ void cardinal_j(int N, int j, int j0, double th0, dou
 // t = tan(dh / 2) and b_j = pi (j0 - j) / N, so each j costs one division and keeps full relative accuracy
 // (|dh| < pi / N keeps every phi_j, j != j0, at least pi / N from 0); j = j0 takes the Fourier sums.
 __device__ __forceinline__ void cardinal_ring_sing(int N, int j0, double dh, double sh, double ch, double t,
-                                                   const double* r0, const double* D, const double* Dp,
+                                                   const double* scm, const double* D, const double* Dp,
                                                    double* r, double* rh, double* rs) {
     for (int c = 0; c < 3; ++c) { r[c] = 0.0; rh[c] = 0.0; rs[c] = 0.0; }
     for (int j = 0; j < N; ++j) {
@@ -225,8 +225,7 @@ __device__ __forceinline__ void cardinal_ring_sing(int N, int j0, double dh, dou
         if (m == 0) {
             cardinal_j(N, j, j0, 0.0, dh, sh, ch, &C, &dC);
         } else {
-            double sb, cb;
-            sincospi((double)m / N, &sb, &cb);
+            const double sb = scm[2 * (m + N - 1)], cb = scm[2 * (m + N - 1) + 1];   // sincospi(m / N)
             const double cotb = cb / sb;
             const double cot = (cotb - t) / (1.0 + t * cotb);          // cot((dh + 2 pi m / N) / 2)
             const double sg = (m & 1) ? -1.0 : 1.0;
@@ -240,7 +239,6 @@ __device__ __forceinline__ void cardinal_ring_sing(int N, int j0, double dh, dou
             rs[c] += Dp[3 * j + c] * C;
         }
     }
-    (void)r0;
 }
 
 // kernel matrix (rows a = target component, cols b = source component), times J omega
@@ -269,7 +267,7 @@ __device__ __forceinline__ void kernel_vals(int kernel, const double r[3], const
 // shared memory layout (doubles) of one CTA
 struct Smem {
     int ns, nt, W, ldE, rows, ldv;       // rows: DMMA rows (16 Stokes, 8 Laplace); ldv = rows + 4 (banks)
-    size_t dq, bs, hb, wb, sub, warp0, per_warp, total;
+    size_t dq, bs, hb, wb, sub, trig, warp0, per_warp, total;
 };
 
 __host__ __device__ inline Smem smem_layout(int ns, int nt, int W, int ldE, int KD) {
@@ -282,6 +280,7 @@ __host__ __device__ inline Smem smem_layout(int ns, int nt, int W, int ldE, int 
     S.hb = o; o += (size_t)W * kd2 * nt;                // h_j per warp slot
     S.wb = o; o += (size_t)W * ns;                      // w_s l_i(s) per warp slot
     S.sub = o; o += (size_t)kMaxSub * 3 + 8;            // sub-panels (a, b, type) + misc
+    S.trig = o; o += (size_t)6 * nt;                   // sincospi(2q / nt), q < nt; sincospi(m / nt), |m| < nt
     o = (o + 1) & ~(size_t)1;
     S.warp0 = o;
     // per warp: ring D[nt][3], D'[nt][3], modes Rh[(L+1)][3][2], Rp[(L+1)][3][2], l[ns], dl[ns],
@@ -345,6 +344,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
         double* Hb = sm + S.hb;
         double* Wb = sm + S.wb;
         double* Sub = sm + S.sub;
+        double* cs2 = sm + S.trig;               // [nt][2]: sincospi(2 q / nt) = (sin, cos)(2 pi q / nt)
+        double* scm = cs2 + 2 * nt;              // [2 nt - 1][2]: sincospi(m / nt), m = 1 - nt .. nt - 1
         double* wbase = sm + S.warp0 + (size_t)warp * S.per_warp;
         double* Dr = wbase;                      // [nt][3]
         double* Dp = Dr + nt * 3;                // [nt][3]
@@ -369,6 +370,9 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
             Dq[3 * q + 2] = x2 - yv[2];
         }
         for (int q = threadIdx.x; q < kd2 * ns * nt; q += blockDim.x) Bs[q] = 0.0;
+        for (int q = threadIdx.x; q < nt; q += blockDim.x) sincospi(2.0 * (double)q / nt, &cs2[2 * q], &cs2[2 * q + 1]);
+        for (int q = threadIdx.x; q < 2 * nt - 1; q += blockDim.x)
+            sincospi((double)(q - (nt - 1)) / nt, &scm[2 * q], &scm[2 * q + 1]);
         for (int q = lane; q < kChunk * S.ldv; q += 32) Vb[q] = 0.0;        // padded rows stay zero
         __syncthreads();
         if (sing && threadIdx.x == 0) {
@@ -443,7 +447,10 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                     const double step = fabs(tn - ts) + fabs(dh);
                     ts = tn;
                     hs += dh;
-                    if (step < 1e-15) break;
+                    // the closest point only places the s sub-panels (Bernstein test) and sets dmin, which is
+                    // second order in the t error: 1e-12 is far below anything the partition can resolve
+                    // (a 1e-15 test never triggers when |hs| ~ pi rounds at ~4e-16 per step: 40 iterations)
+                    if (step < 1e-12) break;
                 }
                 eval_pt(ts, hs, r, rt, rh);
                 dmin = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
@@ -561,9 +568,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         (void)wh;
                         double v = 0.0, dv = 0.0;
                         for (int j = 0; j < nt; ++j) {
-                            double sj, cj;
-                            sincospi(2.0 * (double)((l * j) % nt) / nt, &sj, &cj);
-                            const double f = im ? -sj : cj;
+                            const int q2 = (l * j) % nt;
+                            const double f = im ? -cs2[2 * q2] : cs2[2 * q2 + 1];
                             v += Dr[3 * j + c] * f;
                             dv += Dp[3 * j + c] * f;
                         }
@@ -572,13 +578,18 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                     }
                     __syncwarp();
                     // significant modes (a circle: l <= 1)
+                    // (fmax is exact, so the lane-parallel maxima equal the serial ones)
                     double mx = 0.0;
-                    for (int e = 0; e < (L + 1) * 6; ++e) mx = fmax(mx, fmax(fabs(Rh[e]), fabs(Rp[e])));
-                    for (int l = 0; l <= L; ++l) {
+                    for (int e = lane; e < (L + 1) * 6; e += 32) mx = fmax(mx, fmax(fabs(Rh[e]), fabs(Rp[e])));
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    int lhi = 0;
+                    for (int l = lane; l <= L; l += 32) {
                         double v = 0.0;
                         for (int e = 0; e < 6; ++e) v = fmax(v, fmax(fabs(Rh[6 * l + e]), fabs(Rp[6 * l + e])));
-                        if (v > 1e-17 * mx) leff = l;
+                        if (v > 1e-17 * mx) lhi = l;
                     }
+                    leff = __reduce_max_sync(0xffffffffu, lhi);
                 }
                 if (!sing) {
                     // closest angle: 64 samples, then Newton on f = |r|^2 / 2 (all lanes, redundantly)
@@ -625,7 +636,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         const double lim2 = 0.5;
                         step = fmax(-lim2, fmin(lim2, step));
                         th0 += step;
-                        if (fabs(step) < 1e-15) break;
+                        if (fabs(step) < 1e-13) break;     // Newton: the remaining error is ~step^2
                     }
                     double r[3], rh[3], rhh[3];
                     ring(th0, r, rh, rhh);
@@ -638,8 +649,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                     for (int j = 0; j < nt; ++j) {
                         if (j == j0) continue;
                         const double sg = ((j0 - j) & 1) ? -1.0 : 1.0;
-                        double sp, cp;
-                        sincospi((double)(j0 - j) / nt, &sp, &cp);
+                        const double sp = scm[2 * (j0 - j + nt - 1)], cp = scm[2 * (j0 - j + nt - 1) + 1];
                         const double dc = 0.5 * sg * cp / sp;
                         for (int c = 0; c < 3; ++c) rh[c] += Dr[3 * j + c] * dc;
                     }
@@ -666,6 +676,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         double V[9];
                         double r[3], rh[3], rs[3];
                         const double th = th0 + dh;
+                        double s1, c1;
+                        sincos(th, &s1, &c1);
                         if (wq != 0.0) {
                             // the element's own node: relative-accuracy nodal geometry only where r is small
                             // (close ring and |dh| < 1); elsewhere the modes are accurate to eps |r|
@@ -673,8 +685,6 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                             // beyond it |r| > ~rho pi / N and the modal form is accurate to ~eps N)
                             const bool nodal = sing && alpha < 0.5 && fabs(dh) < kPi / nt;
                             if (!nodal) {
-                                double s1, c1;
-                                sincos(th, &s1, &c1);
                                 for (int c = 0; c < 3; ++c) { r[c] = Rh[2 * c]; rh[c] = 0.0; rs[c] = Rp[2 * c]; }
                                 double cl = 1.0, sl = 0.0;
                                 for (int l = 1; l <= leff; ++l) {
@@ -693,7 +703,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                             } else {
                                 double sh, ch;
                                 sincos(0.5 * nt * dh, &sh, &ch);
-                                cardinal_ring_sing(nt, j0, dh, sh, ch, tan(0.5 * dh), nullptr, Dr, Dp, r, rh, rs);
+                                cardinal_ring_sing(nt, j0, dh, sh, ch, tan(0.5 * dh), scm, Dr, Dp, r, rh, rs);
                             }
                             // y = x - r: y_th x y_s = r_th x r_s (outward, R8); J = |.|, n = ./J
                             const double cx = rh[1] * rs[2] - rh[2] * rs[1];
@@ -710,8 +720,6 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
 #pragma unroll
                         for (int e = 0; e < kd2; ++e) vr[e] = V[e];
                         double* er = Eb + lane * A.ld_e;
-                        double s1, c1;
-                        sincos(th, &s1, &c1);
                         double cl = 1.0, sl = 0.0;
                         er[0] = 1.0;
                         er[1] = 0.0;
@@ -755,8 +763,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 for (int e = lane; e < kd2 * nt; e += 32) {
                     const int row = e / nt, j = e % nt;
                     const double* hh = Eb + row * A.ld_e;
-                    double cj, sj;
-                    sincospi(2.0 * j / nt, &sj, &cj);
+                    const double sj = cs2[2 * j], cj = cs2[2 * j + 1];
                     double cl = 1.0, sl = 0.0, v = hh[0];
                     for (int l = 1; l <= L; ++l) {
                         const double cn = cl * cj - sl * sj;
@@ -931,7 +938,8 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
     }
     const int L = a.nt / 2;
     a.ld_e = (2 * (L + 1) + 7) / 8 * 8;
-    int W = 8;
+    static const int w_env = [] { const char* e = getenv("SLB_NQ_WARPS"); return e ? atoi(e) : 8; }();
+    int W = (w_env == 1 || w_env == 2 || w_env == 4 || w_env == 8) ? w_env : 8;   // tuning studies
     size_t bytes = 0;
     for (; W >= 1; W /= 2) {
         const Smem S = smem_layout(a.ns, a.nt, W, a.ld_e, KD);
