@@ -97,6 +97,9 @@ struct Args {
     int* status;                   // 1: a pair exceeded the sub-panel budget
     int warps, ld_e;               // warps per CTA, E row stride
     double bern;                   // Bernstein sum rho + 1/rho of the s sub-panel test (rho = 2.5)
+    int64_t p0, p1;                // this launch's pairs [p0, p1)
+    double* pre;                   // [p1 - p0][4]: s-rule geometry from nq_srule_kernel (ts, dmin, |y_t|, rho)
+    int64_t* prow;                 // [p1 - p0]: the pair's target row
 };
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -166,6 +169,47 @@ __device__ void lagrange_bary(int n, const double* tg, const double* lam, double
         const double e = ds - tg[i];
         l[i] = (lam[i] / e) / den;
         dl[i] = l[i] * (sinv - 1.0 / e);
+    }
+}
+
+// lagrange_bary with the n <= 32 nodes spread over the warp's lanes (lane i owns node i; the two sums by
+// warp reductions).  Same formulas; only the summation order differs.
+__device__ void lagrange_bary_warp(int lane, int n, const double* tg, const double* lam, double ds, int i0, double* l,
+                                   double* dl) {
+    const double s0 = i0 >= 0 ? tg[i0] : 0.0;
+    const bool own = lane < n;
+    const double e = own ? ds + (s0 - tg[lane]) : 1.0;
+    const unsigned hitm = __ballot_sync(0xffffffffu, own && e == 0.0);
+    if (hitm) {
+        const int hit = 31 - __clz(hitm);                // the last such node (as the serial loop)
+        double v = (own && lane != hit) ? (lam[lane] / lam[hit]) / (tg[hit] - tg[lane]) : 0.0;
+        const double sm = wsum(v);
+        if (own) {
+            l[lane] = lane == hit ? 1.0 : 0.0;
+            dl[lane] = lane == hit ? -sm : v;
+        }
+        return;
+    }
+    const bool term = own && lane != i0;                 // i0 < 0: every node
+    const double den0 = wsum(term ? lam[lane] / e : 0.0);
+    const double sinv = wsum(term ? 1.0 / e : 0.0);
+    if (i0 >= 0) {
+        const double den = lam[i0] + ds * den0;
+        if (own) {
+            if (lane == i0) {
+                l[lane] = lam[i0] / den;
+                dl[lane] = l[lane] * sinv;
+            } else {
+                const double q = (lam[lane] / e) / den;
+                l[lane] = q * ds;
+                dl[lane] = q + l[lane] * (sinv - 1.0 / e);
+            }
+        }
+        return;
+    }
+    if (own) {
+        l[lane] = (lam[lane] / e) / den0;
+        dl[lane] = l[lane] * (sinv - 1.0 / e);
     }
 }
 
@@ -241,6 +285,90 @@ __device__ __forceinline__ void cardinal_ring_sing(int N, int j0, double dh, dou
     }
 }
 
+// The s-rule geometry of one (target, element) pair (one warp): for on-surface targets |y_t| and the ring
+// radius |y_th| at the target node; otherwise the closest point (t*, th*) (the nearest node, then Gauss-Newton
+// on |r(t, th)|^2 with t clamped to [-1, 1]), its distance and |y_t| there.  Dq: the element's nodes relative
+// to the target ((i0, j0) zeroed for on-surface pairs); lg / dlg: the warp's Lagrange scratch.
+__device__ void srule_geometry(int lane, int ns, int nt, const double* tg, const double* lam, const double* Dq,
+                               double* lg, double* dlg, bool sing, int i0, int j0, double* out) {
+    // geometry at (t, th): r = sum D_ij l_i C_j, r_t, r_th (warp-cooperative over j)
+    auto eval_pt = [&](double t, double th, double* r, double* rt, double* rh) {
+        lagrange_bary(ns, tg, lam, t, -1, lg, dlg);       // redundantly per lane (ns <= 32)
+        double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = lane; j < nt; j += 32) {
+            double C, dC;
+            cardinal_j(nt, j, -1, th, 0.0, 0.0, 0.0, &C, &dC);
+            double d[3] = {0, 0, 0}, dd[3] = {0, 0, 0};
+            for (int i = 0; i < ns; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    d[c] += Dq[3 * (i * nt + j) + c] * lg[i];
+                    dd[c] += Dq[3 * (i * nt + j) + c] * dlg[i];
+                }
+            for (int c = 0; c < 3; ++c) {
+                a[c] += d[c] * C;
+                a[3 + c] += dd[c] * C;
+                a[6 + c] += d[c] * dC;
+            }
+        }
+        for (int c = 0; c < 3; ++c) {
+            r[c] = wsum(a[c]);
+            rt[c] = wsum(a[3 + c]);
+            rh[c] = wsum(a[6 + c]);
+        }
+    };
+    double ts = 0.0, hs = 0.0, dmin = 0.0, ytn = 1.0, rho = 1.0;
+    if (sing) {
+        double r[3], rt[3], rh[3];
+        eval_pt(tg[i0], 2.0 * kPi * j0 / nt, r, rt, rh);
+        ytn = sqrt(rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2]);
+        rho = sqrt(rh[0] * rh[0] + rh[1] * rh[1] + rh[2] * rh[2]);
+        ts = tg[i0];
+    } else {
+        // closest point: the nearest node, then Gauss-Newton on |r(t, th)|^2 with t clamped to [-1, 1]
+        double best = 1e300;
+        int bq = 0;
+        for (int q = lane; q < ns * nt; q += 32) {
+            const double dd = Dq[3 * q] * Dq[3 * q] + Dq[3 * q + 1] * Dq[3 * q + 1] + Dq[3 * q + 2] * Dq[3 * q + 2];
+            if (dd < best) { best = dd; bq = q; }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+            if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+        }
+        ts = tg[bq / nt];
+        hs = 2.0 * kPi * (bq % nt) / nt;
+        double r[3], rt[3], rh[3];
+        for (int it = 0; it < 40; ++it) {
+            eval_pt(ts, hs, r, rt, rh);
+            const double a11 = rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2];
+            const double a12 = rt[0] * rh[0] + rt[1] * rh[1] + rt[2] * rh[2];
+            const double a22 = rh[0] * rh[0] + rh[1] * rh[1] + rh[2] * rh[2];
+            // minimise |r|^2 with r = x - y: grad = 2 r.r_t, 2 r.r_h; GN step solves [a] delta = -(r.r_t, r.r_h)
+            const double g1 = r[0] * rt[0] + r[1] * rt[1] + r[2] * rt[2];
+            const double g2 = r[0] * rh[0] + r[1] * rh[1] + r[2] * rh[2];
+            const double det = a11 * a22 - a12 * a12;
+            double dt = -(a22 * g1 - a12 * g2) / det, dh = -(a11 * g2 - a12 * g1) / det;
+            double tn = ts + dt;
+            if (tn > 1.0 || tn < -1.0) {
+                tn = tn > 1.0 ? 1.0 : -1.0;
+                dh = -g2 / a22;
+            }
+            const double step = fabs(tn - ts) + fabs(dh);
+            ts = tn;
+            hs += dh;
+            // the closest point only places the s sub-panels (Bernstein test) and sets dmin, which is
+            // second order in the t error: 1e-12 is far below anything the partition can resolve
+            // (a 1e-15 test never triggers when |hs| ~ pi rounds at ~4e-16 per step: 40 iterations)
+            if (step < 1e-12) break;
+        }
+        eval_pt(ts, hs, r, rt, rh);
+        dmin = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        ytn = sqrt(rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2]);
+    }
+    out[0] = ts; out[1] = dmin; out[2] = ytn; out[3] = rho;
+}
+
 // kernel matrix (rows a = target component, cols b = source component), times J omega
 template <int KD>
 __device__ __forceinline__ void kernel_vals(int kernel, const double r[3], const double n[3], double eta, double dl,
@@ -292,6 +420,61 @@ __host__ __device__ inline Smem smem_layout(int ns, int nt, int W, int ldE, int 
     return S;
 }
 
+// Pre-pass: the s-rule geometry of every pair of [p0, p1), one warp per pair (the Gauss-Newton closest point
+// is serial per pair; done here at full occupancy instead of by one warp of the quadrature CTA while the
+// others wait).  Per warp: the element's nodes relative to the target, Lagrange scratch.
+__global__ void __launch_bounds__(128) nq_srule_kernel(const __grid_constant__ Args A, const __grid_constant__ Tables TB) {
+    extern __shared__ __align__(16) double sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per_warp = A.ns * A.nt * 3 + 2 * A.ns;
+    double* Dq = sm + (size_t)warp * per_warp;
+    double* lg = Dq + A.ns * A.nt * 3;
+    double* dlg = lg + A.ns;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t p = A.p0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < A.p1; p += nw) {
+        int64_t t = 0;
+        if (lane == 0) {
+            int64_t lo = 0, hi = A.T;                 // row t: row_ptr[t] <= p < row_ptr[t+1]
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) / 2;
+                if (A.row_ptr[mid] <= p) lo = mid; else hi = mid;
+            }
+            t = lo;
+        }
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const int k = A.panel_idx[p];
+        const int ns = A.pns ? A.pns[k] : A.ns, nt = A.pnt ? A.pnt[k] : A.nt;
+        const int64_t n0 = A.cn0 ? A.cn0[k] : (int64_t)k * ns * nt;
+        int i0 = -1, j0 = -1;
+        const int64_t nd = A.trg_node ? A.trg_node[t] : -1;
+        if (nd >= n0 && nd < n0 + (int64_t)ns * nt) {
+            i0 = (int)((nd - n0) / nt);
+            j0 = (int)((nd - n0) % nt);
+        }
+        const double x0 = A.x[3 * t], x1 = A.x[3 * t + 1], x2 = A.x[3 * t + 2];
+        for (int q = lane; q < ns * nt; q += 32) {
+            const double* yv = A.y + 3 * (n0 + q);
+            Dq[3 * q] = x0 - yv[0];
+            Dq[3 * q + 1] = x1 - yv[1];
+            Dq[3 * q + 2] = x2 - yv[2];
+        }
+        __syncwarp();
+        if (i0 >= 0 && lane == 0) {
+            Dq[3 * (i0 * nt + j0)] = 0.0; Dq[3 * (i0 * nt + j0) + 1] = 0.0; Dq[3 * (i0 * nt + j0) + 2] = 0.0;
+        }
+        __syncwarp();
+        double out[4];
+        srule_geometry(lane, ns, nt, TB.tgl + ns * (ns - 1) / 2, TB.lam + ns * (ns - 1) / 2, Dq, lg, dlg, i0 >= 0,
+                       i0, j0, out);
+        if (lane == 0) {
+            double* o = A.pre + 4 * (p - A.p0);
+            o[0] = out[0]; o[1] = out[1]; o[2] = out[2]; o[3] = out[3];
+            A.prow[p - A.p0] = t;
+        }
+        __syncwarp();
+    }
+}
+
 // KD: kernel dimension (1 Laplace, 3 Stokes); NCT: 8-column DMMA tiles of the modal sums (covers the
 // launch's largest N_th: 2 (N_th/2 + 1) columns), so the accumulators are sized per rule class.
 template <int KD, int NCT>
@@ -305,18 +488,13 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
     const int g = lane >> 2, tq = lane & 3;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_pair = (int64_t)atomicAdd(A.work, 1ull);
+        if (threadIdx.x == 0) s_pair = A.p0 + (int64_t)atomicAdd(A.work, 1ull);
         __syncthreads();
         const int64_t p = s_pair;
-        if (p >= A.nnz) return;
+        if (p >= A.p1) return;
         // ------------------------------------------------ pair setup
         if (threadIdx.x == 0) {
-            int64_t lo = 0, hi = A.T;                 // row t: row_ptr[t] <= p < row_ptr[t+1]
-            while (hi - lo > 1) {
-                const int64_t mid = (lo + hi) / 2;
-                if (A.row_ptr[mid] <= p) lo = mid; else hi = mid;
-            }
-            const int64_t t = lo;
+            const int64_t t = A.prow[p - A.p0];
             const int k = A.panel_idx[p];
             const int ns = A.pns ? A.pns[k] : A.ns, nt = A.pnt ? A.pnt[k] : A.nt;
             const int64_t n0 = A.cn0 ? A.cn0[k] : (int64_t)k * ns * nt;
@@ -379,83 +557,10 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
             Dq[3 * (i0 * nt + j0)] = 0.0; Dq[3 * (i0 * nt + j0) + 1] = 0.0; Dq[3 * (i0 * nt + j0) + 2] = 0.0;
         }
         __syncthreads();
-        // ------------------------------------------------ s rule (warp 0)
+        // ------------------------------------------------ s rule (warp 0, from the pre-pass geometry)
         if (warp == 0) {
-            // geometry at (t, th): r = sum D_ij l_i C_j, r_t, r_th (warp-cooperative over j)
-            auto eval_pt = [&](double t, double th, double* r, double* rt, double* rh) {
-                lagrange_bary(ns, tg, lam, t, -1, lg, dlg);       // redundantly per lane (ns <= 32)
-                double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-                for (int j = lane; j < nt; j += 32) {
-                    double C, dC;
-                    cardinal_j(nt, j, -1, th, 0.0, 0.0, 0.0, &C, &dC);
-                    double d[3] = {0, 0, 0}, dd[3] = {0, 0, 0};
-                    for (int i = 0; i < ns; ++i)
-                        for (int c = 0; c < 3; ++c) {
-                            d[c] += Dq[3 * (i * nt + j) + c] * lg[i];
-                            dd[c] += Dq[3 * (i * nt + j) + c] * dlg[i];
-                        }
-                    for (int c = 0; c < 3; ++c) {
-                        a[c] += d[c] * C;
-                        a[3 + c] += dd[c] * C;
-                        a[6 + c] += d[c] * dC;
-                    }
-                }
-                for (int c = 0; c < 3; ++c) {
-                    r[c] = wsum(a[c]);
-                    rt[c] = wsum(a[3 + c]);
-                    rh[c] = wsum(a[6 + c]);
-                }
-            };
-            double ts = 0.0, hs = 0.0, dmin = 0.0, ytn = 1.0, rho = 1.0;
-            if (sing) {
-                double r[3], rt[3], rh[3];
-                eval_pt(tg[i0], 2.0 * kPi * j0 / nt, r, rt, rh);
-                ytn = sqrt(rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2]);
-                rho = sqrt(rh[0] * rh[0] + rh[1] * rh[1] + rh[2] * rh[2]);
-                ts = tg[i0];
-            } else {
-                // closest point: the nearest node, then Gauss-Newton on |r(t, th)|^2 with t clamped to [-1, 1]
-                double best = 1e300;
-                int bq = 0;
-                for (int q = lane; q < ns * nt; q += 32) {
-                    const double dd = Dq[3 * q] * Dq[3 * q] + Dq[3 * q + 1] * Dq[3 * q + 1] + Dq[3 * q + 2] * Dq[3 * q + 2];
-                    if (dd < best) { best = dd; bq = q; }
-                }
-                for (int o = 16; o; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-                    if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
-                }
-                ts = tg[bq / nt];
-                hs = 2.0 * kPi * (bq % nt) / nt;
-                double r[3], rt[3], rh[3];
-                for (int it = 0; it < 40; ++it) {
-                    eval_pt(ts, hs, r, rt, rh);
-                    const double a11 = rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2];
-                    const double a12 = rt[0] * rh[0] + rt[1] * rh[1] + rt[2] * rh[2];
-                    const double a22 = rh[0] * rh[0] + rh[1] * rh[1] + rh[2] * rh[2];
-                    // minimise |r|^2 with r = x - y: grad = 2 r.r_t, 2 r.r_h; GN step solves [a] delta = -(r.r_t, r.r_h)
-                    const double g1 = r[0] * rt[0] + r[1] * rt[1] + r[2] * rt[2];
-                    const double g2 = r[0] * rh[0] + r[1] * rh[1] + r[2] * rh[2];
-                    const double det = a11 * a22 - a12 * a12;
-                    double dt = -(a22 * g1 - a12 * g2) / det, dh = -(a11 * g2 - a12 * g1) / det;
-                    double tn = ts + dt;
-                    if (tn > 1.0 || tn < -1.0) {
-                        tn = tn > 1.0 ? 1.0 : -1.0;
-                        dh = -g2 / a22;
-                    }
-                    const double step = fabs(tn - ts) + fabs(dh);
-                    ts = tn;
-                    hs += dh;
-                    // the closest point only places the s sub-panels (Bernstein test) and sets dmin, which is
-                    // second order in the t error: 1e-12 is far below anything the partition can resolve
-                    // (a 1e-15 test never triggers when |hs| ~ pi rounds at ~4e-16 per step: 40 iterations)
-                    if (step < 1e-12) break;
-                }
-                eval_pt(ts, hs, r, rt, rh);
-                dmin = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-                ytn = sqrt(rt[0] * rt[0] + rt[1] * rt[1] + rt[2] * rt[2]);
-            }
+            const double* pg = A.pre + 4 * (p - A.p0);
+            const double ts = pg[0], dmin = pg[1], ytn = pg[2], rho = pg[3];
             if (lane == 0) {
                 int nsub = 0, over = 0;
                 auto push = [&](double a, double b, int type) {
@@ -543,7 +648,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                 else if (type == 2) { ds = a + (b - a) * c_logrule_u[m]; wsn = (b - a) * c_logrule_w[m]; }
                 else { ds = b - (b - a) * c_logrule_u[m]; wsn = (b - a) * c_logrule_w[m]; }
                 // Lagrange basis at s (relative differences for singular pairs)
-                if (lane == 0) lagrange_bary(ns, tg, lam, ds, sing ? i0 : -1, lg, dlg);
+                lagrange_bary_warp(lane, ns, tg, lam, ds, sing ? i0 : -1, lg, dlg);
                 __syncwarp();
                 // ring D_j(s) = sum_i (x - y_ij) l_i(s), D'_j = sum_i (x - y_ij) l_i'(s)
                 for (int e = lane; e < nt * 3; e += 32) {
@@ -968,13 +1073,32 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
     { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
     int per_sm = 0;
     SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, W * 32, bytes));
-    const int64_t grid = std::min<int64_t>(nnz, (int64_t)num_sms() * std::max(1, per_sm));
-    {
+    // pre-pass geometry for pairs in chunks (32 + 8 bytes per pair)
+    const int64_t chunk = std::min<int64_t>(nnz, (int64_t)1 << 22);
+    SLB_CUDA(cudaMallocAsync(&a.pre, sizeof(double) * 4 * chunk, s));
+    SLB_CUDA(cudaMallocAsync(&a.prow, sizeof(int64_t) * chunk, s));
+    const void* fpre = (const void*)nq_srule_kernel;
+    const size_t pre_bytes = sizeof(double) * 4 * ((size_t)a.ns * a.nt * 3 + 2 * a.ns);   // 4 warps
+    { slb_status st_ = smem_optin(fpre); if (st_ != SLB_OK) return st_; }
+    int pre_per_sm = 0;
+    SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pre_per_sm, fpre, 128, pre_bytes));
+    slb_status r = SLB_OK;
+    for (int64_t c0 = 0; c0 < nnz && r == SLB_OK; c0 += chunk) {
+        a.p0 = c0;
+        a.p1 = std::min<int64_t>(nnz, c0 + chunk);
+        const int64_t np = a.p1 - a.p0;
         void* args[] = {(void*)&a, (void*)tb.get()};
+        const int64_t gpre = std::min<int64_t>((np + 3) / 4, (int64_t)num_sms() * std::max(1, pre_per_sm));
+        SLB_CUDA(cudaLaunchKernel(fpre, dim3((unsigned)gpre), dim3(128), args, pre_bytes, s));
+        ++g_launch_count;
+        r = check_launch("nq_srule_kernel");
+        if (r != SLB_OK) break;
+        SLB_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long), s));
+        const int64_t grid = std::min<int64_t>(np, (int64_t)num_sms() * std::max(1, per_sm));
         SLB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(W * 32), args, bytes, s));
+        ++g_launch_count;
+        r = check_launch("nq_modal_kernel");
     }
-    ++g_launch_count;
-    slb_status r = check_launch("nq_modal_kernel");
     int h = 0;
     if (r == SLB_OK) {
         cudaError_t e = cudaMemcpyAsync(&h, a.status, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -982,6 +1106,8 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
         if (e != cudaSuccess) { set_error(std::string("nearquad (modal): ") + cudaGetErrorString(e)); r = SLB_ERR_CUDA; }
     }
     cudaFreeAsync(work, s);
+    cudaFreeAsync(a.pre, s);
+    cudaFreeAsync(a.prow, s);
     if (r == SLB_OK && h) {
         set_error("nearquad (modal): s sub-panel budget exceeded (target extremely close to an element)");
         r = SLB_ERR_UNSUPPORTED;

@@ -1,10 +1,9 @@
 #!/bin/bash
-# N1 iteration: parity tests + c3 timing (W = 8 and W = 4) + setup bench for the small workloads.
+# N1 iteration: parity tests + c3 / c3v timing + setup bench for the small workloads.
 set -u
 O=gpurun_out/r02nq
 mkdir -p $O
+timeout 300 python tools/nq_profile.py c3 > $O/nq_c3.log 2>&1; echo c3=$?
 timeout 900 python -m pytest tests/test_gpu_nearquad_parity.py -x -q > $O/pytest_nq_parity.log 2>&1; echo parity=$?
-timeout 300 python tools/nq_profile.py c3 > $O/nq_c3_w8.log 2>&1; echo w8=$?
-SLB_NQ_WARPS=4 timeout 300 python tools/nq_profile.py c3 > $O/nq_c3_w4.log 2>&1; echo w4=$?
-timeout 300 python tools/nq_profile.py c3v > $O/nq_c3v_w8.log 2>&1; echo c3v=$?
+timeout 300 python tools/nq_profile.py c3v > $O/nq_c3v.log 2>&1; echo c3v=$?
 timeout 600 python tools/setup_bench.py torus torus_slender c2 c3 > $O/setup_bench.jsonl 2> $O/setup_bench.err; echo setup=$?
