@@ -68,6 +68,8 @@ __host__ __device__ inline int class_of_nt(int nt) { return nt <= 12 ? 0 : nt <=
 struct RuleSet {
     const double* th;              // angular nodes relative to th0
     const double* w;               // weights (0 on padding)
+    const double* E;               // [node][lde]: cos(l th_m), sin(l th_m), l = 0 .. the class's largest N_th / 2
+    int lde;
     int off[kNRules], cnt[kNRules];   // cnt: multiple of kChunk
 };
 
@@ -97,7 +99,8 @@ struct Args {
     int* status;                   // 1: a pair exceeded the sub-panel budget
     int warps, ld_e;               // warps per CTA, E row stride
     double bern;                   // Bernstein sum rho + 1/rho of the s sub-panel test (rho = 2.5)
-    int64_t p0, p1;                // this launch's pairs [p0, p1)
+    int64_t p0, p1;                // this launch's pairs: plist[p0 .. p1) (plist NULL: the pair ids p0 .. p1)
+    const int64_t* plist;
     double* pre;                   // [p1 - p0][4]: s-rule geometry from nq_srule_kernel (ts, dmin, |y_t|, rho)
     int64_t* prow;                 // [p1 - p0]: the pair's target row
 };
@@ -412,8 +415,8 @@ __host__ __device__ inline Smem smem_layout(int ns, int nt, int W, int ldE, int 
     o = (o + 1) & ~(size_t)1;
     S.warp0 = o;
     // per warp: ring D[nt][3], D'[nt][3], modes Rh[(L+1)][3][2], Rp[(L+1)][3][2], l[ns], dl[ns],
-    //           V[kChunk][rows], E[kChunk][ldE] (also the hhat staging [rows][ldE])
-    size_t pw = (size_t)nt * 6 + (size_t)(L + 1) * 12 + 2 * ns + (size_t)kChunk * S.ldv + (size_t)kChunk * ldE;
+    //           V[kChunk][rows], the ghat staging [rows][ldE]
+    size_t pw = (size_t)nt * 6 + (size_t)(L + 1) * 12 + 2 * ns + (size_t)kChunk * S.ldv + (size_t)S.rows * ldE;
     S.per_warp = (pw + 1) & ~(size_t)1;
     o += S.per_warp * W;
     S.total = o;
@@ -431,7 +434,8 @@ __global__ void __launch_bounds__(128) nq_srule_kernel(const __grid_constant__ A
     double* lg = Dq + A.ns * A.nt * 3;
     double* dlg = lg + A.ns;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t p = A.p0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; p < A.p1; p += nw) {
+    for (int64_t q = A.p0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; q < A.p1; q += nw) {
+        const int64_t p = A.plist ? A.plist[q] : q;
         int64_t t = 0;
         if (lane == 0) {
             int64_t lo = 0, hi = A.T;                 // row t: row_ptr[t] <= p < row_ptr[t+1]
@@ -467,9 +471,9 @@ __global__ void __launch_bounds__(128) nq_srule_kernel(const __grid_constant__ A
         srule_geometry(lane, ns, nt, TB.tgl + ns * (ns - 1) / 2, TB.lam + ns * (ns - 1) / 2, Dq, lg, dlg, i0 >= 0,
                        i0, j0, out);
         if (lane == 0) {
-            double* o = A.pre + 4 * (p - A.p0);
+            double* o = A.pre + 4 * (q - A.p0);
             o[0] = out[0]; o[1] = out[1]; o[2] = out[2]; o[3] = out[3];
-            A.prow[p - A.p0] = t;
+            A.prow[q - A.p0] = t;
         }
         __syncwarp();
     }
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(128) nq_srule_kernel(const __grid_constant__ A
 template <int KD, int NCT>
 __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ Args A, const __grid_constant__ Tables TB) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ int64_t s_pair;
+    __shared__ int64_t s_pair, s_q;
     __shared__ int s_info[8];
     __shared__ double s_real[16];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = A.warps;
@@ -488,13 +492,17 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
     const int g = lane >> 2, tq = lane & 3;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_pair = A.p0 + (int64_t)atomicAdd(A.work, 1ull);
+        if (threadIdx.x == 0) {
+            const int64_t q = A.p0 + (int64_t)atomicAdd(A.work, 1ull);
+            s_q = q;
+            s_pair = q < A.p1 ? (A.plist ? A.plist[q] : q) : -1;
+        }
         __syncthreads();
-        const int64_t p = s_pair;
-        if (p >= A.p1) return;
+        const int64_t p = s_pair, qi = s_q - A.p0;      // qi: index into the pre-pass arrays
+        if (p < 0) return;
         // ------------------------------------------------ pair setup
         if (threadIdx.x == 0) {
-            const int64_t t = A.prow[p - A.p0];
+            const int64_t t = A.prow[qi];
             const int k = A.panel_idx[p];
             const int ns = A.pns ? A.pns[k] : A.ns, nt = A.pnt ? A.pnt[k] : A.nt;
             const int64_t n0 = A.cn0 ? A.cn0[k] : (int64_t)k * ns * nt;
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
         __syncthreads();
         // ------------------------------------------------ s rule (warp 0, from the pre-pass geometry)
         if (warp == 0) {
-            const double* pg = A.pre + 4 * (p - A.p0);
+            const double* pg = A.pre + 4 * qi;
             const double ts = pg[0], dmin = pg[1], ytn = pg[2], rho = pg[3];
             if (lane == 0) {
                 int nsub = 0, over = 0;
@@ -824,20 +832,11 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                         double* vr = Vb + lane * S.ldv;
 #pragma unroll
                         for (int e = 0; e < kd2; ++e) vr[e] = V[e];
-                        double* er = Eb + lane * A.ld_e;
-                        double cl = 1.0, sl = 0.0;
-                        er[0] = 1.0;
-                        er[1] = 0.0;
-                        for (int l = 1; l <= L; ++l) {
-                            const double cn = cl * c1 - sl * s1;
-                            sl = sl * c1 + cl * s1;
-                            cl = cn;
-                            er[2 * l] = cl;
-                            er[2 * l + 1] = sl;
-                        }
                     }
                     __syncwarp();
-                    // hhat[row][col] += sum_m V[m][row] E[m][col]
+                    // ghat[row][col] += sum_m V[m][row] E[m][col], E = the rule's stored modes e^{i l th_m} (th_m
+                    // relative to th0; the rotation by e^{i l th0} is applied in the inverse DFT)
+                    const double* Et = RS.E + (size_t)(roff + c0) * RS.lde;
 #pragma unroll
                     for (int k0 = 0; k0 < kChunk; k0 += 4) {
                         const int mrow = k0 + tq;
@@ -847,7 +846,7 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
 #pragma unroll
                         for (int ct = 0; ct < NCT; ++ct) {
                             if (ct < nct) {
-                                const double bv = Eb[mrow * A.ld_e + 8 * ct + g];
+                                const double bv = __ldg(Et + (size_t)mrow * RS.lde + 8 * ct + g);
 #pragma unroll
                                 for (int rt = 0; rt < NRT; ++rt) dmma(acc[rt][ct][0], acc[rt][ct][1], av[rt], bv);
                             }
@@ -855,7 +854,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                     }
                     __syncwarp();
                 }
-                // stage hhat in Eb as [row][ld_e], then the inverse DFT h_j (Eq. e:modal-greens-fn-wts)
+                // stage ghat in Eb as [row][ld_e], then the inverse DFT h_j (Eq. e:modal-greens-fn-wts) of
+                // hhat_l = e^{i l th0} ghat_l: Re(hhat_l e^{-i l th_j}) = Re(ghat_l e^{-i l (th_j - th0)})
 #pragma unroll
                 for (int rt = 0; rt < NRT; ++rt)
 #pragma unroll
@@ -865,10 +865,13 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
                             Eb[(8 * rt + g) * A.ld_e + 8 * ct + 2 * tq + 1] = acc[rt][ct][1];
                         }
                 __syncwarp();
+                double st0, ct0;
+                sincos(th0, &st0, &ct0);
                 for (int e = lane; e < kd2 * nt; e += 32) {
                     const int row = e / nt, j = e % nt;
                     const double* hh = Eb + row * A.ld_e;
-                    const double sj = cs2[2 * j], cj = cs2[2 * j + 1];
+                    const double sj = cs2[2 * j] * ct0 - cs2[2 * j + 1] * st0;      // sin(th_j - th0)
+                    const double cj = cs2[2 * j + 1] * ct0 + cs2[2 * j] * st0;      // cos(th_j - th0)
                     double cl = 1.0, sl = 0.0, v = hh[0];
                     for (int l = 1; l <= L; ++l) {
                         const double cn = cl * cj - sl * sj;
@@ -907,6 +910,8 @@ __global__ void __launch_bounds__(256) nq_modal_kernel(const __grid_constant__ A
 struct RuleBuf {
     double* th = nullptr;
     double* w = nullptr;
+    double* E = nullptr;
+    int lde = 0;
     int off[kNRules], cnt[kNRules];
 };
 
@@ -976,6 +981,18 @@ static const RuleBuf* rules_for_class(int c) {
     RuleBuf rb;
     std::vector<double> th, w;
     build_rules(lmax_of_class(c), th, w, rb.off, rb.cnt);
+    // stored modes of every node ("precomputed and stored along with the quadrature rule")
+    const int Lc = (c == 0 ? 12 : c == 1 ? 24 : c == 2 ? 40 : 64) / 2;
+    rb.lde = (2 * (Lc + 1) + 7) / 8 * 8;
+    std::vector<double> E(th.size() * rb.lde, 0.0);
+    for (size_t m = 0; m < th.size(); ++m)
+        for (int l = 0; 2 * l + 1 < rb.lde; ++l) {
+            E[m * rb.lde + 2 * l] = std::cos(l * th[m]);
+            E[m * rb.lde + 2 * l + 1] = std::sin(l * th[m]);
+        }
+    if (cudaMalloc(&rb.E, sizeof(double) * E.size()) != cudaSuccess ||
+        cudaMemcpy(rb.E, E.data(), sizeof(double) * E.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return nullptr;
     if (cudaMalloc(&rb.th, sizeof(double) * th.size()) != cudaSuccess) return nullptr;
     if (cudaMalloc(&rb.w, sizeof(double) * w.size()) != cudaSuccess) { cudaFree(rb.th); return nullptr; }
     if (cudaMemcpy(rb.th, th.data(), sizeof(double) * th.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -1020,6 +1037,8 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
         SLB_REQUIRE(rb, SLB_ERR_OOM, "nearquad (modal): rule tables");
         tb->rs[c].th = rb->th;
         tb->rs[c].w = rb->w;
+        tb->rs[c].E = rb->E;
+        tb->rs[c].lde = rb->lde;
         std::memcpy(tb->rs[c].off, rb->off, sizeof(rb->off));
         std::memcpy(tb->rs[c].cnt, rb->cnt, sizeof(rb->cnt));
     }
@@ -1041,63 +1060,105 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
         static const double rb = [] { const char* e = getenv("SLB_NQ_BERN_RHO"); return e ? atof(e) : 2.5; }();
         a.bern = rb + 1.0 / rb;          // SLB_NQ_BERN_RHO: tuning / accuracy studies only
     }
-    const int L = a.nt / 2;
-    a.ld_e = (2 * (L + 1) + 7) / 8 * 8;
-    static const int w_env = [] { const char* e = getenv("SLB_NQ_WARPS"); return e ? atoi(e) : 8; }();
-    int W = (w_env == 1 || w_env == 2 || w_env == 4 || w_env == 8) ? w_env : 8;   // tuning studies
-    size_t bytes = 0;
-    for (; W >= 1; W /= 2) {
-        const Smem S = smem_layout(a.ns, a.nt, W, a.ld_e, KD);
-        bytes = S.total * sizeof(double);
-        if (bytes <= 200 * 1024) break;
-    }
-    SLB_REQUIRE(W >= 1, SLB_ERR_UNSUPPORTED, "nearquad (modal): shared memory");
-    a.warps = W;
     int64_t nnz = 0;
     SLB_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_trg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     SLB_CUDA(cudaStreamSynchronize(s));
     a.nnz = nnz;
     if (nnz == 0) return SLB_OK;
+    // Segments of pairs with one launch configuration each.  Uniform orders: one segment, every pair.  Ragged
+    // orders: the pairs grouped by the angular rule class of their element (N_th <= 12 / 24 / 40 / 64), each
+    // group launched with its own accumulator width, shared-memory layout and CTA size, so the small elements
+    // do not pay for the largest one (pair order inside a group: ascending, i.e. target-major).
+    struct Seg { int64_t off, cnt; int ns, nt; };
+    std::vector<Seg> segs;
+    int64_t* plist_d = nullptr;
+    if (pnt) {
+        std::vector<int32_t> pidx(nnz);
+        SLB_CUDA(cudaMemcpyAsync(pidx.data(), panel_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s));
+        SLB_CUDA(cudaStreamSynchronize(s));
+        int32_t P = 0;
+        for (int64_t q = 0; q < nnz; ++q) P = std::max(P, pidx[q] + 1);
+        std::vector<int32_t> hnt(P), hns(P, ns_uniform);
+        SLB_CUDA(cudaMemcpy(hnt.data(), pnt, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+        if (pns) SLB_CUDA(cudaMemcpy(hns.data(), pns, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> order;
+        order.reserve(nnz);
+        for (int c = 0; c < kNClass; ++c) {
+            Seg g{(int64_t)order.size(), 0, 1, 1};
+            for (int64_t q = 0; q < nnz; ++q) {
+                const int k = pidx[q];
+                if (class_of_nt(hnt[k]) != c) continue;
+                order.push_back(q);
+                g.ns = std::max(g.ns, hns[k]);
+                g.nt = std::max(g.nt, hnt[k]);
+            }
+            g.cnt = (int64_t)order.size() - g.off;
+            if (g.cnt) segs.push_back(g);
+        }
+        SLB_CUDA(cudaMallocAsync(&plist_d, sizeof(int64_t) * nnz, s));
+        SLB_CUDA(cudaMemcpyAsync(plist_d, order.data(), sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        SLB_CUDA(cudaStreamSynchronize(s));              // order is a host temporary
+    } else {
+        segs.push_back({0, nnz, a.ns, a.nt});
+    }
+    a.plist = plist_d;
     unsigned long long* work = nullptr;
     SLB_CUDA(cudaMallocAsync(&work, sizeof(unsigned long long) + sizeof(int) * 2, s));
     SLB_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
     a.work = work;
     a.status = reinterpret_cast<int*>(work + 1);
-    const int nct_launch = (2 * (a.nt / 2 + 1) + 7) / 8;
-    const int NCTc = nct_launch <= 2 ? 2 : nct_launch <= 4 ? 4 : nct_launch <= 6 ? 6 : 9;
-    const void* fn;
-#define NQ_FN(K, C) (const void*)nq_modal_kernel<K, C>
-    if (KD == 3) fn = NCTc == 2 ? NQ_FN(3, 2) : NCTc == 4 ? NQ_FN(3, 4) : NCTc == 6 ? NQ_FN(3, 6) : NQ_FN(3, 9);
-    else fn = NCTc == 2 ? NQ_FN(1, 2) : NCTc == 4 ? NQ_FN(1, 4) : NCTc == 6 ? NQ_FN(1, 6) : NQ_FN(1, 9);
-#undef NQ_FN
-    { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
-    int per_sm = 0;
-    SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, W * 32, bytes));
     // pre-pass geometry for pairs in chunks (32 + 8 bytes per pair)
     const int64_t chunk = std::min<int64_t>(nnz, (int64_t)1 << 22);
     SLB_CUDA(cudaMallocAsync(&a.pre, sizeof(double) * 4 * chunk, s));
     SLB_CUDA(cudaMallocAsync(&a.prow, sizeof(int64_t) * chunk, s));
-    const void* fpre = (const void*)nq_srule_kernel;
-    const size_t pre_bytes = sizeof(double) * 4 * ((size_t)a.ns * a.nt * 3 + 2 * a.ns);   // 4 warps
-    { slb_status st_ = smem_optin(fpre); if (st_ != SLB_OK) return st_; }
-    int pre_per_sm = 0;
-    SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pre_per_sm, fpre, 128, pre_bytes));
+    static const int w_env = [] { const char* e = getenv("SLB_NQ_WARPS"); return e ? atoi(e) : 8; }();
     slb_status r = SLB_OK;
-    for (int64_t c0 = 0; c0 < nnz && r == SLB_OK; c0 += chunk) {
-        a.p0 = c0;
-        a.p1 = std::min<int64_t>(nnz, c0 + chunk);
-        const int64_t np = a.p1 - a.p0;
-        void* args[] = {(void*)&a, (void*)tb.get()};
-        const int64_t gpre = std::min<int64_t>((np + 3) / 4, (int64_t)num_sms() * std::max(1, pre_per_sm));
-        SLB_CUDA(cudaLaunchKernel(fpre, dim3((unsigned)gpre), dim3(128), args, pre_bytes, s));
-        ++g_launch_count;
-        r = check_launch("nq_srule_kernel");
+    for (const Seg& g : segs) {
         if (r != SLB_OK) break;
-        SLB_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long), s));
-        const int64_t grid = std::min<int64_t>(np, (int64_t)num_sms() * std::max(1, per_sm));
-        SLB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(W * 32), args, bytes, s));
-        ++g_launch_count;
-        r = check_launch("nq_modal_kernel");
+        a.ns = g.ns;
+        a.nt = g.nt;
+        const int L = a.nt / 2;
+        a.ld_e = (2 * (L + 1) + 7) / 8 * 8;
+        int W = (w_env == 1 || w_env == 2 || w_env == 4 || w_env == 8) ? w_env : 8;   // tuning studies
+        size_t bytes = 0;
+        for (; W >= 1; W /= 2) {
+            const Smem S = smem_layout(a.ns, a.nt, W, a.ld_e, KD);
+            bytes = S.total * sizeof(double);
+            if (bytes <= 200 * 1024) break;
+        }
+        SLB_REQUIRE(W >= 1, SLB_ERR_UNSUPPORTED, "nearquad (modal): shared memory");
+        a.warps = W;
+        const int nct_launch = (2 * (a.nt / 2 + 1) + 7) / 8;
+        const int NCTc = nct_launch <= 2 ? 2 : nct_launch <= 4 ? 4 : nct_launch <= 6 ? 6 : 9;
+        const void* fn;
+#define NQ_FN(K, C) (const void*)nq_modal_kernel<K, C>
+        if (KD == 3) fn = NCTc == 2 ? NQ_FN(3, 2) : NCTc == 4 ? NQ_FN(3, 4) : NCTc == 6 ? NQ_FN(3, 6) : NQ_FN(3, 9);
+        else fn = NCTc == 2 ? NQ_FN(1, 2) : NCTc == 4 ? NQ_FN(1, 4) : NCTc == 6 ? NQ_FN(1, 6) : NQ_FN(1, 9);
+#undef NQ_FN
+        { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
+        int per_sm = 0;
+        SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, W * 32, bytes));
+        const void* fpre = (const void*)nq_srule_kernel;
+        const size_t pre_bytes = sizeof(double) * 4 * ((size_t)a.ns * a.nt * 3 + 2 * a.ns);   // 4 warps
+        { slb_status st_ = smem_optin(fpre); if (st_ != SLB_OK) return st_; }
+        int pre_per_sm = 0;
+        SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pre_per_sm, fpre, 128, pre_bytes));
+        for (int64_t c0 = g.off; c0 < g.off + g.cnt && r == SLB_OK; c0 += chunk) {
+            a.p0 = c0;
+            a.p1 = std::min<int64_t>(g.off + g.cnt, c0 + chunk);
+            const int64_t np = a.p1 - a.p0;
+            void* args[] = {(void*)&a, (void*)tb.get()};
+            const int64_t gpre = std::min<int64_t>((np + 3) / 4, (int64_t)num_sms() * std::max(1, pre_per_sm));
+            SLB_CUDA(cudaLaunchKernel(fpre, dim3((unsigned)gpre), dim3(128), args, pre_bytes, s));
+            ++g_launch_count;
+            r = check_launch("nq_srule_kernel");
+            if (r != SLB_OK) break;
+            SLB_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long), s));
+            const int64_t grid = std::min<int64_t>(np, (int64_t)num_sms() * std::max(1, per_sm));
+            SLB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(W * 32), args, bytes, s));
+            ++g_launch_count;
+            r = check_launch("nq_modal_kernel");
+        }
     }
     int h = 0;
     if (r == SLB_OK) {
@@ -1108,6 +1169,7 @@ slb_status nearquad_modal_run(slb_kernel kernel, int64_t n_trg, const double* x_
     cudaFreeAsync(work, s);
     cudaFreeAsync(a.pre, s);
     cudaFreeAsync(a.prow, s);
+    if (plist_d) cudaFreeAsync(plist_d, s);
     if (r == SLB_OK && h) {
         set_error("nearquad (modal): s sub-panel budget exceeded (target extremely close to an element)");
         r = SLB_ERR_UNSUPPORTED;

@@ -336,7 +336,7 @@ upsample_warp_kernel(int kind, int64_t n_panels, int ns, int nt, int ms, int mt,
 // shared-memory buffer), which leaves ~12 KB of shared memory per warp and 16 warps per SM; the coarse
 // density is still double-buffered by TMA bulk copies.
 
-template <int NS, int NT, int MS, int MT, int WARPS>
+template <int NS, int NT, int MS, int MT, int WARPS, int ORD>
 __global__ void __launch_bounds__(WARPS * 32)
 upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const double* __restrict__ sc_in,
                     const double* __restrict__ scale, double* __restrict__ dyn, double* __restrict__ copy_out,
@@ -393,6 +393,7 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
         const int64_t m0 = f_off ? f_off[p] : p * (int64_t)NOUT;
         // this lane's fine-node scales (2 adjacent nodes per output tile), loads in flight during the GEMMs
         double sc0[NA][NB], sc1[NA][NB];
+        if (ORD == 0)
 #pragma unroll
         for (int ta = 0; ta < NA; ++ta)
 #pragma unroll
@@ -414,6 +415,48 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
             for (int q = lane; q < NIN; q += 32) dst[q] = R[q];
         }
         // step 1: T1_c[i][b] = sum_j sigma[i][j][c] F[b][j], rows r = i NC + c
+        if constexpr (ORD == 1) {
+            // every fragment loaded before the first T1 store (the compiler cannot move shared loads across
+            // shared stores it cannot disambiguate): all ROWS8/8 x MTP/8 output tiles are independent DMMA chains
+            constexpr int NRT1 = ROWS8 / 8, NK1 = NTP / 4, NN1 = MTP / 8;
+            double av[NRT1][NK1], bv[NN1][NK1], d0[NRT1][NN1], d1[NRT1][NN1];
+#pragma unroll
+            for (int rt = 0; rt < NRT1; ++rt) {
+                const int r = rt * 8 + g;
+                const int rb = (r < ROWS) ? (r / NC) * NT * NC + (r % NC) : 0;
+#pragma unroll
+                for (int kk = 0; kk < NK1; ++kk) {
+                    const int j = kk * 4 + tq;
+                    av[rt][kk] = (r < ROWS && j < NT) ? R[rb + j * NC] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int nn = 0; nn < NN1; ++nn)
+#pragma unroll
+                for (int kk = 0; kk < NK1; ++kk) bv[nn][kk] = F[(nn * 8 + g) * LDF + kk * 4 + tq];
+#pragma unroll
+            for (int rt = 0; rt < NRT1; ++rt)
+#pragma unroll
+                for (int nn = 0; nn < NN1; ++nn) d0[rt][nn] = d1[rt][nn] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < NK1; ++kk)
+#pragma unroll
+                for (int rt = 0; rt < NRT1; ++rt)
+#pragma unroll
+                    for (int nn = 0; nn < NN1; ++nn) dmma_8x8x4(d0[rt][nn], d1[rt][nn], av[rt][kk], bv[nn][kk]);
+#pragma unroll
+            for (int rt = 0; rt < NRT1; ++rt) {
+                const int r = rt * 8 + g;
+                if (r < ROWS) {
+#pragma unroll
+                    for (int nn = 0; nn < NN1; ++nn) {
+                        double* T = T1 + ((r % NC) * NSP + r / NC) * LDT + nn * 8 + 2 * tq;
+                        T[0] = d0[rt][nn];
+                        T[1] = d1[rt][nn];
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int r0 = 0; r0 < ROWS8; r0 += 8) {
             const int r = r0 + g;
@@ -442,6 +485,63 @@ upsample_rec_kernel(int64_t n_panels, const double* __restrict__ mats, const dou
         }
         // step 2 + epilogue: records {g, 0} of two adjacent nodes per lane straight from the accumulators
         double2* D2 = reinterpret_cast<double2*>(dyn);
+        if constexpr (ORD == 1) {
+            // fine-theta tile outer: each T1 fragment feeds all NA fine-s tiles (NA x NC independent DMMA chains,
+            // a third of the T1 loads); this tile's scales are loaded first and land during the contraction
+#pragma unroll
+            for (int tb = 0; tb < NB; ++tb) {
+                const int b = tb * 8 + 2 * tq;
+                double s0[NA], s1[NA];
+#pragma unroll
+                for (int ta = 0; ta < NA; ++ta) {
+                    const int a = ta * 8 + g;
+                    if (a < MS && b < MT) {
+                        const double2 v = __ldg(reinterpret_cast<const double2*>(scale + m0 + a * MT + b));
+                        s0[ta] = v.x;
+                        s1[ta] = v.y;
+                    } else {
+                        s0[ta] = s1[ta] = 0.0;
+                    }
+                }
+                double d0[NA][NC], d1[NA][NC];
+#pragma unroll
+                for (int ta = 0; ta < NA; ++ta)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) d0[ta][c] = d1[ta][c] = 0.0;
+#pragma unroll
+                for (int k0 = 0; k0 < NSP; k0 += 4) {
+                    double bv[NC];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) bv[c] = T1[(c * NSP + k0 + tq) * LDT + tb * 8 + g];
+#pragma unroll
+                    for (int ta = 0; ta < NA; ++ta) {
+                        const double av = Ps[(ta * 8 + g) * LDP + k0 + tq];
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) dmma_8x8x4(d0[ta][c], d1[ta][c], av, bv[c]);
+                    }
+                }
+#pragma unroll
+                for (int ta = 0; ta < NA; ++ta) {
+                    const int a = ta * 8 + g;
+                    if (a < MS && b < MT) {
+                        const int64_t m = m0 + a * MT + b;
+                        if (dyn_mc) {
+                            double* o = dyn_mc + 4 * m;
+                            multimem_st2(o, s0[ta] * d0[ta][0], s0[ta] * d0[ta][1]);
+                            multimem_st2(o + 2, s0[ta] * d0[ta][2], 0.0);
+                            multimem_st2(o + 4, s1[ta] * d1[ta][0], s1[ta] * d1[ta][1]);
+                            multimem_st2(o + 6, s1[ta] * d1[ta][2], 0.0);
+                        } else {
+                            double2* o = D2 + 2 * m;
+                            o[0] = make_double2(s0[ta] * d0[ta][0], s0[ta] * d0[ta][1]);
+                            o[1] = make_double2(s0[ta] * d0[ta][2], 0.0);
+                            o[2] = make_double2(s1[ta] * d1[ta][0], s1[ta] * d1[ta][1]);
+                            o[3] = make_double2(s1[ta] * d1[ta][2], 0.0);
+                        }
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int ta = 0; ta < NA; ++ta) {
 #pragma unroll
@@ -496,14 +596,20 @@ static slb_status launch_rec(int64_t n_panels, const double* mats, const double*
                              double* dyn, double* copy_out, const int32_t* plist, const int64_t* c_off,
                              const int64_t* f_off, cudaStream_t s, double* dyn_mc) {
     const size_t bytes = rec_smem_bytes<NS, NT, MS, MT>(WARPS);
-    const void* fn = (const void*)upsample_rec_kernel<NS, NT, MS, MT, WARPS>;
+    static const int ord = [] { const char* e = getenv("SLB_UPS_ORD"); return (e && e[0] == '0') ? 0 : 1; }();
+    const void* fn = ord ? (const void*)upsample_rec_kernel<NS, NT, MS, MT, WARPS, 1>
+                         : (const void*)upsample_rec_kernel<NS, NT, MS, MT, WARPS, 0>;
     { slb_status st_ = smem_optin(fn); if (st_ != SLB_OK) return st_; }
     int per_sm = 0;
     SLB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, bytes));
     const unsigned grid = (unsigned)std::max<int64_t>(
         1, std::min<int64_t>((n_panels + WARPS - 1) / WARPS, (int64_t)num_sms() * std::max(1, per_sm)));
-    upsample_rec_kernel<NS, NT, MS, MT, WARPS><<<grid, WARPS * 32, bytes, s>>>(n_panels, mats, sc_in, scale, dyn,
-                                                                              copy_out, plist, c_off, f_off, dyn_mc);
+    if (ord)
+        upsample_rec_kernel<NS, NT, MS, MT, WARPS, 1><<<grid, WARPS * 32, bytes, s>>>(n_panels, mats, sc_in, scale, dyn,
+                                                                                     copy_out, plist, c_off, f_off, dyn_mc);
+    else
+        upsample_rec_kernel<NS, NT, MS, MT, WARPS, 0><<<grid, WARPS * 32, bytes, s>>>(n_panels, mats, sc_in, scale, dyn,
+                                                                                     copy_out, plist, c_off, f_off, dyn_mc);
     ++g_launch_count;
     return check_launch("upsample_rec_kernel");
 }
