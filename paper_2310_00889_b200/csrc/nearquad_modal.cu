@@ -46,6 +46,7 @@
 namespace slb {
 
 #include "nq_logrule.inc"
+#include "nq_chebrules.inc"
 
 namespace nqm {
 
@@ -923,7 +924,8 @@ struct RuleBuf {
 //   k >= 1 (alpha in [2^-k, 2^(1-k))): 16-point GL on panels [0, 2^-k], [2^-k, 2^(1-k)], ... up to pi,
 //     no panel longer than 16 / lmax (resolves e^{i lmax th}), mirrored to [-pi, 0].
 // Every rule is padded with zero-weight nodes to a multiple of kChunk.
-static void build_rules(int lmax, std::vector<double>& th, std::vector<double>& w, int* off, int* cnt) {
+static void build_rules(int cls, int lmax, std::vector<double>& th, std::vector<double>& w, int* off, int* cnt) {
+    static const bool composite = [] { const char* e = getenv("SLB_NQ_COMPOSITE"); return e && e[0] == '1'; }();
     double gx[kQa], gw[kQa];
     gl_nodes(kQa, gx, gw);
     auto pad = [&](int start) {
@@ -944,6 +946,21 @@ static void build_rules(int lmax, std::vector<double>& th, std::vector<double>& 
     }
     const double hcap = 16.0 / lmax;
     for (int k = 1; k <= kMaxK; ++k) {
+        if (!composite && k <= kChebK && c_cheb_rule[cls][k - 1][1] > 0) {
+            // the generalized Chebyshev rule of this class and bracket (App. B; tools/gen_cheb_rules.py), built on
+            // (0, pi) for the even integrands and mirrored
+            const int o = c_cheb_rule[cls][k - 1][0], n = c_cheb_rule[cls][k - 1][1];
+            const int start = (int)th.size();
+            off[kNTrap - 1 + k] = start;
+            for (int sgn = -1; sgn <= 1; sgn += 2)
+                for (int j = 0; j < n; ++j) {
+                    th.push_back(sgn * c_cheb_th[o + j]);
+                    w.push_back(c_cheb_w[o + j]);
+                }
+            pad(start);
+            cnt[kNTrap - 1 + k] = (int)th.size() - start;
+            continue;
+        }
         const double al = std::ldexp(1.0, -k);
         std::vector<double> e{0.0, al};
         while (e.back() * 2.0 < kPi) e.push_back(e.back() * 2.0);
@@ -980,7 +997,7 @@ static const RuleBuf* rules_for_class(int c) {
     if (it != cache.end()) return &it->second;
     RuleBuf rb;
     std::vector<double> th, w;
-    build_rules(lmax_of_class(c), th, w, rb.off, rb.cnt);
+    build_rules(c, lmax_of_class(c), th, w, rb.off, rb.cnt);
     // stored modes of every node ("precomputed and stored along with the quadrature rule")
     const int Lc = (c == 0 ? 12 : c == 1 ? 24 : c == 2 ? 40 : 64) / 2;
     rb.lde = (2 * (Lc + 1) + 7) / 8 * 8;
