@@ -275,6 +275,21 @@ def main():
     far_ms = st_mean[2]
     fin_ms = st_mean[3]
 
+    # the upsample (+projector) kernels alone: K back-to-back launches of apply stage 1 (slb_operator_prepare),
+    # CUDA events on the launching stream -- the kernels' own duration, without the in-apply stage events' launch
+    # gap (stage_ms keeps the in-apply figure)
+    barrier()
+    k_up = 50
+    u0 = torch.cuda.Event(enable_timing=True)
+    u1 = torch.cuda.Event(enable_timing=True)
+    dp.op.prepare(dp.sigma)
+    u0.record(stream)
+    for _ in range(k_up):
+        dp.op.prepare(dp.sigma)
+    u1.record(stream)
+    barrier()
+    up_kernel_ms = u0.elapsed_time(u1) / k_up
+
     # e2e through the public API with host buffers (H2D sigma, D2H u inside the timed region)
     no, fo = pr.node_off(), pr.fine_off()
     sig_h = torch.from_numpy(pr.sigma.reshape(pr.N, pr.sdim)[no[dp.pb]:no[dp.pe]].copy()).pin_memory()
@@ -349,9 +364,12 @@ def main():
                               "achieved": near_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": near_gbs / hbm_peak,
                               "bytes_per_launch": near_bytes, "launch_ms": fin_ms},
             "roofline_upsample": {"bound": "hbm", "kernel": "upsample_rec_kernel / upsample_warp_kernel (+ projector; DMMA m8n8k4, TMA-fed)",
-                                  "achieved": up_bytes / (st_mean[0] * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                                  "frac": up_bytes / (st_mean[0] * 1e-3) / 1e9 / hbm_peak,
-                                  "bytes_per_launch": up_bytes, "launch_ms": st_mean[0]},
+                                  "achieved": up_bytes / (up_kernel_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": up_bytes / (up_kernel_ms * 1e-3) / 1e9 / hbm_peak,
+                                  "bytes_per_launch": up_bytes, "launch_ms": up_kernel_ms,
+                                  "timing": "50 back-to-back launches of apply stage 1 (slb_operator_prepare), CUDA events",
+                                  "in_apply_stage_ms": st_mean[0],
+                                  "frac_in_apply_stage": up_bytes / (st_mean[0] * 1e-3) / 1e9 / hbm_peak},
             "stage_ms": {"projector_upsample": st_mean[0], "allgather": st_mean[1], "far": far_ms,
                          "finalize_near": fin_ms},
             "cpu_baseline": cpu_base,

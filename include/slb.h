@@ -258,6 +258,13 @@ slb_status slb_matvec(slb_operator* op, const double* sigma_local, double* u_loc
 slb_status slb_matvec_host(slb_operator* op, const double* sigma_local_host, double* u_local_host,
                            cudaStream_t s);
 
+/* Stage 1 of an apply alone: the projector (mobility operators) and
+ * the upsample of sigma_local into the operator's fine source records, exactly the kernels slb_matvec
+ * launches first; nothing else (no gather, far field or finalize).  For per-kernel timing (bench.py's
+ * upsample roofline); the records it writes are the next apply's inputs, so it leaves the operator valid.
+ * Errors: SLB_ERR_INVALID_ARG (null operator, null density with local nodes), SLB_ERR_CUDA. */
+slb_status slb_operator_prepare(slb_operator* op, const double* sigma_local, cudaStream_t s);
+
 /* Stage timing of the last slb_matvec (ms, CUDA events on s; -1 if unavailable):
  * [0] projector+upsample, [1] all-gather, [2] far field, [3] finalize (reduce+near+identity). */
 slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]);

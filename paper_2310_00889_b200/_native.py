@@ -52,6 +52,7 @@ _SIGS = {
     "slb_matvec": (I32, [P, P, P, P]),
     "slb_matvec_host": (I32, [P, P, P, P]),
     "slb_operator_last_timings": (I32, [P, ctypes.POINTER(ctypes.c_float)]),
+    "slb_operator_prepare": (I32, [P, P, P]),
     "slb_operator_launches_per_matvec": (I32, [P]),
     "slb_operator_nvls": (I32, [P]),
     "slb_nvls_supported": (I32, []),

@@ -300,6 +300,10 @@ class Operator:
                                        ctypes.byref(rr), _stream()))
         return rig, x, it.value, rr.value
 
+    def prepare(self, sigma_local):
+        """Stage 1 of an apply alone (projector + upsample into the fine records), for kernel timing."""
+        check(lib().slb_operator_prepare(self.h, _dev(sigma_local, "sigma"), _stream()))
+
     def timings(self):
         arr = (ctypes.c_float * 4)()
         check(lib().slb_operator_last_timings(self.h, arr))

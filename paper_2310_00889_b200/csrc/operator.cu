@@ -481,19 +481,16 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
 
 }  // extern "C"
 
-// The apply itself.  captured: being recorded into the operator's whole-apply graph (the stage events
-// become event-record nodes; the constant-bank tiles are recorded inline and the bank lock is taken by
-// the caller around the graph launch).
-static slb_status matvec_body(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s,
-                              bool captured) {
+// Stage 1 of an apply: the projector (mobility operators) and the upsample of the local panels into the
+// fine source records (op->dyn at the rank's offset).  Returns where the later stages read sigma'.
+struct PrepOut {
+    const double* near_sig;
+    const double* id_sig;
+    const double* Lsig;
+};
+static slb_status prep_stage(slb_operator* op, const double* sigma_local, cudaStream_t s, PrepOut* po) {
     const slb_operator_desc& d = op->d;
-    auto rec_ev = [&](int q) {
-        return captured ? cudaEventRecordWithFlags(op->ev[q], s, cudaEventRecordExternal) : cudaEventRecord(op->ev[q], s);
-    };
-    unsigned long long* zc = coincident_counter();
-    SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
     slb_status st;
-    SLB_CUDA(rec_ev(0));
     // local sigma' inside the global coarse buffer.  One GPU without the projector: the caller's sigma IS
     // sigma' and the finalize reads it in place (no copy).  With a communicator the upsample writes the
     // staged density into the global buffer as it reads it (fused copy), the projector writes sigma' there.
@@ -545,6 +542,31 @@ static slb_status matvec_body(slb_operator* op, const double* sigma_local, doubl
                              op->nvls_on ? op->dyn_mc + d.panel_begin * op->Mn * 4 : nullptr);
         if (st != SLB_OK) return st;
     }
+    po->near_sig = near_sig;
+    po->id_sig = id_sig;
+    po->Lsig = Lsig;
+    return SLB_OK;
+}
+
+// The apply itself.  captured: being recorded into the operator's whole-apply graph (the stage events
+// become event-record nodes; the constant-bank tiles are recorded inline and the bank lock is taken by
+// the caller around the graph launch).
+static slb_status matvec_body(slb_operator* op, const double* sigma_local, double* u_local, cudaStream_t s,
+                              bool captured) {
+    const slb_operator_desc& d = op->d;
+    auto rec_ev = [&](int q) {
+        return captured ? cudaEventRecordWithFlags(op->ev[q], s, cudaEventRecordExternal) : cudaEventRecord(op->ev[q], s);
+    };
+    unsigned long long* zc = coincident_counter();
+    SLB_REQUIRE(zc, SLB_ERR_CUDA, "coincident counter allocation failed");
+    slb_status st;
+    SLB_CUDA(rec_ev(0));
+    PrepOut po;
+    st = prep_stage(op, sigma_local, s, &po);
+    if (st != SLB_OK) return st;
+    const double* near_sig = po.near_sig;
+    const double* id_sig = po.id_sig;
+    const double* Lsig = po.Lsig;
     SLB_CUDA(rec_ev(1));
     if (op->nvls_on) {
         // the records reached every rank's copy through the multicast stores; a barrier makes sure all
@@ -685,6 +707,14 @@ slb_status slb_matvec_host(slb_operator* op, const double* sigma_host, double* u
                              cudaMemcpyDeviceToHost, s));
     SLB_CUDA(cudaStreamSynchronize(s));
     return SLB_OK;
+}
+
+slb_status slb_operator_prepare(slb_operator* op, const double* sigma_local, cudaStream_t s) {
+    SLB_REQUIRE(op, SLB_ERR_INVALID_ARG, "null operator");
+    SLB_REQUIRE(op->N_loc == 0 || sigma_local, SLB_ERR_INVALID_ARG, "null density");
+    SLB_REQUIRE(check_sticky("slb_operator_prepare") == SLB_OK, SLB_ERR_CUDA, slb_last_error());
+    PrepOut po;
+    return prep_stage(op, sigma_local, s, &po);
 }
 
 slb_status slb_operator_last_timings(slb_operator* op, float out_ms[4]) {
