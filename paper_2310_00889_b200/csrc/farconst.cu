@@ -129,6 +129,78 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
     }
 }
 
+// Variant with fewer NON-FP64 instructions per pair (the FP64 count stays 27): source record read as
+// five 16-byte constant loads, the coincident-pair select applied to the high word of the MUFU seed
+// only (its low word is zero), coincident pairs detected through a running minimum of r2's high word
+// and recounted exactly after the loop (rare).
+template <int J>
+__device__ __forceinline__ void const_pairs_lean(const double (&x)[J][3], const double2* s, double (&acc)[J][3],
+                                                 unsigned& mn) {
+    const double2 q0 = s[0], q1 = s[1], q2 = s[2], q3 = s[3], q4 = s[4];
+    const double y_0 = q0.x, y_1 = q0.y, y_2 = q1.x, a0 = q1.y, a1 = q2.x, a2 = q2.y, g0 = q3.x, g1 = q3.y, g2 = q4.x;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const double rx = x[j][0] - y_0, ry = x[j][1] - y_1, rz = x[j][2] - y_2;
+        const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
+        const unsigned hi = (unsigned)__double2hiint(r2);
+        int yh = __double2hiint(rsqrt_mufu(r2));
+        yh = hi ? yh : 0;                               // coincident pair (R14): seed 0 -> rinv = 0
+        mn = min(mn, hi);
+        const double y0 = __hiloint2double(yh, 0);
+        const double e = fma(-r2, y0 * y0, 1.0);
+        const double h = e * fma(e, 0.375, 0.5);
+        const double rinv = fma(y0, h, y0);
+        const double s2 = rinv * rinv;
+        const double rg = fma(rx, g0, fma(ry, g1, rz * g2));
+        const double ra = fma(rx, a0, fma(ry, a1, rz * a2));
+        const double c = (rg * s2) * fma(ra, s2, 1.0);
+        acc[j][0] = fma(rinv, fma(c, rx, g0), acc[j][0]);
+        acc[j][1] = fma(rinv, fma(c, ry, g1), acc[j][1]);
+        acc[j][2] = fma(rinv, fma(c, rz, g2), acc[j][2]);
+    }
+}
+
+template <int J, int BUF, int UNR, int MINB>
+__global__ void __launch_bounds__(kConstThreads, MINB)
+far_const_lean_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
+                      double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
+    double x[J][3], acc[J][3];
+    bool valid[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int64_t t = (int64_t)blockIdx.x * kConstThreads * J + threadIdx.x + kConstThreads * j;
+        valid[j] = t < T;
+        const int64_t tc = valid[j] ? t : T - 1;
+        x[j][0] = x_trg[3 * tc]; x[j][1] = x_trg[3 * tc + 1]; x[j][2] = x_trg[3 * tc + 2];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[j][q] = first ? 0.0 : partial[tc * 3 + q];
+    }
+    unsigned mn = 0xffffffffu;
+    const double* base = c_rec + BUF * kSlot;
+    const double2* b2 = reinterpret_cast<const double2*>(base);
+#pragma unroll UNR
+    for (int m = 0; m < n_src; ++m) const_pairs_lean<J>(x, b2 + (kRec / 2) * m, acc, mn);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int64_t t = (int64_t)blockIdx.x * kConstThreads * J + threadIdx.x + kConstThreads * j;
+        if (valid[j]) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) partial[t * 3 + q] = acc[j][q];
+        }
+    }
+    if (mn == 0) {   // some pair of this thread was coincident: count exactly (valid targets only)
+        unsigned long long zc = 0;
+        for (int m = 0; m < n_src; ++m)
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const double rx = x[j][0] - base[kRec * m], ry = x[j][1] - base[kRec * m + 1],
+                             rz = x[j][2] - base[kRec * m + 2];
+                zc += (valid[j] && is_zero_r2(fma(rx, rx, fma(ry, ry, rz * rz)))) ? 1 : 0;
+            }
+        if (zc) atomicAdd(coincident, zc);
+    }
+}
+
 // rec[m] = {geo[m][0..5], dyn[m][0..2], 0}
 __global__ void pack_rec_kernel(int64_t M, const double* __restrict__ geo, const double* __restrict__ dyn,
                                 double* __restrict__ rec) {
@@ -174,6 +246,8 @@ static void launch_tile(int64_t T, const double* x, int n, int first, double* pa
             case 2: launch_tile_v<KIND, BUF, 2, 8, 4>(T, x, n, first, part, zc, s); return;
             case 3: launch_tile_v<KIND, BUF, 3, 2, 3>(T, x, n, first, part, zc, s); return;
             case 4: launch_tile_v<KIND, BUF, 1, 8, 8>(T, x, n, first, part, zc, s); return;
+            case 6: far_const_lean_kernel<2, BUF, 4, 4><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc); return;
+            case 7: far_const_lean_kernel<2, BUF, 2, 4><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc); return;
             default: launch_tile_v<KIND, BUF, 4, 1, 2>(T, x, n, first, part, zc, s); return;
         }
     }

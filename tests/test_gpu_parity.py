@@ -266,6 +266,22 @@ def test_const_path_fewer_tiles_than_buffers(S, monkeypatch):
     assert err <= TOL, err
 
 
+def test_const_path_coincident_pairs(S, monkeypatch):
+    """r = 0 pairs on the constant-bank far path (R14): contribute 0, are counted, parity holds."""
+    monkeypatch.setenv("SLB_FAR_PATH", "const")
+    pr = make_config("c2", panels=4)
+    pr.x_trg = pr.x_trg.copy()
+    far_src = [int(np.argmax(np.linalg.norm(pr.y_f - pr.x_trg[t], axis=1))) for t in (7, 300)]
+    pr.x_trg[7] = pr.y_f[far_src[0]]          # two targets moved onto far fine sources
+    pr.x_trg[300] = pr.y_f[far_src[1]]
+    S.slb_coincident_reset()
+    err, u, u2 = _matvec_vs_oracle(S, pr)
+    assert err <= TOL, err
+    assert np.array_equal(u, u2)
+    assert S.slb_coincident_count() >= 4      # 2 pairs x 2 applies (more if a moved target is near-listed)
+    S.slb_coincident_reset()
+
+
 def test_operator_rejects_bad_csr(S):
     from paper_2310_00889_b200 import Operator, SlbError
     pr = make_config("c2", panels=4)
