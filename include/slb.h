@@ -84,7 +84,11 @@ const char* slb_last_error(void);
 double slb_eta_cfie(double rho);
 
 /* Number of coincident (r == 0) target/source pairs skipped by far-field launches since
- * the last reset (device counter; synchronises the device).  R14. */
+ * the last reset (device counter; synchronises the device).  R14.
+ * Operators on the constant-bank far path (M >= 2^16) decide once, at slb_operator_create, whether
+ * any such pair exists between their targets and sources (one extra far-field pass with zero
+ * strengths, not counted here); if none does, their applies run kernels without the r == 0 test --
+ * same results bit for bit, nothing to count.  SLB_CONST_PRESCAN=0 keeps the test in every apply. */
 long long slb_coincident_count(void);
 void slb_coincident_reset(void);
 

@@ -175,7 +175,9 @@ unsigned long long* coincident_counter();
 // ---- constant-bank far field (farconst.cu) ----
 slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
                            double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
-                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches);
+                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches, bool check = true);
+// check = false: the kernels without the r = 0 select and count -- only for operators whose create-time
+// prescan found no coincident (target, source) pair (bitwise-identical results in that case)
 slb_status pack_rec_launch(int64_t M, const double* geo, const double* dyn, double* rec, cudaStream_t s);
 int far_const_bufs(int64_t M);   // streams / partial arrays for M sources
 // Scoped host lock + device event chain serialising all users of the constant bank (farconst.cu).

@@ -35,7 +35,7 @@ __constant__ double c_rec[kConstRecs * kRec];
 // with 4 x 200) -- twice the launches and copies cost more than the better SM fill gains.
 static int const_bufs_for(int64_t M) { (void)M; return 4; }
 
-template <int KIND, int J, int CM>
+template <int KIND, int J, int CM, int ORD = 3>
 __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const double* s, double (&acc)[J][3],
                                             bool& anyz, unsigned& zc) {
 #pragma unroll
@@ -44,12 +44,19 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
         const double r2 = fma(rx, rx, fma(ry, ry, rz * rz));
         const double y0 = rsqrt_mufu(r2);
         const double e = fma(-r2, y0 * y0, 1.0);
-        const double h = e * fma(e, 0.375, 0.5);
+        double h;
+        if constexpr (ORD == 3) h = e * fma(e, 0.375, 0.5);
+        else if constexpr (ORD == 4) {                 // cubic term (~2^-46 y0) in FP32: one FP64 instruction fewer
+            const float ef = __double2float_rn(e);
+            h = fma(e, 0.5, (double)(0.375f * ef * ef));
+        } else h = 0.5 * e;                            // ORD 2: measurement only (error ~3/8 e^2 ~ 2e-14)
         double rinv = fma(y0, h, y0);                  // y0 (1 + e/2 + 3e^2/8)
-        const bool z = is_zero_r2(r2);
-        rinv = z ? 0.0 : rinv;
-        if (CM == 0) anyz |= z;                        // rare: exact recount after the loop
-        else zc += z;
+        if constexpr (CM != 2) {                       // CM 2: no coincident-pair handling (measurement only)
+            const bool z = is_zero_r2(r2);
+            rinv = z ? 0.0 : rinv;
+            if (CM == 0) anyz |= z;                    // rare: exact recount after the loop
+            else zc += z;
+        }
         if constexpr (KIND == FAR_STOKES_SLDL) {
             // u += rinv (g + c r),  c = (r.g) rinv^2 (1 + (r.a) rinv^2)
             const double s2 = rinv * rinv;
@@ -80,7 +87,7 @@ __device__ __forceinline__ void const_pairs(const double (&x)[J][3], const doubl
     }
 }
 
-template <int KIND, int J, int BUF, int CM, int UNR = 4, int MINB = 4>
+template <int KIND, int J, int BUF, int CM, int UNR = 4, int MINB = 4, int ORD = 3>
 __global__ void __launch_bounds__(kConstThreads, MINB)
 far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int first,
                  double* __restrict__ partial, unsigned long long* __restrict__ coincident) {
@@ -100,7 +107,7 @@ far_const_kernel(int64_t T, const double* __restrict__ x_trg, int n_src, int fir
     unsigned zc0 = 0;
     const double* base = c_rec + BUF * kSlot;     // BUF: buffer offset in eighths of the bank
 #pragma unroll UNR
-    for (int m = 0; m < n_src; ++m) const_pairs<KIND, J, CM>(x, base + kRec * m, acc, anyz, zc0);
+    for (int m = 0; m < n_src; ++m) const_pairs<KIND, J, CM, ORD>(x, base + kRec * m, acc, anyz, zc0);
     if (CM == 1 && zc0) {
         bool any = false;
 #pragma unroll
@@ -229,23 +236,33 @@ static int const_variant() {
     return v;
 }
 
-template <int KIND, int BUF, int J, int UNR, int MINB>
+template <int KIND, int BUF, int J, int UNR, int MINB, int CM = 1, int ORD = 3>
 static void launch_tile_v(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
                           cudaStream_t s) {
     const unsigned grid = (unsigned)((T + kConstThreads * J - 1) / (kConstThreads * J));
-    far_const_kernel<KIND, J, BUF, 1, UNR, MINB><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+    far_const_kernel<KIND, J, BUF, CM, UNR, MINB, ORD><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
 }
 
 template <int KIND, int BUF>
 static void launch_tile(int64_t T, const double* x, int n, int first, double* part, unsigned long long* zc,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool check) {
     const unsigned grid = (unsigned)((T + kConstThreads * kJ - 1) / (kConstThreads * kJ));
+    if (!check) {
+        far_const_kernel<KIND, kJ, BUF, 2><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc);
+        return;
+    }
     if (KIND == FAR_STOKES_SLDL && const_variant() != 0) {
         switch (const_variant()) {
             case 1: launch_tile_v<KIND, BUF, 2, 2, 4>(T, x, n, first, part, zc, s); return;
             case 2: launch_tile_v<KIND, BUF, 2, 8, 4>(T, x, n, first, part, zc, s); return;
             case 3: launch_tile_v<KIND, BUF, 3, 2, 3>(T, x, n, first, part, zc, s); return;
             case 4: launch_tile_v<KIND, BUF, 1, 8, 8>(T, x, n, first, part, zc, s); return;
+            case 8: launch_tile_v<KIND, BUF, 2, 4, 4, 2, 3>(T, x, n, first, part, zc, s); return;   // no r = 0 handling
+            case 9: launch_tile_v<KIND, BUF, 2, 4, 4, 2, 2>(T, x, n, first, part, zc, s); return;   // + 2nd-order rsqrt
+            case 10: launch_tile_v<KIND, BUF, 2, 4, 4, 1, 2>(T, x, n, first, part, zc, s); return;  // 2nd-order rsqrt only
+            case 12: launch_tile_v<KIND, BUF, 2, 4, 4, 1, 4>(T, x, n, first, part, zc, s); return;  // FP32 cubic term
+            case 13: launch_tile_v<KIND, BUF, 2, 4, 4, 2, 4>(T, x, n, first, part, zc, s); return;  // + no r = 0 handling
+            case 11: launch_tile_v<KIND, BUF, 2, 4, 5>(T, x, n, first, part, zc, s); return;         // 5 CTAs/SM (<= 102 regs)
             case 6: far_const_lean_kernel<2, BUF, 4, 4><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc); return;
             case 7: far_const_lean_kernel<2, BUF, 2, 4><<<grid, kConstThreads, 0, s>>>(T, x, n, first, part, zc); return;
             default: launch_tile_v<KIND, BUF, 4, 1, 2>(T, x, n, first, part, zc, s); return;
@@ -259,16 +276,16 @@ static void launch_tile(int64_t T, const double* x, int n, int first, double* pa
 
 template <int KIND>
 static void launch_tile_buf(int slot, int64_t T, const double* x, int n, int first, double* part,
-                            unsigned long long* zc, cudaStream_t s) {
+                            unsigned long long* zc, cudaStream_t s, bool check) {
     switch (slot) {
-        case 0: launch_tile<KIND, 0>(T, x, n, first, part, zc, s); break;
-        case 1: launch_tile<KIND, 1>(T, x, n, first, part, zc, s); break;
-        case 2: launch_tile<KIND, 2>(T, x, n, first, part, zc, s); break;
-        case 3: launch_tile<KIND, 3>(T, x, n, first, part, zc, s); break;
-        case 4: launch_tile<KIND, 4>(T, x, n, first, part, zc, s); break;
-        case 5: launch_tile<KIND, 5>(T, x, n, first, part, zc, s); break;
-        case 6: launch_tile<KIND, 6>(T, x, n, first, part, zc, s); break;
-        default: launch_tile<KIND, 7>(T, x, n, first, part, zc, s); break;
+        case 0: launch_tile<KIND, 0>(T, x, n, first, part, zc, s, check); break;
+        case 1: launch_tile<KIND, 1>(T, x, n, first, part, zc, s, check); break;
+        case 2: launch_tile<KIND, 2>(T, x, n, first, part, zc, s, check); break;
+        case 3: launch_tile<KIND, 3>(T, x, n, first, part, zc, s, check); break;
+        case 4: launch_tile<KIND, 4>(T, x, n, first, part, zc, s, check); break;
+        case 5: launch_tile<KIND, 5>(T, x, n, first, part, zc, s, check); break;
+        case 6: launch_tile<KIND, 6>(T, x, n, first, part, zc, s, check); break;
+        default: launch_tile<KIND, 7>(T, x, n, first, part, zc, s, check); break;
     }
 }
 
@@ -276,7 +293,7 @@ static void launch_tile_buf(int slot, int64_t T, const double* x, int n, int fir
 // partials: [nb][T][D].  Returns the number of kernel launches issued.
 slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, const double* rec,
                            double* partials, unsigned long long* zc, cudaStream_t s, cudaStream_t* ws,
-                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches) {
+                           cudaEvent_t fork, cudaEvent_t* join, int64_t* launches, bool check) {
     const int D = far_scalar(kind) ? 1 : 3;
     const int nb = const_bufs_for(M);
     const int tile = kConstRecs / nb;                // 200 or 100 records per buffer
@@ -299,10 +316,10 @@ slb_status far_const_issue(FarKind kind, int64_t M, int64_t T, const double* x, 
             double* part = partials + (int64_t)b * T * D;
             const int first = (i < nb) ? 1 : 0;
             switch (kind) {
-                case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
-                case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
-                case FAR_LAPLACE_SLDL: launch_tile_buf<FAR_LAPLACE_SLDL>(b * stride, T, x, n, first, part, zc, ws[b]); break;
-                default: launch_tile_buf<FAR_LAPLACE>(b * stride, T, x, n, first, part, zc, ws[b]); break;
+                case FAR_STOKES_SLDL: launch_tile_buf<FAR_STOKES_SLDL>(b * stride, T, x, n, first, part, zc, ws[b], check); break;
+                case FAR_STOKES_DL: launch_tile_buf<FAR_STOKES_DL>(b * stride, T, x, n, first, part, zc, ws[b], check); break;
+                case FAR_LAPLACE_SLDL: launch_tile_buf<FAR_LAPLACE_SLDL>(b * stride, T, x, n, first, part, zc, ws[b], check); break;
+                default: launch_tile_buf<FAR_LAPLACE>(b * stride, T, x, n, first, part, zc, ws[b], check); break;
             }
             ++*launches;
         }
@@ -367,7 +384,7 @@ slb_status far_const_prepare() {
     SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 5, C>));                 \
     SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 6, C>));                 \
     SLB_CUDA(cudaFuncGetAttributes(&fa, far_const_kernel<K, kJ, 7, C>));
-#define PREP(K) PREP1(K, 0) PREP1(K, 1)
+#define PREP(K) PREP1(K, 0) PREP1(K, 1) PREP1(K, 2)
     PREP(FAR_STOKES_SLDL)
     PREP(FAR_STOKES_DL)
     PREP(FAR_LAPLACE)

@@ -451,6 +451,39 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         for (auto& e : op->join) OPCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         OPST(far_const_prepare());
         OPCUDA(cudaDeviceSynchronize());
+        // Coincident-pair prescan (R14).  Targets and sources are fixed per operator, so whether any r = 0
+        // pair exists is decided once: one checked far pass with zero strengths (dyn = 0 here) counts this
+        // rank's pairs into a private counter.  With none, every apply uses the kernels without the select
+        // and count (1.2 % faster on c4, bitwise-identical results); otherwise the checked kernels as before.
+        static const bool prescan = [] { const char* e = getenv("SLB_CONST_PRESCAN"); return !(e && e[0] == '0'); }();
+        if (prescan && T > 0) {
+            unsigned long long* cnt = nullptr;
+            OPCUDA(cudaMalloc(&cnt, sizeof(unsigned long long)));
+            cudaStream_t ps = nullptr;
+            cudaError_t pe = cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking);
+            slb_status st = (pe == cudaSuccess) ? SLB_OK : SLB_ERR_CUDA;
+            if (st == SLB_OK && cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), ps) != cudaSuccess) st = SLB_ERR_CUDA;
+            if (st == SLB_OK) st = pack_rec_launch(op->M, op->geo, op->dyn, op->rec, ps);
+            if (st == SLB_OK) {
+                ConstBankLock bank;
+                st = bank.acquire(ps);
+                int64_t nl = 0;
+                if (st == SLB_OK)
+                    st = far_const_issue(op->kind, op->M, T, d->x_trg, op->rec, op->partials, cnt, ps, op->ws, op->fork,
+                                         op->join, &nl, true);
+                g_launch_count += (unsigned long long)nl;
+                if (st == SLB_OK) st = bank.release(ps);
+            }
+            unsigned long long h = 1;
+            if (st == SLB_OK && (cudaStreamSynchronize(ps) != cudaSuccess ||
+                                 cudaMemcpy(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess))
+                st = SLB_ERR_CUDA;
+            if (ps) cudaStreamDestroy(ps);
+            cudaFree(cnt);
+            OPST(st);
+            op->prescan_pairs = h;
+            op->far_check = (h != 0);
+        }
         // capture the tile sequence once; if capture is not possible, slb_matvec issues it directly
         cudaStream_t cs = nullptr;
         OPCUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -458,7 +491,7 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
         if (ok) {
             slb_status st = far_const_issue(op->kind, op->M, T, d->x_trg, op->rec, op->partials, coincident_counter(),
-                                            cs, op->ws, op->fork, op->join, &op->const_launches);
+                                            cs, op->ws, op->fork, op->join, &op->const_launches, op->far_check);
             cudaError_t e1 = cudaStreamEndCapture(cs, &g);
             ok = (st == SLB_OK && e1 == cudaSuccess && g != nullptr);
             if (ok) ok = cudaGraphInstantiate(&op->graph, g, 0) == cudaSuccess;
@@ -589,7 +622,7 @@ static slb_status matvec_body(slb_operator* op, const double* sigma_local, doubl
         if (captured) {                            // tiles recorded inline; the caller holds the bank lock
             int64_t nl = 0;
             st = far_const_issue(op->kind, op->M, d.n_trg_local, d.x_trg, op->rec, op->partials, zc, s, op->ws,
-                                 op->fork, op->join, &nl);
+                                 op->fork, op->join, &nl, op->far_check);
             if (st != SLB_OK) return st;
             g_launch_count += (unsigned long long)nl;
         } else {
@@ -602,7 +635,7 @@ static slb_status matvec_body(slb_operator* op, const double* sigma_local, doubl
             } else {
                 int64_t nl = 0;
                 st = far_const_issue(op->kind, op->M, d.n_trg_local, d.x_trg, op->rec, op->partials, zc, s, op->ws,
-                                     op->fork, op->join, &nl);
+                                     op->fork, op->join, &nl, op->far_check);
                 if (st != SLB_OK) return st;
                 g_launch_count += (unsigned long long)nl;
             }

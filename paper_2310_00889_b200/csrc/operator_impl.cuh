@@ -118,6 +118,8 @@ struct slb_operator {
     cudaEvent_t fork = nullptr, join[8] = {};
     cudaGraphExec_t graph = nullptr;
     int64_t const_launches = 0;
+    bool far_check = true;              // false: create-time prescan found no r = 0 pair (R14) -> unchecked kernels
+    unsigned long long prescan_pairs = 0;
     int near_G = 1;                     // targets per warp in the near stream kernel
     // ragged angular orders (NEXT N4): per-(nt, mt) buckets; all empty / NULL for uniform panels
     bool ragged = false;
