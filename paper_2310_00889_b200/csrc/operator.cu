@@ -455,7 +455,8 @@ slb_status slb_operator_create(const slb_operator_desc* d, slb_comm* comm, slb_o
         // pair exists is decided once: one checked far pass with zero strengths (dyn = 0 here) counts this
         // rank's pairs into a private counter.  With none, every apply uses the kernels without the select
         // and count (1.2 % faster on c4, bitwise-identical results); otherwise the checked kernels as before.
-        static const bool prescan = [] { const char* e = getenv("SLB_CONST_PRESCAN"); return !(e && e[0] == '0'); }();
+        const char* pe_env = getenv("SLB_CONST_PRESCAN");      // read per create (tests toggle it)
+        const bool prescan = !(pe_env && pe_env[0] == '0');
         if (prescan && T > 0) {
             unsigned long long* cnt = nullptr;
             OPCUDA(cudaMalloc(&cnt, sizeof(unsigned long long)));

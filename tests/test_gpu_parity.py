@@ -282,6 +282,23 @@ def test_const_path_coincident_pairs(S, monkeypatch):
     S.slb_coincident_reset()
 
 
+def test_const_path_prescan_is_bitwise_neutral(S, monkeypatch):
+    """Create-time coincident-pair prescan: without r = 0 pairs the applies use the unchecked far kernels;
+    results are bit for bit those of the checked kernels (SLB_CONST_PRESCAN=0), and nothing is counted."""
+    from harness import DeviceProblem
+    monkeypatch.setenv("SLB_FAR_PATH", "const")
+    pr = make_config("c4", n_loops=2, panels=8)
+    out = {}
+    S.slb_coincident_reset()
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SLB_CONST_PRESCAN", flag)
+        dp = DeviceProblem(pr)
+        out[flag] = dp.matvec().cpu().numpy()
+        dp.close()
+    assert np.array_equal(out["1"], out["0"])
+    assert S.slb_coincident_count() == 0
+
+
 def test_operator_rejects_bad_csr(S):
     from paper_2310_00889_b200 import Operator, SlbError
     pr = make_config("c2", panels=4)
